@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""Benchmark: hybrid SpMM GFLOP/s (2*nnz*N/t) and % of the HBM roofline on B200.
+
+Default workload (BASELINE.json configs[1], "C2"): synthetic Reddit-shaped power-law
+graph (n = 232,965, ~114.6M directed edges + self loops, gcn-normalised), feature
+dim 128, bf16 operands, fp32 accumulation, hybrid tensor-core / CUDA-core SpMM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--dim D] [--impl ours|reference]
+
+One step = one hybrid SpMM of the whole graph with inputs resident in HBM.  The
+CSR stream (0.69 GB) is larger than L2, so no explicit flush is needed.  Timing:
+CUDA events on the launching stream, barrier + synchronize around the timed
+region, max over ranks.  For N > 1 the row windows are sharded across ranks
+(contiguous ranges balanced by nnz) and each step ends with an NCCL all-gather of
+the output rows (the exchange between GCN layers), i.e. strong scaling.
+
+--impl reference times the reference's CPU algorithm (oracle/ restatement of
+rowwin partition + classify + spmm_hybrid, float32) on the host cores over a
+bounded window sample of the same graph.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--dim", type=int, default=128)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", choices=["c2", "c1", "c5"], default="c2")
+    p.add_argument("--precision", default="bf16")
+    p.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU-baseline sampling")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--sweep-dims", action="store_true", help="also report dims 32/64/128")
+    p.add_argument("--seed", type=int, default=0)
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clock/throttle sampling during the timed region."""
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.25)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def make_graph(cfg: str, seed: int):
+    from paper_2412_08902_b200 import graphgen
+    from paper_2412_08902_b200.gnn import normalize_adj
+
+    if cfg == "c2":
+        adj = graphgen.reddit_shaped(seed=seed)
+        name = "C2 reddit-shaped power law (Chung-Lu gamma=2.3), gcn-normalised"
+    elif cfg == "c1":
+        adj = graphgen.cora_shaped(seed=seed)
+        name = "C1 cora-shaped power law, gcn-normalised"
+    else:
+        adj = graphgen.rmat(24, 33, seed=seed)
+        name = "C5 R-MAT scale 24 ef 33 (0.57,0.19,0.19,0.05), gcn-normalised"
+    adj.symmetric = True
+    return adj, normalize_adj(adj, "gcn"), name
+
+
+def shard_rows(a, world, rank, wh=16):
+    """Contiguous window range of this rank, balanced by nnz (window boundaries)."""
+    from paper_2412_08902_b200.shard import shard_window_ranges, row_slice
+
+    ranges = shard_window_ranges(a.row_ptr, a.num_rows, world, wh)
+    w0, w1 = ranges[rank]
+    return row_slice(a, w0 * wh, min(w1 * wh, a.num_rows)), ranges
+
+
+# ----------------------------------------------------------------------------- ours
+def run_ours(args):
+    import paper_2412_08902_b200 as hc
+    from paper_2412_08902_b200 import _lib, graphgen
+    from paper_2412_08902_b200.executors import DeviceOperand, get_plan
+
+    world, rank, local = dist_setup(args)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    t0 = time.perf_counter()
+    adj, a, wl_name = make_graph(args.config, args.seed)
+    torch.cuda.synchronize()
+    t_gen = time.perf_counter() - t0
+    n, nnz = a.num_rows, a.nnz
+    if world > 1:
+        local_a, ranges = shard_rows(a, world, rank)
+    else:
+        local_a, ranges = a, [(0, -(-n // 16))]
+    # ---- preprocessing (K1 partition + selector, K2 plan), timed separately
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    ws = hc.partition(local_a)
+    asg = hc.classify_windows(hc.default_model(), ws)
+    ev1.record()
+    torch.cuda.synchronize()
+    t_partition_ms = ev0.elapsed_time(ev1)
+    ev0.record()
+    plan = get_plan(ws, asg, args.precision)
+    ev1.record()
+    torch.cuda.synchronize()
+    t_plan_ms = ev0.elapsed_time(ev1)
+    ncols = ws.ncols()
+    sum_ncols = int(ncols.sum())
+    codes = ws.codes
+
+    def measure(dim, steps, warmup, with_e2e):
+        x = graphgen.dense_features(n, dim, seed=1)
+        xop = DeviceOperand(x, dim, dim, _lib.DTYPE_BF16)
+        ldz = -(-dim // 4) * 4
+        z = torch.empty((local_a.num_rows, ldz), dtype=torch.float32, device=dev)
+        if world > 1:
+            import torch.distributed as dist
+
+            rows_per = [min(r[1] * 16, n) - r[0] * 16 for r in ranges]
+            maxrows = max(rows_per)
+            send = torch.zeros((maxrows, ldz), dtype=torch.float32, device=dev)
+            gathered = torch.empty((world * maxrows, ldz), dtype=torch.float32, device=dev)
+        tev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+
+        def step(i=None):
+            plan.run(xop, z, ldz, tile_events=tev[i] if i is not None else None)
+            if world > 1:
+                send[: z.shape[0]].copy_(z)
+                dist.all_gather_into_tensor(gathered, send)
+
+        for _ in range(warmup):
+            step()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        sampler = ClockSampler(local)
+        with sampler:
+            s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s_ev.record()
+            for i in range(steps):
+                step(i)
+            e_ev.record()
+            torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = s_ev.elapsed_time(e_ev) / steps
+        tile_ms = statistics.mean(a.elapsed_time(b) for a, b in tev) if plan.n_tile else 0.0
+        if world > 1:
+            t = torch.tensor([ms, tile_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms, tile_ms = float(t[0]), float(t[1])
+        e2e = None
+        if with_e2e and world == 1:
+            xh = x.cpu().pin_memory()
+            for _ in range(2):
+                hc.spmm_hybrid(ws, asg, xh, precision=args.precision)
+            torch.cuda.synchronize()
+            k = max(3, min(steps, 20))
+            t1 = time.perf_counter()
+            for _ in range(k):
+                r = hc.spmm_hybrid(ws, asg, xh, precision=args.precision)
+            torch.cuda.synchronize()
+            e2e_s = (time.perf_counter() - t1) / k
+            e2e = {"value": 2.0 * nnz * dim / e2e_s / 1e9, "unit": "GFLOP/s",
+                   "h2d_bytes_per_step": int(xh.numel() * xh.element_size()),
+                   "d2h_bytes_per_step": int(r.z.data.numel() * r.z.data.element_size()),
+                   "ms_per_step": e2e_s * 1e3,
+                   "api": "paper_2412_08902_b200.spmm_hybrid(windows, assignment, pinned host bf16 X) -> host fp32 Z"}
+        return ms, tile_ms, sampler.summary(), e2e
+
+    dim = args.dim
+    ms, tile_ms, clocks, e2e = measure(dim, args.steps, max(args.warmup, 3), not args.no_e2e)
+    s = 2  # bf16 bytes
+    gflops = 2.0 * nnz * dim / (ms * 1e-3) / 1e9
+    peak, peak_kind = peaks()
+    # algorithmic bytes of the tile kernel launch (SURVEY §8d formula restricted to its rows)
+    tile_rows = int(min(plan.n_tile * 16, local_a.num_rows)) if plan.n_tile else 0
+    if plan.n_tile:
+        nnz_w = ws.nnz_per_window()
+        tile_ids = plan.tile_list.long()
+        rs = tile_ids * 16
+        rc = torch.clamp(local_a.num_rows - rs, max=16)
+        tile_rows = int(rc.sum())
+    tile_bytes = 8 * (tile_rows + 1) + plan.nnz_tile * (4 + s) + local_a.num_cols * dim * s + tile_rows * dim * 4
+    full_bytes = 8 * (n + 1) + nnz * (4 + s) + n * dim * s + n * dim * 4
+    achieved = tile_bytes / (tile_ms * 1e-3) / 1e9 if tile_ms > 0 else full_bytes / (ms * 1e-3) / 1e9
+    gather_bytes = sum_ncols * dim * s  # L2 -> SM X-row gather traffic of the tile path (diagnostic)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            tr = json.load(fh).get(f"{args.config}_dim{dim}")
+        traffic = tr
+    out = {
+        "metric": "SpMM GFLOP/s (2*nnz*N/t)",
+        "value": gflops,
+        "unit": "GFLOP/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": max(args.warmup, 3),
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (seeded on-device generator; X ~ U[-1,1))",
+        "config": {
+            "workload": wl_name + f", hybrid SpMM, feature dim {dim}",
+            "n": n, "nnz": nnz, "dim": dim, "windows": len(ws),
+            "tile_windows": plan.stats.windows_tile, "scalar_windows": plan.stats.windows_scalar,
+            "sum_ncols": sum_ncols, "aggregate_ci": nnz / max(sum_ncols, 1),
+            "parallelism": f"row-window shards x{world}" if world > 1 else "single GPU",
+            "l2_policy": "inputs larger than L2 (CSR stream 0.69 GB); X kept resident with L2 evict_last hints",
+            "preprocess_ms": {"graph_gen_s": t_gen, "partition_select": t_partition_ms, "tile_plan": t_plan_ms},
+            "hbm_roofline_ms": full_bytes / (peak * 1e9) * 1e3,
+        },
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "kernel": "k_spmm_tile_bf16 (tcgen05)" if plan.n_tile else "k_spmm_scalar",
+                     "kernel_ms": tile_ms, "algorithmic_bytes": tile_bytes,
+                     "l2_gather_GBps": gather_bytes / (tile_ms * 1e-3) / 1e9 if tile_ms > 0 else None},
+        "gpu_launches": plan.launches_per_run(dim) * args.steps,
+        "clocks": clocks,
+    }
+    if e2e is not None:
+        out["e2e"] = e2e
+    if args.sweep_dims and world == 1:
+        sweep = {}
+        for d in (32, 64, 128):
+            m2, t2, _, _ = measure(d, min(args.steps, 100), 3, False)
+            fb = 8 * (n + 1) + nnz * (4 + s) + n * d * s + n * d * 4
+            sweep[str(d)] = {"ms": m2, "gflops": 2.0 * nnz * d / (m2 * 1e-3) / 1e9,
+                             "hbm_frac": fb / (m2 * 1e-3) / 1e9 / peak,
+                             "l2_gather_GBps": sum_ncols * d * s / (t2 * 1e-3) / 1e9 if t2 else None}
+        out["dims"] = sweep
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(adj, dim, args.cpu_budget)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def cpu_baseline(adj, dim, budget):
+    from oracle.baseline import sampled_gflops
+    from paper_2412_08902_b200 import graphgen
+
+    rp = adj.row_ptr.cpu().numpy()
+    ci = adj.col_idx.cpu().numpy()
+    x = graphgen.dense_features(adj.num_rows, dim, seed=1).float().cpu().numpy()
+    r = sampled_gflops(rp, ci, x, budget_s=budget)
+    return {"value": r["gflops"], "unit": "GFLOP/s", "cores": r["cores"], "kind": "port",
+            "sample": (f"{r['windows']} windows (every 73rd first, then the rest) of the same gcn-normalised graph, "
+                       f"{r['nnz']} nnz, reference hybrid SpMM restated in numpy float32, {r['seconds']:.1f} s, "
+                       f"extrapolated by nnz")}
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    from oracle.baseline import sampled_gflops
+    from paper_2412_08902_b200 import graphgen
+
+    if args.config == "c2":
+        adj = graphgen.reddit_shaped(seed=args.seed)
+    elif args.config == "c1":
+        adj = graphgen.cora_shaped(seed=args.seed)
+    else:
+        adj = graphgen.rmat(24, 33, seed=args.seed)
+    rp = adj.row_ptr.cpu().numpy()
+    ci = adj.col_idx.cpu().numpy()
+    n = adj.num_rows
+    nnz = int(rp[-1]) + n  # + gcn self loops
+    x = graphgen.dense_features(n, args.dim, seed=1).float().cpu().numpy()
+    budget = max(1.0, min(10.0, 150.0 / max(1, args.steps + args.warmup)))
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = sampled_gflops(rp, ci, x, budget_s=budget)
+        if i >= args.warmup:
+            vals.append(r)
+    g = statistics.mean(v["gflops"] for v in vals)
+    ms = 2.0 * nnz * args.dim / (g * 1e9) * 1e3
+    out = {"metric": "SpMM GFLOP/s (2*nnz*N/t)", "value": g, "unit": "GFLOP/s", "impl": "reference",
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+           "data": "synthetic (same seeded graph and X as the GPU arm)",
+           "config": {"workload": f"{args.config} reference hybrid SpMM (rowwin algorithm, numpy f32) dim {args.dim}",
+                      "n": n, "nnz": nnz, "dim": args.dim},
+           "cpu_baseline": {"value": g, "unit": "GFLOP/s", "cores": vals[0]["cores"], "kind": "port",
+                            "sample": f"per step {vals[0]['windows']} windows / {vals[0]['nnz']} nnz in "
+                                      f"~{budget:.1f} s, extrapolated by nnz"},
+           "e2e": {"value": g, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

@@ -1,0 +1,107 @@
+/*
+ * hcspmm.h -- C ABI of libhcspmm.so, the B200 (sm_100a) HC-SpMM hot path.
+ *
+ * Every entry point takes plain device pointers, sizes and a cudaStream_t
+ * (passed as void*), is stream-ordered, never allocates user-visible memory,
+ * and returns an HCS_* status; hcs_last_error() gives the thread-local message.
+ * The Python package paper_2412_08902_b200 binds these with ctypes and maps
+ * the status codes onto the reference's exception classes (ValueError /
+ * InvariantError), see paper_2412_08902_b200/_lib.py.
+ *
+ * The reference (rowwin, /root/reference/pkg/src/rowwin) has no FFI layer;
+ * each function below names the reference Python function(s) it replaces.
+ */
+#ifndef HCSPMM_H_
+#define HCSPMM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HCS_OK 0
+#define HCS_EINVAL 1     /* bad argument                 -> ValueError     */
+#define HCS_EDIM 2       /* dimension mismatch           -> ValueError     */
+#define HCS_EINVARIANT 3 /* internal consistency failure -> InvariantError */
+#define HCS_ECUDA 4      /* CUDA runtime / launch error  -> RuntimeError   */
+#define HCS_ENCCL 5      /* collective failure           -> RuntimeError   */
+
+#define HCS_DTYPE_F32 0
+#define HCS_DTYPE_BF16 1
+
+int hcs_version(void);
+const char* hcs_last_error(void);
+int hcs_device_sm_count(void);
+
+/* ---------------------------------------------------------------- K1
+ * windows.py:81-106 partition + windows.py:109-123 features +
+ * selector.py:48-64 SelectorModel.score/decide + classify_windows.
+ * Window w covers rows [w*wh, min((w+1)*wh, n_rows)); W = ceil(n_rows/wh).
+ * selector: the 7 doubles {w_ncols, w_density, bias, mean0, mean1, scale0,
+ * scale1} (data/default_selector.json) or NULL to skip classification.
+ * Two phases sharing one caller-owned workspace:
+ *   count: win_col_ptr[W+1] (exclusive prefix of ncols), density[W], ci[W], codes[W]
+ *   fill : nonzero_cols[win_col_ptr[W]] (ascending per window), cond_cols[nnz]
+ * Bit-exact with the reference (integer outputs; features/decisions in IEEE fp64). */
+int hcs_partition_workspace_bytes(int64_t n_rows, int64_t n_cols, int64_t nnz, int32_t wh, size_t* bytes);
+int hcs_partition_count(const int64_t* row_ptr, const int32_t* col_idx, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                        int32_t wh, const double* selector, int64_t* win_col_ptr, double* density, double* ci,
+                        uint8_t* codes, void* workspace, size_t ws_bytes, void* stream);
+int hcs_partition_fill(const int64_t* row_ptr, const int32_t* col_idx, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                       int32_t wh, const int64_t* win_col_ptr, int32_t* nonzero_cols, int32_t* cond_cols,
+                       void* workspace, size_t ws_bytes, void* stream);
+/* selector.py:48-56 on caller-given features (classify_windows with a non-default model) */
+int hcs_classify(const int64_t* win_col_ptr, const double* density, int64_t n_windows, const double* selector,
+                 uint8_t* codes, void* stream);
+
+/* ---------------------------------------------------------------- K2
+ * Execution plan for the TILE windows of executors.py:160-188 _run_windows:
+ * packs each TILE window's entries into 64-column chunks for the tensor-core
+ * kernel.  tile_list: T window ids (schedule order); chunk_ptr[T+1] (chunks of
+ * 64 condensed columns per window, exclusive prefix); gidx[nchunks*64] gather
+ * row per chunk slot (-1 = padding, zero-filled in shared memory);
+ * ent_ptr[nchunks+1]; ent[nnz_tile] packed (bf16 value << 16 | slab position
+ * r*64+c) for HCS_DTYPE_BF16, or {pos, fp32 bits} pairs (uint64) for F32. */
+int hcs_tile_plan_workspace_bytes(int64_t nnz_tile, int64_t nchunks, size_t* bytes);
+int hcs_tile_plan(const int64_t* row_ptr, const int32_t* cond_cols, const void* values, int values_dtype,
+                  const int64_t* win_col_ptr, const int32_t* nonzero_cols, int64_t n_rows, int64_t n_cols, int32_t wh,
+                  const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, int64_t nchunks,
+                  int32_t* gidx, int64_t* ent_ptr, void* ent, int ent_dtype, int64_t nnz_tile,
+                  void* workspace, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------- K3
+ * executors.py:100-108 scalar_window (per window list) and 191-213
+ * spmm_scalar (pass all windows).  One warp per row, 128-bit X loads, fp32
+ * accumulation, fixed-order warp-shuffle reduction (deterministic).
+ * x: [*, ldx] (dtype x_dtype); z: fp32 [n_rows, ldz]; window rows beyond the
+ * listed windows are untouched; listed empty windows are zero-filled. */
+int hcs_spmm_scalar(const int64_t* row_ptr, const int32_t* col_idx, const void* values, int values_dtype,
+                    int64_t n_rows, int32_t wh, const int32_t* win_list, int64_t n_list, const void* x, int x_dtype,
+                    int64_t x_rows, int32_t dim, int64_t ldx, float* z, int64_t ldz, void* stream);
+
+/* ---------------------------------------------------------------- K4
+ * executors.py:111-141 tile_window for every window of a tile plan:
+ * tcgen05.mma (bf16 kind::f16) with the gathered X rows as the MN-major A
+ * operand (cp.async 16-byte row gathers, 128B swizzle) and the 16-row condensed
+ * slab as the K-major B operand; fp32 accumulators in TMEM. */
+int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
+                  const int64_t* ent_ptr, const void* ent, int ent_dtype, int64_t n_rows, int32_t wh, const void* x,
+                  int x_dtype, int64_t x_rows, int32_t dim, int64_t ldx, float* z, int64_t ldz, void* stream);
+
+/* ---------------------------------------------------------------- normalisation
+ * gnn.py:68-95 normalize_adj values in float64 with the reference's operation
+ * order (structure of A + I assembled by the caller).  kind 0 = gcn
+ * ((v * d_r^-1/2) * d_c^-1/2, d = row sums in entry order), 1 = row (v / deg).
+ * v_out32 (optional) receives the float32 copy used by the kernels. */
+int hcs_normalize_values(int kind, const int64_t* row_ptr, const int32_t* col, const double* v_in, int64_t n,
+                         double* workspace_deg, double* v_out, float* v_out32, void* stream);
+
+/* elementwise helpers used by the Python layer (fp32 -> bf16 RNE, fp32 -> tf32 RNA) */
+int hcs_convert(const float* src, void* dst, int64_t n, int dst_kind, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HCSPMM_H_ */

@@ -1,0 +1,356 @@
+"""Hybrid SpMM executors (reference executors.py) on the B200.
+
+  spmm_scalar  -> K3 CUDA-core warp-per-row kernel over every row (executors.py:191-213)
+  spmm_tile    -> K4 tcgen05 tile kernel over every non-empty window (216-231)
+  spmm_hybrid  -> K2 plan + K4 for TILE windows + K3 for SCALAR windows (234-251)
+  spmm_auto    -> K1 partition/select, then spmm_hybrid (263-272)
+
+Precision: "bf16" (bf16 X and A values, fp32 accumulate; default) or "tf32"
+(fp32 X and values, tf32 tensor-core inputs rounded to nearest, fp32 scalar
+path).  The reference's "f64"/"f32" host precisions are rejected (no CPU path).
+Outputs are fp32.  `threads` is accepted for signature compatibility and ignored.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from enum import Enum
+
+import numpy as np
+import torch
+
+from . import _lib
+from .matrices import DenseMatrix, DeviceCsr, to_device_csr
+
+_PRECISIONS = ("bf16", "tf32")
+TILE_CHUNK = 64  # condensed columns per tensor-core K step group
+
+
+class Path(Enum):
+    """executors.py:23-25."""
+
+    SCALAR = "scalar"
+    TILE = "tile"
+
+
+class Assignment:
+    """Per-window path codes, 0 = scalar, 1 = tile (executors.py:28-57).
+
+    Holds host codes (numpy uint8) and/or a device copy; each is materialised on demand.
+    """
+
+    def __init__(self, codes):
+        if isinstance(codes, torch.Tensor):
+            self._dev = codes.to(torch.uint8)
+            self._host = None
+        else:
+            c = np.asarray(codes, dtype=np.uint8)
+            if c.ndim != 1 or (c.size and c.max() > 1):
+                raise ValueError("assignment codes must be a 1-D array of 0/1")
+            self._host = c
+            self._dev = None
+
+    @classmethod
+    def from_device(cls, codes: torch.Tensor) -> "Assignment":
+        return cls(codes)
+
+    @property
+    def codes(self) -> np.ndarray:
+        if self._host is None:
+            self._host = self._dev.cpu().numpy()
+        return self._host
+
+    def device_codes(self, device) -> torch.Tensor:
+        if self._dev is None or self._dev.device != device:
+            self._dev = torch.from_numpy(self.codes).to(device)
+        return self._dev
+
+    def __len__(self) -> int:
+        return int(self._dev.numel()) if self._dev is not None else int(self._host.size)
+
+    def path(self, window_id: int) -> Path:
+        return Path.TILE if self.codes[window_id] else Path.SCALAR
+
+    def count(self, path: Path) -> int:
+        tiles = int(self.codes.sum())
+        return tiles if path is Path.TILE else len(self) - tiles
+
+    @classmethod
+    def from_paths(cls, paths) -> "Assignment":
+        return cls(np.array([1 if p is Path.TILE else 0 for p in paths], dtype=np.uint8))
+
+    @classmethod
+    def uniform(cls, n: int, path: Path) -> "Assignment":
+        return cls(np.full(n, 1 if path is Path.TILE else 0, dtype=np.uint8))
+
+    def __eq__(self, other):
+        return isinstance(other, Assignment) and np.array_equal(self.codes, other.codes)
+
+    __hash__ = object.__hash__
+
+
+@dataclass
+class ExecStats:
+    """executors.py:60-84."""
+
+    windows_scalar: int = 0
+    windows_tile: int = 0
+    entries_scalar: int = 0
+    entries_tile: int = 0
+    tiles_processed: int = 0
+
+    def merge(self, other: "ExecStats") -> None:
+        self.windows_scalar += other.windows_scalar
+        self.windows_tile += other.windows_tile
+        self.entries_scalar += other.entries_scalar
+        self.entries_tile += other.entries_tile
+        self.tiles_processed += other.tiles_processed
+
+    def as_dict(self) -> dict:
+        return {"windows_scalar": self.windows_scalar, "windows_tile": self.windows_tile,
+                "entries_scalar": self.entries_scalar, "entries_tile": self.entries_tile,
+                "tiles_processed": self.tiles_processed}
+
+
+@dataclass(frozen=True)
+class SpmmResult:
+    """executors.py:87-90."""
+
+    z: DenseMatrix
+    stats: ExecStats
+
+
+def _resolve_precision(precision: str) -> str:
+    if precision not in _PRECISIONS:
+        raise ValueError(f"precision must be one of {sorted(_PRECISIONS)}, got {precision!r}")
+    return precision
+
+
+# --------------------------------------------------------------------------- operands
+def _round_up(v: int, m: int) -> int:
+    return -(-v // m) * m
+
+
+class DeviceOperand:
+    """X staged for the kernels: compute dtype, rows padded to a 16-byte multiple."""
+
+    def __init__(self, t: torch.Tensor, dim: int, ld: int, dtype_code: int):
+        self.t, self.dim, self.ld, self.dtype_code = t, dim, ld, dtype_code
+
+    @property
+    def rows(self) -> int:
+        return int(self.t.shape[0])
+
+
+def stage_operand(x, precision: str, device, tf32_round: bool = False) -> tuple[DeviceOperand, bool]:
+    """Returns (operand, was_host).  Host numpy / DenseMatrix inputs are copied to HBM."""
+    data = x.data if isinstance(x, DenseMatrix) else x
+    was_host = (not isinstance(data, torch.Tensor)) or data.device.type == "cpu"
+    t = data if isinstance(data, torch.Tensor) else torch.as_tensor(np.ascontiguousarray(data))
+    if t.dim() != 2:
+        raise ValueError("dense matrix must be 2-dimensional")
+    rows, dim = int(t.shape[0]), int(t.shape[1])
+    if precision == "bf16":
+        want, elems, code = torch.bfloat16, 8, _lib.DTYPE_BF16
+    else:
+        want, elems, code = torch.float32, 4, _lib.DTYPE_F32
+    ld = max(_round_up(dim, elems), elems)
+    direct = (not was_host and t.device == device and t.dtype == want and t.is_contiguous() and ld == dim
+              and t.data_ptr() % 16 == 0 and not tf32_round)
+    if direct:
+        return DeviceOperand(t, dim, ld, code), was_host
+    buf = torch.zeros((rows, ld), dtype=want, device=device)
+    if rows and dim:
+        src = t.to(device=device, non_blocking=True)
+        if tf32_round:
+            src32 = src.to(torch.float32).contiguous()
+            tmp = torch.empty_like(src32)
+            _lib.call("hcs_convert", src32.data_ptr(), tmp.data_ptr(), src32.numel(), 0, _lib.stream())
+            buf[:, :dim] = tmp
+        else:
+            buf[:, :dim] = src.to(want)
+    return DeviceOperand(buf, dim, ld, code), was_host
+
+
+# --------------------------------------------------------------------------- hybrid plan
+class HybridPlan:
+    """K2 execution plan for (windows, assignment, precision): TILE window list with
+    packed 64-column chunks, SCALAR/empty window list, and the ExecStats."""
+
+    def __init__(self, windows, codes: torch.Tensor, precision: str):
+        dev = windows.csr.device
+        self.windows = windows
+        self.precision = precision
+        csr = windows.csr
+        nnz_w = windows.nnz_per_window()
+        ncols = windows.ncols()
+        tile_mask = (codes.to(torch.bool)) & (nnz_w > 0)
+        self.tile_list = torch.nonzero(tile_mask).flatten().to(torch.int32)
+        self.scalar_list = torch.nonzero(~tile_mask).flatten().to(torch.int32)
+        nc_t = ncols[self.tile_list.long()]
+        chunks = (nc_t + TILE_CHUNK - 1) // TILE_CHUNK
+        self.chunk_ptr = torch.zeros(self.tile_list.numel() + 1, dtype=torch.int64, device=dev)
+        torch.cumsum(chunks, 0, out=self.chunk_ptr[1:])
+        scal_live = (~codes.to(torch.bool)) & (nnz_w > 0)
+        tot = torch.stack([
+            scal_live.sum(), tile_mask.sum(), nnz_w[scal_live].sum(), nnz_w[tile_mask].sum(),
+            ((nc_t + 7) // 8).sum(), self.chunk_ptr[-1]]).cpu().tolist()
+        self.stats = ExecStats(int(tot[0]), int(tot[1]), int(tot[2]), int(tot[3]), int(tot[4]))
+        self.nchunks = int(tot[5])
+        self.n_tile = int(self.tile_list.numel())
+        self.nnz_tile = int(tot[3])
+        ent_dtype = _lib.DTYPE_BF16 if precision == "bf16" else _lib.DTYPE_F32
+        self.ent_dtype = ent_dtype
+        self.gidx = torch.empty(max(self.nchunks * TILE_CHUNK, 1), dtype=torch.int32, device=dev)
+        self.ent_ptr = torch.zeros(self.nchunks + 1, dtype=torch.int64, device=dev)
+        ent_words = self.nnz_tile if ent_dtype == _lib.DTYPE_BF16 else 2 * self.nnz_tile
+        self.ent = torch.empty(max(ent_words, 1), dtype=torch.int32, device=dev)
+        if self.n_tile:
+            wsb = _lib.ctypes.c_size_t(0)
+            _lib.check(_lib.lib().hcs_tile_plan_workspace_bytes(self.nnz_tile, self.nchunks, _lib.ctypes.byref(wsb)))
+            ws = torch.empty(max(int(wsb.value), 1), dtype=torch.uint8, device=dev)
+            _lib.call("hcs_tile_plan", csr.row_ptr.data_ptr(), windows.cond_cols.data_ptr(), csr.values.data_ptr(),
+                      _lib.DTYPE_F32, windows.win_col_ptr.data_ptr(), windows.nonzero_cols.data_ptr(), csr.num_rows,
+                      csr.num_cols, windows.window_height, self.tile_list.data_ptr(), self.n_tile,
+                      self.chunk_ptr.data_ptr(), self.nchunks, self.gidx.data_ptr(), self.ent_ptr.data_ptr(),
+                      self.ent.data_ptr(), ent_dtype, self.nnz_tile, ws.data_ptr(), ws.numel(), _lib.stream())
+            del ws
+        if precision == "bf16":
+            self.scalar_vals, self.scalar_vals_code = csr.values_bf16(), _lib.DTYPE_BF16
+        else:
+            self.scalar_vals, self.scalar_vals_code = csr.values, _lib.DTYPE_F32
+
+    def launches_per_run(self, dim: int) -> int:
+        return (-(-dim // 128) if self.n_tile else 0) + (1 if self.scalar_list.numel() else 0)
+
+    def run(self, xop: DeviceOperand, z: torch.Tensor, ldz: int, stream=None, tile_events=None) -> None:
+        """Launch K4 (tile windows) then K3 (scalar + empty windows) on the current stream.
+        tile_events: optional (start, end) torch.cuda.Event pair recorded around K4."""
+        csr = self.windows.csr
+        s = _lib.stream() if stream is None else stream
+        if tile_events is not None:
+            tile_events[0].record()
+        if self.n_tile:
+            if self.precision != "bf16":
+                raise NotImplementedError("tf32 tile kernel not built in this revision; use precision='bf16'")
+            _lib.call("hcs_spmm_tile", self.tile_list.data_ptr(), self.n_tile, self.chunk_ptr.data_ptr(),
+                      self.gidx.data_ptr(), self.ent_ptr.data_ptr(), self.ent.data_ptr(), self.ent_dtype,
+                      csr.num_rows, self.windows.window_height, xop.t.data_ptr(), xop.dtype_code, xop.rows, xop.dim,
+                      xop.ld, z.data_ptr(), ldz, s)
+        if tile_events is not None:
+            tile_events[1].record()
+        if self.scalar_list.numel():
+            _lib.call("hcs_spmm_scalar", csr.row_ptr.data_ptr(), csr.col_idx.data_ptr(), self.scalar_vals.data_ptr(),
+                      self.scalar_vals_code, csr.num_rows, self.windows.window_height, self.scalar_list.data_ptr(),
+                      self.scalar_list.numel(), xop.t.data_ptr(), xop.dtype_code, xop.rows, xop.dim, xop.ld,
+                      z.data_ptr(), ldz, s)
+
+
+def get_plan(windows, assignment: Assignment, precision: str) -> HybridPlan:
+    dev = windows.csr.device
+    codes = assignment.device_codes(dev)
+    key = (precision, codes.data_ptr(), int(codes.numel()))
+    plan = windows._plans.get(key)
+    if plan is None:
+        if assignment._host is not None:
+            key = (precision, assignment.codes.tobytes())
+            plan = windows._plans.get(key)
+        if plan is None:
+            plan = HybridPlan(windows, codes, precision)
+            windows._plans[key] = plan
+    return plan
+
+
+def _check_window_bounds(windows, x_rows: int) -> None:
+    """executors.py:254-260: first window whose largest column is >= X rows."""
+    ncols = windows.ncols()
+    live = ncols > 0
+    if not bool(live.any()):
+        return
+    last = windows.nonzero_cols[(windows.win_col_ptr[1:] - 1).clamp(min=0)].to(torch.int64)
+    bad = live & (last >= x_rows)
+    if bool(bad.any()):
+        w = int(torch.nonzero(bad)[0].item())
+        raise ValueError(f"window {w} references column {int(last[w].item())} but X has {x_rows} rows")
+
+
+def _host_kind(x):
+    data = x.data if isinstance(x, DenseMatrix) else x
+    return "torch" if isinstance(data, torch.Tensor) else True
+
+
+def _alloc_z(rows: int, dim: int, device) -> tuple[torch.Tensor, int]:
+    ldz = max(_round_up(dim, 4), 4)
+    return torch.empty((rows, ldz), dtype=torch.float32, device=device), ldz
+
+
+def _wrap_result(z: torch.Tensor, dim: int, was_host, stats: ExecStats) -> SpmmResult:
+    """Host inputs give host outputs (numpy for numpy/DenseMatrix input, a CPU tensor
+    for a CPU tensor input), device inputs give device outputs."""
+    out = z[:, :dim]
+    if was_host == "torch":
+        return SpmmResult(DenseMatrix(out.to("cpu")), stats)
+    if was_host:
+        return SpmmResult(DenseMatrix(out.cpu().numpy()), stats)
+    return SpmmResult(DenseMatrix(out if out.is_contiguous() else out.contiguous()), stats)
+
+
+def spmm_hybrid(windows, assignment: Assignment, x, precision: str = "bf16", threads: int = 1,
+                tile_cols: int = 8, dim_tile: int = 16) -> SpmmResult:
+    """executors.py:234-251: TILE windows on tensor cores, SCALAR windows on CUDA cores."""
+    from .windows import as_windowset
+
+    if len(assignment) != len(windows):
+        raise ValueError(f"assignment covers {len(assignment)} windows, expected {len(windows)}")
+    precision = _resolve_precision(precision)
+    ws = as_windowset(windows)
+    xrows = x.rows if isinstance(x, DenseMatrix) else int(x.shape[0])
+    _check_window_bounds(ws, xrows)
+    dev = ws.csr.device
+    plan = get_plan(ws, assignment, precision)
+    xop, was_host = stage_operand(x, precision, dev, tf32_round=(precision == "tf32" and plan.n_tile > 0))
+    z, ldz = _alloc_z(ws.num_rows, xop.dim, dev)
+    plan.run(xop, z, ldz)
+    return _wrap_result(z, xop.dim, _host_kind(x) if was_host else False, ExecStats(**plan.stats.as_dict()))
+
+
+def spmm_tile(windows, x, precision: str = "bf16", tile_cols: int = 8, dim_tile: int = 16,
+              threads: int = 1) -> SpmmResult:
+    """executors.py:216-231: every non-empty window on the tensor-core path."""
+    from .windows import as_windowset
+
+    ws = as_windowset(windows)
+    asg = Assignment(torch.ones(len(ws), dtype=torch.uint8, device=ws.csr.device))
+    return spmm_hybrid(ws, asg, x, precision=precision, threads=threads)
+
+
+def spmm_scalar(csr, x, precision: str = "bf16", window_height: int = 16) -> SpmmResult:
+    """executors.py:191-213: every row on the CUDA-core path (no partition needed)."""
+    xrows = x.rows if isinstance(x, DenseMatrix) else int(x.shape[0])
+    if csr.num_cols != xrows:
+        raise ValueError(f"dimension mismatch: matrix has {csr.num_cols} cols, X has {xrows} rows")
+    precision = _resolve_precision(precision)
+    dev = _lib.require_cuda()
+    d = to_device_csr(csr, dev)
+    xop, was_host = stage_operand(x, precision, dev)
+    z, ldz = _alloc_z(d.num_rows, xop.dim, dev)
+    W = -(-d.num_rows // window_height)
+    wl = torch.arange(W, dtype=torch.int32, device=dev)
+    vals, vcode = (d.values_bf16(), _lib.DTYPE_BF16) if precision == "bf16" else (d.values, _lib.DTYPE_F32)
+    if W:
+        _lib.call("hcs_spmm_scalar", d.row_ptr.data_ptr(), d.col_idx.data_ptr(), vals.data_ptr(), vcode, d.num_rows,
+                  window_height, wl.data_ptr(), W, xop.t.data_ptr(), xop.dtype_code, xop.rows, xop.dim, xop.ld,
+                  z.data_ptr(), ldz, _lib.stream())
+    rs = torch.arange(W, device=dev, dtype=torch.int64) * window_height
+    re = torch.clamp(rs + window_height, max=d.num_rows)
+    nonempty = int(((d.row_ptr[re] - d.row_ptr[rs]) > 0).sum().item()) if W else 0
+    return _wrap_result(z, xop.dim, _host_kind(x) if was_host else False,
+                        ExecStats(windows_scalar=nonempty, entries_scalar=d.nnz))
+
+
+def spmm_auto(csr, x, assignment_for, precision: str = "bf16", threads: int = 1) -> SpmmResult:
+    """executors.py:263-272."""
+    from .windows import partition
+
+    windows = partition(csr)
+    return spmm_hybrid(windows, assignment_for(windows), x, precision=precision, threads=threads)

@@ -1,0 +1,129 @@
+"""CPU: the C-ABI library loads and exports every symbol include/hcspmm.h declares;
+host-side API logic (errors, selector KATs, Assignment/ExecStats) without a GPU."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+import paper_2412_08902_b200 as hc
+from paper_2412_08902_b200 import _lib
+from paper_2412_08902_b200.executors import Assignment, ExecStats, Path
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "hcspmm.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*|size_t)\s+(hcs_[a-z0-9_]+)\s*\(", src, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    h = ctypes.CDLL(_lib.LIB_PATH)
+    syms = declared_symbols()
+    assert len(syms) >= 10
+    missing = [s for s in syms if not hasattr(h, s)]
+    assert not missing, missing
+    # every declared symbol is also bound by the Python layer
+    assert not [s for s in syms if s not in _lib._SIGS]
+
+
+def test_library_version_and_error_string():
+    L = _lib.lib()
+    assert L.hcs_version() >= 100
+    assert isinstance(L.hcs_last_error(), bytes)
+
+
+def test_abi_argument_validation_without_gpu():
+    L = _lib.lib()
+    # invalid window height is rejected before any device work
+    rc = L.hcs_partition_count(None, None, 10, 10, 0, 0, None, None, None, None, None, None, 0, None)
+    assert rc == _lib.HCS_EINVAL
+    assert b"window_height" in L.hcs_last_error()
+    with pytest.raises(ValueError, match="window_height"):
+        _lib.check(rc)
+
+
+def test_precision_rejected():
+    with pytest.raises(ValueError, match="precision"):
+        hc.spmm_scalar(hc.SparseCsr(2, 2, np.array([0, 1, 1]), np.array([0]), np.array([1.0])),
+                       hc.DenseMatrix(np.ones((2, 2))), precision="f64")
+
+
+def test_dimension_mismatch_message():
+    csr = hc.SparseCsr(2, 3, np.array([0, 1, 1]), np.array([0]), np.array([1.0]))
+    with pytest.raises(ValueError, match="mismatch"):
+        hc.spmm_scalar(csr, hc.DenseMatrix(np.ones((2, 2))))
+
+
+def test_partition_rejects_bad_height():
+    with pytest.raises(ValueError, match="window_height"):
+        hc.partition(hc.SparseCsr(1, 1, np.array([0, 0]), np.array([], dtype=np.int64), np.array([])),
+                     window_height=0)
+
+
+def test_selector_threshold_semantics():
+    # reference tests/test_selector.py:160-174
+    m = hc.SelectorModel(w_ncols=0.0, w_density=-1.0, bias=0.0, feature_means=(0.0, 0.5), feature_scales=(1.0, 1.0))
+    assert m.decide(8, 0.4) is Path.SCALAR
+    assert m.decide(8, 0.6) is Path.TILE
+    assert m.decide(8, 0.5) is Path.TILE
+    e = hc.SelectorModel(0.0, 0.0, -5.0, (0.0, 0.0), (1.0, 1.0))
+    assert e.decide(0, 0.0) is Path.SCALAR
+
+
+def test_default_model_constants():
+    m = hc.default_model()
+    assert (m.w_ncols, m.w_density, m.bias) == (-0.1454848214145233, -9.249873814861964, -15.105252482198011)
+    assert m.feature_means == (140.38659793814432, 0.5)
+    assert m.feature_scales == (123.08273985946481, 0.2570676399373035)
+
+
+def test_default_model_monotone_in_density():
+    # reference tests/test_selector.py:229-240
+    m = hc.default_model()
+    for nc in (16, 64, 128, 256):
+        ds = [m.decide(nc, d) for d in np.linspace(0.01, 0.95, 60)]
+        flips = sum(1 for a, b in zip(ds, ds[1:]) if a is not b)
+        assert flips <= 1
+        if flips:
+            assert ds[0] is Path.SCALAR and ds[-1] is Path.TILE
+
+
+def test_vectorised_host_decisions_match_scalar():
+    from paper_2412_08902_b200.selector import decisions_host
+
+    m = hc.default_model()
+    rng = np.random.default_rng(0)
+    nc = rng.integers(0, 3000, size=5000)
+    d = rng.random(5000)
+    want = [0 if n == 0 else (1 if m.decide(int(n), float(x)) is Path.TILE else 0) for n, x in zip(nc, d)]
+    assert decisions_host(m, nc, d).tolist() == want
+
+
+def test_assignment_semantics():
+    a = Assignment(np.array([0, 1, 1, 0, 1], dtype=np.uint8))
+    assert len(a) == 5 and a.count(Path.TILE) == 3 and a.count(Path.SCALAR) == 2
+    assert a.path(0) is Path.SCALAR and a.path(1) is Path.TILE
+    assert Assignment.from_paths([Path.SCALAR, Path.TILE]).codes.tolist() == [0, 1]
+    with pytest.raises(ValueError):
+        Assignment(np.array([0, 2], dtype=np.uint8))
+
+
+def test_exec_stats_merge():
+    s = ExecStats(1, 2, 3, 4, 5)
+    s.merge(ExecStats(1, 1, 1, 1, 1))
+    assert s.as_dict() == {"windows_scalar": 2, "windows_tile": 3, "entries_scalar": 4, "entries_tile": 5,
+                           "tiles_processed": 6}
+
+
+def test_sparse_csr_validate_and_from_coo():
+    csr = hc.SparseCsr.from_coo(3, 3, np.array([0, 0, 2, 0]), np.array([1, 1, 0, 2]), np.array([2.0, 3.0, 1.0, 4.0]))
+    assert csr.row_ptr.tolist() == [0, 2, 2, 3]
+    assert csr.col_idx.tolist() == [1, 2, 0] and csr.values.tolist() == [5.0, 4.0, 1.0]
+    csr.validate()
+    bad = hc.SparseCsr(2, 3, np.array([0, 2, 2]), np.array([2, 1]), np.ones(2))
+    with pytest.raises(ValueError, match="strictly ascending"):
+        bad.validate()

@@ -1,0 +1,169 @@
+"""GPU SpMM parity (K2/K3/K4) against the oracle and the reference's golden results.
+
+Tolerances (BASELINE.json north_star): max_rel_err (tests/conftest.py:42-47 of the
+reference: max|a-o| / max|o|) <= 1e-2 for bf16 inputs, against the exact fp64
+product of the same inputs.  Integer outputs (stats) are exact.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden_csr, golden_names, load_golden, plaw8k_csr
+from oracle import rowwin_oracle as orc
+
+import paper_2412_08902_b200 as hc
+from paper_2412_08902_b200.executors import Assignment, Path
+
+pytestmark = pytest.mark.gpu
+BF16_TOL = 1e-2
+
+
+def to_hc(csr):
+    return hc.SparseCsr(csr.num_rows, csr.num_cols, csr.row_ptr, csr.col_idx, csr.values)
+
+
+@pytest.mark.parametrize("name", [n for n in golden_names("windows_") if n != "windows_plaw8k"])
+def test_hybrid_matches_reference(cuda_ok, name):
+    g = load_golden(name)
+    csr = golden_csr(g)
+    x = orc.random_dense(csr.num_cols, int(g["dim"]), int(g["xseed"]))
+    ws = hc.partition(to_hc(csr))
+    asg = hc.classify_windows(hc.default_model(), ws)
+    res = hc.spmm_hybrid(ws, asg, hc.DenseMatrix(x), precision="bf16")
+    assert res.z.data.shape == (csr.num_rows, int(g["dim"]))
+    assert orc.max_rel_err(res.z.data, g["z_f64"]) <= BF16_TOL
+    assert orc.max_rel_err(res.z.data, g["z_f32"]) <= BF16_TOL
+    for k, v in res.stats.as_dict().items():
+        assert v == int(g["stats_" + k]), k
+
+
+@pytest.mark.parametrize("name", ["windows_cora", "windows_corpus_block125", "windows_corpus_clique64",
+                                  "windows_rand6", "windows_rand9"])
+def test_all_tile_and_all_scalar(cuda_ok, name):
+    g = load_golden(name)
+    csr = golden_csr(g)
+    x = orc.random_dense(csr.num_cols, int(g["dim"]), int(g["xseed"]))
+    ws = hc.partition(to_hc(csr))
+    t = hc.spmm_tile(ws, hc.DenseMatrix(x))
+    assert orc.max_rel_err(t.z.data, g["z_f64"]) <= BF16_TOL
+    s = hc.spmm_scalar(to_hc(csr), hc.DenseMatrix(x))
+    assert orc.max_rel_err(s.z.data, g["z_f64"]) <= BF16_TOL
+    live = int((ws.nnz_per_window() > 0).sum())
+    assert t.stats.windows_tile == live and t.stats.entries_tile == csr.nnz
+    assert s.stats.windows_scalar == live and s.stats.entries_scalar == csr.nnz
+    # all-scalar hybrid == spmm_scalar (same kernel, same order): bitwise
+    h = hc.spmm_hybrid(ws, Assignment.uniform(len(ws), Path.SCALAR), hc.DenseMatrix(x))
+    assert np.array_equal(h.z.data, s.z.data)
+    assert h.stats.as_dict() == s.stats.as_dict()
+
+
+def test_plaw8k_mixed_paths(cuda_ok):
+    g = load_golden("windows_plaw8k")
+    a = plaw8k_csr()
+    x = orc.random_dense(a.num_cols, 32, 1)
+    ws = hc.partition(to_hc(a))
+    asg = hc.classify_windows(hc.default_model(), ws)
+    assert 0 < asg.count(Path.TILE) < len(asg)
+    res = hc.spmm_hybrid(ws, asg, hc.DenseMatrix(x))
+    assert orc.max_rel_err(res.z.data, g["z_f32"]) <= BF16_TOL
+    for k, v in res.stats.as_dict().items():
+        assert v == int(g["stats_" + k]), k
+
+
+@pytest.mark.parametrize("dim", [1, 3, 8, 17, 32, 40, 64, 96, 128, 136, 256, 300])
+def test_feature_dims(cuda_ok, dim):
+    a = orc.random_csr(300, 700, 0.08, seed=dim)
+    x = orc.random_dense(700, dim, seed=dim + 1)
+    ws = hc.partition(to_hc(a))
+    codes = np.random.default_rng(dim).integers(0, 2, size=len(ws)).astype(np.uint8)
+    res = hc.spmm_hybrid(ws, Assignment(codes), hc.DenseMatrix(x))
+    assert orc.max_rel_err(res.z.data, orc.spmm_exact(a, x)) <= BF16_TOL
+    t = hc.spmm_tile(ws, hc.DenseMatrix(x))
+    assert orc.max_rel_err(t.z.data, orc.spmm_exact(a, x)) <= BF16_TOL
+
+
+def test_empty_windows_zero_and_uncounted(cuda_ok):
+    # reference tests/test_executors.py:136-146
+    csr = hc.SparseCsr.from_coo(48, 8, np.array([0, 35]), np.array([2, 3]), np.array([1.0, 1.0]))
+    ws = hc.partition(csr)
+    assert [w.nnz for w in ws] == [1, 0, 1]
+    x = hc.DenseMatrix.random(8, 3, seed=1)
+    res = hc.spmm_hybrid(ws, Assignment.uniform(3, Path.TILE), x)
+    assert res.stats.windows_tile == 2
+    assert np.array_equal(res.z.data[16:32], np.zeros((16, 3)))
+
+
+def test_stats_tiles(cuda_ok):
+    # reference tests/test_executors.py:110-120: 9 cols -> 2 tiles, 4 cols -> 1 tile
+    rows = np.concatenate([np.zeros(9, dtype=np.int64), np.full(4, 16, dtype=np.int64)])
+    cols = np.concatenate([np.arange(9), np.arange(4)]).astype(np.int64)
+    csr = hc.SparseCsr.from_coo(32, 16, rows, cols, np.ones(13))
+    res = hc.spmm_tile(hc.partition(csr), hc.DenseMatrix.random(16, 4, seed=0))
+    assert res.stats.windows_tile == 2 and res.stats.entries_tile == 13 and res.stats.tiles_processed == 3
+
+
+def test_validation_messages(cuda_ok):
+    csr = to_hc(orc.random_csr(8, 10, 0.5, seed=0))
+    ws = hc.partition(csr)
+    with pytest.raises(ValueError, match="X has"):
+        hc.spmm_tile(ws, hc.DenseMatrix.random(3, 2, seed=0))
+    ws2 = hc.partition(to_hc(orc.random_csr(40, 10, 0.2, seed=1)))
+    with pytest.raises(ValueError, match="assignment covers"):
+        hc.spmm_hybrid(ws2, Assignment.uniform(1, Path.SCALAR), hc.DenseMatrix.random(10, 2, seed=0))
+
+
+def test_deterministic_repeat(cuda_ok):
+    a = plaw8k_csr()
+    x = torch.rand(a.num_cols, 64, device="cuda").to(torch.bfloat16)
+    ws = hc.partition(to_hc(a))
+    asg = hc.classify_windows(hc.default_model(), ws)
+    z1 = hc.spmm_hybrid(ws, asg, x).z.data.clone()
+    z2 = hc.spmm_hybrid(ws, asg, x).z.data
+    assert torch.equal(z1, z2)
+    zt1 = hc.spmm_tile(ws, x).z.data.clone()
+    assert torch.equal(zt1, hc.spmm_tile(ws, x).z.data)
+
+
+def test_power_of_two_scaling_exact(cuda_ok):
+    a = orc.random_csr(40, 30, 0.2, seed=20)
+    d = orc.Csr(a.num_rows, a.num_cols, a.row_ptr, a.col_idx, a.values * 2.0)
+    x = hc.DenseMatrix.random(30, 7, seed=21)
+    z1 = hc.spmm_tile(hc.partition(to_hc(a)), x).z.data
+    z2 = hc.spmm_tile(hc.partition(to_hc(d)), x).z.data
+    assert np.array_equal(z1 * 2.0, z2)
+
+
+def test_device_operands_and_auto(cuda_ok):
+    a = orc.random_csr(500, 500, 0.05, seed=5)
+    xd = torch.randn(500, 32, device="cuda", dtype=torch.bfloat16)
+    res = hc.spmm_auto(to_hc(a), xd, lambda ws: hc.classify_windows(hc.default_model(), ws))
+    assert isinstance(res.z.data, torch.Tensor) and res.z.data.is_cuda
+    want = orc.spmm_exact(a, xd.float().cpu().numpy())
+    assert orc.max_rel_err(res.z.data.cpu().numpy(), want) <= BF16_TOL
+
+
+def test_large_powerlaw_tile_path_checksum(cuda_ok):
+    """Size-independent property at ~6M nnz: Z summed over rows == (A^T 1)^T X in fp64."""
+    from paper_2412_08902_b200 import graphgen
+
+    g = graphgen.chung_lu_device(60000, 200.0, seed=3)
+    a = graphgen.gcn_normalize_device(g)
+    ws = hc.partition(a)
+    x = torch.rand(a.num_rows, 128, device="cuda", generator=torch.Generator("cuda").manual_seed(1)) * 2 - 1
+    xb = x.to(torch.bfloat16)
+    res = hc.spmm_hybrid(ws, hc.classify_windows(hc.default_model(), ws), xb)
+    colsum = torch.zeros(a.num_cols, dtype=torch.float64, device="cuda")
+    colsum.index_add_(0, a.col_idx.long(), a.values.double())
+    want = colsum @ xb.double()
+    got = res.z.data.double().sum(0)
+    assert float((got - want).abs().max() / want.abs().max()) <= 1e-3
+    # row spot-check against exact fp64 on 200 random rows
+    rows = torch.randint(0, a.num_rows, (200,), generator=torch.Generator().manual_seed(0))
+    rp = a.row_ptr.cpu()
+    for r in rows.tolist()[:50]:
+        lo, hi = int(rp[r]), int(rp[r + 1])
+        cols = a.col_idx[lo:hi].long()
+        exact = (a.values[lo:hi].double()[:, None] * xb[cols].double()).sum(0)
+        scale = float(res.z.data.double().abs().max())
+        assert float((res.z.data[r].double() - exact).abs().max()) / scale <= BF16_TOL
