@@ -39,8 +39,8 @@ int hcs_device_sm_count(void);
  * windows.py:81-106 partition + windows.py:109-123 features +
  * selector.py:48-64 SelectorModel.score/decide + classify_windows.
  * Window w covers rows [w*wh, min((w+1)*wh, n_rows)); W = ceil(n_rows/wh).
- * selector: the 7 doubles {w_ncols, w_density, bias, mean0, mean1, scale0,
- * scale1} (data/default_selector.json) or NULL to skip classification.
+ * selector: HOST pointer to the 7 doubles {w_ncols, w_density, bias, mean0, mean1,
+ * scale0, scale1} (data/selector_default.json) or NULL to skip classification.
  * Two phases sharing one caller-owned workspace:
  *   count: win_col_ptr[W+1] (exclusive prefix of ncols), density[W], ci[W], codes[W]
  *   fill : nonzero_cols[win_col_ptr[W]] (ascending per window), cond_cols[nnz]
@@ -52,7 +52,8 @@ int hcs_partition_count(const int64_t* row_ptr, const int32_t* col_idx, int64_t 
 int hcs_partition_fill(const int64_t* row_ptr, const int32_t* col_idx, int64_t n_rows, int64_t n_cols, int64_t nnz,
                        int32_t wh, const int64_t* win_col_ptr, int32_t* nonzero_cols, int32_t* cond_cols,
                        void* workspace, size_t ws_bytes, void* stream);
-/* selector.py:48-56 on caller-given features (classify_windows with a non-default model) */
+/* selector.py:48-56 on caller-given features (classify_windows with a non-default model);
+ * selector is a HOST pointer to the 7 doubles, the other pointers are device memory. */
 int hcs_classify(const int64_t* win_col_ptr, const double* density, int64_t n_windows, const double* selector,
                  uint8_t* codes, void* stream);
 

@@ -5,42 +5,37 @@
 // gathered X rows; here each chunk is one K=64 step of
 //     D[f][r] += sum_k Xg[k][f] * S[r][k]            (D = Z^T of the window)
 // issued as 4 x tcgen05.mma.kind::f16 (M=128 features, N=16 window rows, K=16):
-//   A = gathered X rows, MN-major, 128B-swizzled, staged by cp.async (LDGSTS)
+//   A = gathered X rows, MN-major, 64B/128B-swizzled, staged by cp.async (LDGSTS)
 //   B = the window's 16 x 64 slab, K-major, 128B-swizzled, built in smem
-//   D = fp32 accumulator in TMEM (two 16-column buffers: MMA of window i+1
-//       overlaps the epilogue of window i).
-// Warp roles (persistent CTA per SM):
-//   w0-w1 producers  : cp.async 16B gathers of X rows + staged packed entries
-//   w2    builder    : zero + scatter the chunk's entries into the B slab
-//   w3    MMA issuer : one elected lane issues tcgen05.mma, commits to mbarriers
-//   w4-w7 epilogue   : tcgen05.ld -> fp32 Z rows (coalesced 128B stores)
-// Gathering with cp.async instead of TMA tile::gather4: measured on B200,
-// gather4 sustains ~2.3 TB/s of 128B rows, LDG/LDGSTS row gathers ~13 TB/s
-// from L2 (tools/probe, profiles/r01_probe.md).
+//   D = fp32 accumulator in TMEM (two 16-column buffers: the MMAs of window i+1
+//       overlap the epilogue of window i).
+// A pipeline stage holds G chunks (16 KB of gathered rows): G = 1 for dim <= 128,
+// 2 for dim <= 64, 4 for dim <= 32, so per-stage overheads are amortised evenly.
+//
+// Warp roles (persistent CTA per SM, 12 warps):
+//   w0-w3  producers : gather-index prefetch (cp.async into an index ring, D stages
+//                      ahead) + 16-byte cp.async row gathers + packed-entry staging;
+//                      completion tracked per thread with commit/wait_group, then
+//                      published on an mbarrier.
+//   w4-w5  builders  : zero + scatter a stage's entries into its B slabs (alternating)
+//   w6     MMA       : one lane issues tcgen05.mma and commits to mbarriers
+//   w8-w11 epilogue  : tcgen05.ld -> fp32 Z rows (coalesced 128B stores)
+// Why cp.async and not TMA tile::gather4: on B200 gather4 sustains ~2.3 TB/s of
+// 128B rows (one row per ~18 cycles per SM) while LDG/LDGSTS row gathers reach
+// ~13 TB/s from L2 (tools/probe, profiles/).  Control data (indices, entry
+// pointers) is prefetched far ahead because loads complete in issue order behind
+// the gathers in the SM's L1TEX queue.
 #include "common.cuh"
 
 namespace hcs {
 
-constexpr int kTileThreads = 256;
-constexpr int kEntCap = 512;  // staged packed entries per chunk (2 KB); rest read from global
-
-struct TileSmem {
-  int stages;
-  uint32_t a_bytes;     // per stage
-  uint32_t off_a, off_slab, off_ent, off_bar, total;
-};
-
-__host__ __device__ inline TileSmem tile_smem_layout(int nblk, int stages) {
-  TileSmem L;
-  L.stages = stages;
-  L.a_bytes = (uint32_t)nblk * 64 * 128;
-  L.off_a = 0;
-  L.off_slab = L.off_a + stages * L.a_bytes;
-  L.off_ent = L.off_slab + stages * 2048;
-  L.off_bar = L.off_ent + stages * kEntCap * 4;
-  L.total = L.off_bar + (3 * stages + 4) * 8 + 16;
-  return L;
-}
+constexpr int kProducers = 8;   // warps 0-7: X-row gathers
+constexpr int kBuilders = 2;    // warps 8-9: B slabs
+constexpr int kMmaWarp = 10;    // warp 10: tcgen05.mma issuer
+constexpr int kCtrlWarp = 11;   // warp 11: packed-entry staging + stage records
+constexpr int kEpiWarp0 = 12;   // warps 12-15: epilogue (TMEM lane quadrants 0-3)
+constexpr int kTileThreads = 16 * 32;
+constexpr int kEntCapPerChunk = 128;  // staged packed entries per chunk; the rest is read from global
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes, uint64_t pol) {
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(dst), "l"(src),
@@ -50,10 +45,12 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32
 __device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
 }
-__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-
 
 // first t in [0, n] with a[t] >= v  (a non-decreasing, length n+1)
 __device__ __forceinline__ int64_t lower_bound_i64(const int64_t* __restrict__ a, int64_t n, int64_t v) {
@@ -65,53 +62,136 @@ __device__ __forceinline__ int64_t lower_bound_i64(const int64_t* __restrict__ a
   return lo;
 }
 
-// warp-cooperative prefetching reader of a monotone int64 array (e.g. ent_ptr):
-// lanes hold a[base .. base+63]; get(i) for base <= i < base+64.
+// Warp-cooperative prefetching reader of a monotone int64 array: lanes hold
+// a[base .. base+95] in three registers; get(i) for base <= i < base+64.  The
+// third block is requested 32+ steps before it is read.
 struct I64Window {
   const int64_t* p;
-  int64_t base, lim;  // valid indices < lim
-  int64_t a, b;
+  int64_t base, lim;
+  int64_t a, b, c;
+  __device__ __forceinline__ int64_t ld(int64_t i) const { return i < lim ? p[i] : 0; }
   __device__ __forceinline__ void init(const int64_t* p_, int64_t base_, int64_t lim_, int lane) {
     p = p_; base = base_; lim = lim_;
-    a = (base + lane < lim) ? p[base + lane] : 0;
-    b = (base + 32 + lane < lim) ? p[base + 32 + lane] : 0;
+    a = ld(base + lane);
+    b = ld(base + 32 + lane);
+    c = ld(base + 64 + lane);
   }
   __device__ __forceinline__ void advance(int64_t i, int lane) {
     while (i >= base + 32) {
       a = b;
+      b = c;
       base += 32;
-      b = (base + 32 + lane < lim) ? p[base + 32 + lane] : 0;
+      c = ld(base + 64 + lane);
     }
   }
   __device__ __forceinline__ int64_t get(int64_t i) const {
-    int d = (int)(i - base);
-    int64_t va = __shfl_sync(0xffffffffu, a, d & 31);
-    int64_t vb = __shfl_sync(0xffffffffu, b, d & 31);
-    return d < 32 ? va : vb;
+    const int d = (int)(i - base);  // warp-uniform
+    return d < 32 ? __shfl_sync(0xffffffffu, a, d) : __shfl_sync(0xffffffffu, b, d - 32);
   }
 };
 
-template <int NBLK>
+// Deterministic stage sequence shared by every role: windows t in [tb0, tb1),
+// each split into stages of up to G consecutive chunks.
+template <int G>
+struct StageIter {
+  I64Window cp;  // chunk_ptr
+  int64_t t, tb1, c, c_end;
+  __device__ __forceinline__ void init(const int64_t* chunk_ptr, int64_t tb0, int64_t tb1_, int lane) {
+    cp.init(chunk_ptr, tb0, tb1_ + 1, lane);
+    t = tb0;
+    tb1 = tb1_;
+    if (t < tb1) {
+      c = cp.get(t);
+      c_end = cp.get(t + 1);
+    }
+  }
+  __device__ __forceinline__ bool valid() const { return t < tb1; }
+  __device__ __forceinline__ int g() const { return (int)(c_end - c < G ? c_end - c : G); }
+  __device__ __forceinline__ bool first(int64_t c0) const { return c == c0; }
+  __device__ __forceinline__ bool last() const { return c + G >= c_end; }
+  __device__ __forceinline__ void next(int lane) {
+    c += G;
+    if (c >= c_end) {
+      ++t;
+      if (t < tb1) {
+        cp.advance(t, lane);
+        c = cp.get(t);
+        c_end = cp.get(t + 1);
+      }
+    }
+  }
+};
+
+template <int VEC>
+struct TileCfg {
+  // VEC: 16-byte vectors per gathered row (dim <= 8*VEC)
+  static constexpr int ROWB = VEC <= 4 ? 64 : 128;             // smem bytes per gathered row per MN block
+  static constexpr int NBLK = VEC > 8 ? 2 : 1;                 // MN (feature) blocks of 64 bf16
+  static constexpr int G = VEC <= 4 ? 4 : (VEC <= 8 ? 2 : 1);  // chunks per stage
+  static constexpr int LAYOUT = ROWB == 64 ? 4 : 2;             // UMMA SWIZZLE_64B / SWIZZLE_128B
+  static constexpr int SBO = 8 * ROWB;                          // 8-row swizzle atom
+  static constexpr int CHUNK_A = 64 * ROWB;                     // bytes of one chunk in one MN block
+  static constexpr int STAGE_A = G * CHUNK_A * NBLK;            // 16 KB
+  static constexpr int STAGE_SLAB = G * 2048;
+  static constexpr int STAGE_ENT = G * kEntCapPerChunk * 4;
+  static constexpr int STAGE_BYTES = STAGE_A + STAGE_SLAB + STAGE_ENT;
+  static constexpr int IDX_SLOT = G * 64 * 4;
+  static constexpr int STAGES = (200 * 1024 - 16 * IDX_SLOT) / STAGE_BYTES;
+  static constexpr int INFLIGHT = STAGES - 2;  // stages of gathers in flight per producer thread
+  static constexpr int IDX_DIST = INFLIGHT + 1;  // index prefetch distance (stages)
+  static constexpr int IDX_SLOTS = IDX_DIST + 1;
+  static constexpr int OFF_A = 0;
+  static constexpr int OFF_SLAB = OFF_A + STAGES * STAGE_A;
+  static constexpr int OFF_ENT = OFF_SLAB + STAGES * STAGE_SLAB;
+  static constexpr int OFF_IDX = OFF_ENT + STAGES * STAGE_ENT;
+  static constexpr int OFF_INFO = OFF_IDX + IDX_SLOTS * IDX_SLOT;
+  static constexpr int OFF_BAR = OFF_INFO + STAGES * 64;
+  static constexpr int SMEM = OFF_BAR + (3 * STAGES + 4) * 8 + 16 + 1024;  // + alignment slack
+  static_assert(SMEM <= 227 * 1024, "tile kernel shared memory budget");
+  static_assert(STAGES >= 4, "pipeline too shallow");
+};
+
+// Per-stage record written by producer warp 0 (visible to consumers through the
+// full -> built mbarrier chain): entry pointers of the stage's chunks and flags.
+struct StageInfo {
+  int64_t ep[5];  // ent_ptr[c .. c+g]
+  int32_t g;
+  int32_t flags;  // bit0: first stage of a window, bit1: last stage of a window
+};
+
+// number of stages of windows [tb0, tb1) (warp-cooperative)
+template <int G>
+__device__ __forceinline__ int64_t count_stages(const int64_t* __restrict__ chunk_ptr, int64_t tb0, int64_t tb1,
+                                                int lane) {
+  int64_t n = 0;
+  for (int64_t t = tb0 + lane; t < tb1; t += 32) n += (chunk_ptr[t + 1] - chunk_ptr[t] + G - 1) / G;
+  for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+  return n;
+}
+
+template <int VEC>
 __global__ void __launch_bounds__(kTileThreads, 1)
     k_spmm_tile_bf16(const int32_t* __restrict__ tile_list, int64_t T, const int64_t* __restrict__ chunk_ptr,
                      const int32_t* __restrict__ gidx, const int64_t* __restrict__ ent_ptr,
                      const uint32_t* __restrict__ ent, int64_t n_rows, int wh, const __nv_bfloat16* __restrict__ x,
-                     int64_t ldx, int vec, int dim, float* __restrict__ z, int64_t ldz, int stages) {
+                     int64_t ldx, int vec, int dim, float* __restrict__ z, int64_t ldz) {
+  using C = TileCfg<VEC>;
+  constexpr int S = C::STAGES, G = C::G;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const TileSmem L = tile_smem_layout(NBLK, stages);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.off_bar);
-  uint64_t* full = bars;
-  uint64_t* built = bars + stages;
-  uint64_t* empty = bars + 2 * stages;
-  uint64_t* accf = bars + 3 * stages;
-  uint64_t* acce = accf + 2;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+  uint64_t* full = bars;           // S: gathers + staged entries landed (kProducers arrivals)
+  uint64_t* built = bars + S;      // S: B slabs built (1 arrival)
+  uint64_t* empty = bars + 2 * S;  // S: MMAs of the stage done (tcgen05.commit)
+  uint64_t* accf = bars + 3 * S;   // 2: accumulator ready for the epilogue
+  uint64_t* acce = accf + 2;       // 2: accumulator drained (4 epilogue warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
+  StageInfo* info = reinterpret_cast<StageInfo*>(smem + C::OFF_INFO);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < stages; ++s) {
-      mbar_init(&full[s], 64);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], kProducers + 1);  // producers + control warp
       mbar_init(&built[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -128,115 +208,211 @@ __global__ void __launch_bounds__(kTileThreads, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t sbase = smem_u32(smem);
   // contiguous, chunk-balanced range of tile windows for this CTA
-  const int64_t C = chunk_ptr[T];
-  const int64_t G = gridDim.x;
-  const int64_t tb0 = lower_bound_i64(chunk_ptr, T, (C * (int64_t)blockIdx.x) / G);
-  const int64_t tb1 = lower_bound_i64(chunk_ptr, T, (C * ((int64_t)blockIdx.x + 1)) / G);
-  const int64_t cb0 = chunk_ptr[tb0], cb1 = chunk_ptr[tb1];
+  const int64_t Ctot = chunk_ptr[T];
+  const int64_t Gd = gridDim.x;
+  const int64_t tb0 = lower_bound_i64(chunk_ptr, T, (Ctot * (int64_t)blockIdx.x) / Gd);
+  const int64_t tb1 = lower_bound_i64(chunk_ptr, T, (Ctot * ((int64_t)blockIdx.x + 1)) / Gd);
 
-  if (warp < 2) {
-    // ------------------------------------------------------------ producers
+  if (warp < kProducers) {
+    // ================================================================ producers
     const uint64_t keep = policy_evict_last();
-    const uint64_t strm = stream_policy();
     const int p = warp;
-    int stage = 0;
-    uint32_t phase = 0;
-    const int32_t* gp = gidx + 32 * p + lane;
-    // gather-index prefetch ring, distance 4 chunks
-    int i0 = (cb0 + 0 < cb1) ? ld_stream_s32(gp + (cb0 + 0) * 64, strm) : -1;
-    int i1 = (cb0 + 1 < cb1) ? ld_stream_s32(gp + (cb0 + 1) * 64, strm) : -1;
-    int i2 = (cb0 + 2 < cb1) ? ld_stream_s32(gp + (cb0 + 2) * 64, strm) : -1;
-    int i3 = (cb0 + 3 < cb1) ? ld_stream_s32(gp + (cb0 + 3) * 64, strm) : -1;
-    I64Window ep;
-    ep.init(ent_ptr, cb0, cb1 + 1, lane);
-    for (int64_t ch = cb0; ch < cb1; ++ch) {
-      const int cur_idx = i0;
-      i0 = i1; i1 = i2; i2 = i3;
-      i3 = (ch + 4 < cb1) ? ld_stream_s32(gp + (ch + 4) * 64, strm) : -1;
-      ep.advance(ch, lane);
-      const int64_t e_lo = ep.get(ch), e_hi = ep.get(ch + 1);
-      mbar_wait(&empty[stage], phase ^ 1);
-      const uint32_t a_st = sbase + L.off_a + stage * L.a_bytes;
-      for (int o = lane; o < 32 * vec; o += 32) {
-        const int r = o / vec, v = o - r * vec;
-        const int gi = __shfl_sync(__activemask(), cur_idx, r);
-        const int row = 32 * p + r;
-        const uint32_t dst = a_st + (uint32_t)(v >> 3) * 8192u + (uint32_t)row * 128u +
-                             ((uint32_t)((v & 7) ^ (row & 7)) << 4);
-        const __nv_bfloat16* src = (gi >= 0) ? x + (int64_t)gi * ldx + v * 8 : x;
-        cp_async16(dst, src, gi >= 0 ? 16u : 0u, keep);
-      }
-      if (p == 0) {
-        const int ne = (int)(e_hi - e_lo < kEntCap ? e_hi - e_lo : kEntCap);
-        const uint32_t e_st = sbase + L.off_ent + stage * kEntCap * 4;
-        for (int i = lane; i < ne; i += 32) cp_async4(e_st + i * 4, ent + e_lo + i);
-      }
-      cp_async_arrive_noinc(&full[stage]);
-      if (++stage == stages) { stage = 0; phase ^= 1; }
+    constexpr int ROWS_W = 64 * G / kProducers;  // rows of a stage gathered by this warp
+    constexpr int RPI = 32 / VEC;                // rows per warp instruction
+    constexpr int ITERS = ROWS_W * VEC / 32;
+    static_assert(ITERS >= 1 && ROWS_W % RPI == 0, "producer row split");
+    const int lrow = lane / VEC, v = lane % VEC;
+    const int row0 = ROWS_W * p;  // first stage row of this warp
+    const char* xl = reinterpret_cast<const char*>(x + v * 8);
+    const int64_t ldxb = ldx * 2;
+    const uint32_t vbytes = (v < vec) ? 16u : 0u;  // lanes past dim zero-fill
+    // per-iteration smem destination offsets (relative to the stage's A base)
+    uint32_t dofs[ITERS];
+#pragma unroll
+    for (int it = 0; it < ITERS; ++it) {
+      const int row = row0 + it * RPI + lrow;
+      const int jch = row >> 6, r = row & 63, vchunk = v & 7;
+      uint32_t d = (uint32_t)(v >> 3) * (uint32_t)(G * C::CHUNK_A) + (uint32_t)jch * C::CHUNK_A;
+      if (C::ROWB == 128) d += (uint32_t)r * 128u + ((uint32_t)(vchunk ^ (r & 7)) << 4);
+      else d += (uint32_t)(r >> 3) * 512u + (uint32_t)(r & 7) * 64u + ((uint32_t)((vchunk ^ ((r & 7) >> 1)) & 3) << 4);
+      dofs[it] = d;
     }
-  } else if (warp == 2) {
-    // ------------------------------------------------------------ slab builder
-    int stage = 0;
+    StageIter<G> cur, lead;
+    cur.init(chunk_ptr, tb0, tb1, lane);
+    lead.init(chunk_ptr, tb0, tb1, lane);
+    // index prefetch of one stage: this warp's ROWS_W indices -> ring slot (ROWS_W/4 lanes x 16 B)
+    auto prefetch_idx = [&](const StageIter<G>& it, int slot) {
+      if (lane < ROWS_W / 4) {
+        const bool ok = row0 + lane * 4 < it.g() * 64;
+        const uint32_t dst = sbase + C::OFF_IDX + slot * C::IDX_SLOT + (row0 + lane * 4) * 4;
+        cp_async16(dst, ok ? (const void*)(gidx + it.c * 64 + row0 + lane * 4) : (const void*)gidx, ok ? 16u : 0u,
+                   keep);
+      }
+    };
+    int lead_n = 0;
+    for (; lead_n < C::IDX_DIST && lead.valid(); ++lead_n) {
+      prefetch_idx(lead, lead_n % C::IDX_SLOTS);
+      lead.next(lane);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
+
+    int stage = 0, sig = 0, pending = 0, idx_slot = 0, lead_slot = C::IDX_DIST % C::IDX_SLOTS;
     uint32_t phase = 0;
+    for (; cur.valid(); cur.next(lane)) {
+      const int g = cur.g();
+      mbar_wait(&empty[stage], phase ^ 1);
+      const int32_t* idx_s =
+          reinterpret_cast<const int32_t*>(smem + C::OFF_IDX + idx_slot * C::IDX_SLOT) + row0 + lrow;
+      const uint32_t a_st = sbase + C::OFF_A + stage * C::STAGE_A;
+      const int lim = g * 64 - row0 - lrow;  // rows it*RPI < lim are valid
+#pragma unroll
+      for (int it = 0; it < ITERS; ++it) {
+        if (g == G || it * RPI < lim) {
+          const int gi = idx_s[it * RPI];
+          const char* src = xl + (int64_t)max(gi, 0) * ldxb;
+          cp_async16(a_st + dofs[it], src, gi >= 0 ? vbytes : 0u, keep);
+        }
+      }
+      // gather indices IDX_DIST stages ahead (its ring slot was read one stage ago)
+      if (lead.valid()) {
+        prefetch_idx(lead, lead_slot);
+        lead.next(lane);
+      }
+      if (++lead_slot == C::IDX_SLOTS) lead_slot = 0;
+      if (++idx_slot == C::IDX_SLOTS) idx_slot = 0;
+      cp_async_commit();
+      if (++pending > C::INFLIGHT) {  // oldest in-flight stage has landed -> publish it
+        cp_async_wait<C::INFLIGHT>();
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[sig]);
+        if (++sig == S) sig = 0;
+        --pending;
+      }
+      if (++stage == S) { stage = 0; phase ^= 1; }
+    }
+    cp_async_wait<0>();
+    fence_proxy_async_smem();
+    __syncwarp();
+    for (; pending > 0; --pending) {
+      if (lane == 0) mbar_arrive(&full[sig]);
+      if (++sig == S) sig = 0;
+    }
+  } else if (warp == kCtrlWarp) {
+    // ================================================================ control: entries + stage records
+    StageIter<G> cur;
+    cur.init(chunk_ptr, tb0, tb1, lane);
     I64Window ep;
-    ep.init(ent_ptr, cb0, cb1 + 1, lane);
-    for (int64_t ch = cb0; ch < cb1; ++ch) {
-      ep.advance(ch, lane);
-      const int64_t e_lo = ep.get(ch), e_hi = ep.get(ch + 1);
+    ep.init(ent_ptr, tb0 < tb1 ? chunk_ptr[tb0] : 0, chunk_ptr[tb1] + 1, lane);
+    int stage = 0, sig = 0, pending = 0;
+    uint32_t phase = 0;
+    int64_t c0w = cur.valid() ? cur.c : 0;  // first chunk of the current window
+    for (; cur.valid(); cur.next(lane)) {
+      const int g = cur.g();
+      ep.advance(cur.c, lane);
+      int64_t epj[G + 1];
+#pragma unroll
+      for (int j = 0; j <= G; ++j) epj[j] = ep.get(cur.c + (j <= g ? j : g));
+      const bool first = cur.c == c0w, last = cur.last();
+      if (last) c0w = cur.c_end;
+      mbar_wait(&empty[stage], phase ^ 1);
+      if (lane == 0) {
+#pragma unroll
+        for (int j = 0; j <= G; ++j) info[stage].ep[j] = epj[j];
+        info[stage].g = g;
+        info[stage].flags = (first ? 1 : 0) | (last ? 2 : 0);
+      }
+      const int ne = (int)(epj[G] - epj[0]);
+      const int cap = G * kEntCapPerChunk;
+      const int nstg = ne < cap ? ne : cap;
+      const uint32_t e_st = sbase + C::OFF_ENT + stage * C::STAGE_ENT;
+      for (int i = lane; i < nstg; i += 32) cp_async4(e_st + i * 4, ent + epj[0] + i);
+      cp_async_commit();
+      if (++pending > C::INFLIGHT) {
+        cp_async_wait<C::INFLIGHT>();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[sig]);
+        if (++sig == S) sig = 0;
+        --pending;
+      }
+      if (++stage == S) { stage = 0; phase ^= 1; }
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+    for (; pending > 0; --pending) {
+      if (lane == 0) mbar_arrive(&full[sig]);
+      if (++sig == S) sig = 0;
+    }
+  } else if (warp < kProducers + kBuilders) {
+    // ================================================================ slab builders (alternate stages)
+    const int b = warp - kProducers;
+    const int64_t nst = count_stages<G>(chunk_ptr, tb0, tb1, lane);
+    for (int64_t n = b; n < nst; n += kBuilders) {
+      const int stage = (int)(n % S);
+      const uint32_t phase = (uint32_t)((n / S) & 1);
       mbar_wait(&full[stage], phase);
-      uint8_t* slab = smem + L.off_slab + stage * 2048;
+      const StageInfo& inf = info[stage];
+      const int g = inf.g;
+      const int64_t e0 = inf.ep[0];
+      uint8_t* slab = smem + C::OFF_SLAB + stage * C::STAGE_SLAB;
       const int4 zero4 = make_int4(0, 0, 0, 0);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) reinterpret_cast<int4*>(slab)[lane + 32 * i] = zero4;
+      for (int i = 0; i < G * 4; ++i) reinterpret_cast<int4*>(slab)[lane + 32 * i] = zero4;
       __syncwarp();
-      const uint32_t* es = reinterpret_cast<const uint32_t*>(smem + L.off_ent + stage * kEntCap * 4);
-      const int ne = (int)(e_hi - e_lo);
-      for (int i = lane; i < ne; i += 32) {
-        const uint32_t w = (i < kEntCap) ? es[i] : ent[e_lo + i];
-        const uint32_t pos = w & 1023u;
-        *reinterpret_cast<uint16_t*>(slab + sw128_kmajor_off16(pos >> 6, pos & 63u)) = (uint16_t)(w >> 16);
+      const uint32_t* es = reinterpret_cast<const uint32_t*>(smem + C::OFF_ENT + stage * C::STAGE_ENT);
+      const int cap = G * kEntCapPerChunk;
+      for (int j = 0; j < g; ++j) {
+        const int lo = (int)(inf.ep[j] - e0), hi = (int)(inf.ep[j + 1] - e0);
+        uint8_t* sl = slab + j * 2048;
+        for (int i = lo + lane; i < hi; i += 32) {
+          const uint32_t w = (i < cap) ? es[i] : ent[e0 + i];
+          const uint32_t pos = w & 1023u;
+          *reinterpret_cast<uint16_t*>(sl + sw128_kmajor_off16(pos >> 6, pos & 63u)) = (uint16_t)(w >> 16);
+        }
       }
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&built[stage]);
-      if (++stage == stages) { stage = 0; phase ^= 1; }
     }
-  } else if (warp == 3) {
-    // ------------------------------------------------------------ MMA issuer
+  } else if (warp == kMmaWarp) {
+    // ================================================================ MMA issuer
     constexpr uint32_t idesc = umma_idesc(128, 16, 1, 1, 1, 0);
-    const uint32_t lbo = (NBLK == 2) ? 8192u : 0u;  // NBLK==1: features 64..127 alias 0..63 (discarded)
-    int stage = 0;
-    uint32_t phase = 0;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (int64_t t = tb0; t < tb1; ++t) {
-      const int64_t c0 = chunk_ptr[t], c1 = chunk_ptr[t + 1];
-      mbar_wait(&acce[acc], acc_phase ^ 1);
+    // A: MN-major; NBLK == 2 -> second 64-feature block G*CHUNK_A bytes away.
+    // NBLK == 1 (dim <= 64): LBO = 0 makes feature rows 64..127 alias 0..63 (discarded).
+    const uint32_t lbo = (C::NBLK == 2) ? (uint32_t)(G * C::CHUNK_A) : 0u;
+    constexpr uint32_t KSTEP_A = 16 * C::ROWB;  // 16 gathered rows per K=16 MMA
+    const int64_t nst = count_stages<G>(chunk_ptr, tb0, tb1, lane);
+    int stage = 0, acc = 0;
+    uint32_t phase = 0, acc_phase = 0;
+    for (int64_t n = 0; n < nst; ++n) {
+      mbar_wait(&built[stage], phase);
+      const int g = info[stage].g, flags = info[stage].flags;
+      const bool first = flags & 1, last = flags & 2;
+      if (first) mbar_wait(&acce[acc], acc_phase ^ 1);
+      fence_proxy_async_smem();
       tc_fence_after();
-      for (int64_t ch = c0; ch < c1; ++ch) {
-        mbar_wait(&built[stage], phase);
-        fence_proxy_async_smem();
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t a_st = sbase + L.off_a + stage * L.a_bytes;
-          const uint32_t b_st = sbase + L.off_slab + stage * 2048;
+      if (lane == 0) {
+        const uint32_t a_st = sbase + C::OFF_A + stage * C::STAGE_A;
+        const uint32_t b_st = sbase + C::OFF_SLAB + stage * C::STAGE_SLAB;
+        for (int j = 0; j < g; ++j) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            const uint64_t ad = umma_sdesc(a_st + k * 2048, lbo, 1024);
-            const uint64_t bd = umma_sdesc(b_st + k * 32, 0, 1024);
-            umma_f16(tmem + acc * 16, ad, bd, idesc, (ch > c0 || k > 0) ? 1u : 0u);
+            const uint64_t ad = umma_sdesc(a_st + j * C::CHUNK_A + k * KSTEP_A, lbo, C::SBO, C::LAYOUT);
+            const uint64_t bd = umma_sdesc(b_st + j * 2048 + k * 32, 0, 1024, 2);
+            umma_f16(tmem + acc * 16, ad, bd, idesc, (first && j == 0 && k == 0) ? 0u : 1u);
           }
-          umma_commit(&empty[stage]);
         }
-        __syncwarp();
-        if (++stage == stages) { stage = 0; phase ^= 1; }
+        umma_commit(&empty[stage]);
+        if (last) umma_commit(&accf[acc]);
       }
-      if (lane == 0) umma_commit(&accf[acc]);
       __syncwarp();
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (last && ++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (++stage == S) { stage = 0; phase ^= 1; }
     }
-  } else {
-    // ------------------------------------------------------------ epilogue
+  } else if (warp >= kEpiWarp0) {
+    // ================================================================ epilogue
     const int q = warp & 3;  // TMEM lane quadrant accessible to this warp
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -245,7 +421,9 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       const int64_t w = tile_list[t];
       const int64_t rs = w * wh;
       const int rows = (int)(n_rows - rs < wh ? n_rows - rs : wh);
-      mbar_wait(&accf[acc], acc_phase);
+      // one warp polls the mbarrier; the other three block on a named barrier (no spinning)
+      if (q == 0) mbar_wait(&accf[acc], acc_phase);
+      named_bar_sync(1, 128);
       tc_fence_after();
       uint32_t r[16];
       tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + acc * 16, r);
@@ -256,8 +434,8 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       if (f < dim) {
         float* zp = z + rs * ldz + f;
 #pragma unroll
-        for (int n = 0; n < 16; ++n)
-          if (n < rows) __stcs(zp + (int64_t)n * ldz, __uint_as_float(r[n]));
+        for (int nr = 0; nr < 16; ++nr)
+          if (nr < rows) __stcs(zp + (int64_t)nr * ldz, __uint_as_float(r[nr]));
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
@@ -265,6 +443,19 @@ __global__ void __launch_bounds__(kTileThreads, 1)
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc<32>(tmem);
+}
+
+template <int VEC>
+static int launch_tile(int grid, cudaStream_t st, const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr,
+                       const int32_t* gidx, const int64_t* ent_ptr, const uint32_t* ent, int64_t n_rows, int wh,
+                       const __nv_bfloat16* x, int64_t ldx, int vec, int d, float* z, int64_t ldz) {
+  using C = TileCfg<VEC>;
+  auto kern = k_spmm_tile_bf16<VEC>;
+  HCS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+  kern<<<grid, kTileThreads, C::SMEM, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, vec,
+                                            d, z, ldz);
+  HCS_LAUNCH_CHECK("k_spmm_tile_bf16");
+  return HCS_OK;
 }
 
 }  // namespace hcs
@@ -284,27 +475,17 @@ extern "C" int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int
   if (n_tile == 0) return HCS_OK;
   cudaStream_t st = as_stream(stream);
   const int grid = (int)std::min<int64_t>(n_tile, num_sms());
+  const uint32_t* e = (const uint32_t*)ent;
   for (int f0 = 0; f0 < dim; f0 += 128) {
     const int d = std::min(128, dim - f0);
     const int vec = (d + 7) / 8;
-    const int nblk = vec > 8 ? 2 : 1;
-    int stages = nblk == 2 ? 10 : 16;
-    TileSmem L = tile_smem_layout(nblk, stages);
-    size_t smem = L.total + 1024;
     const __nv_bfloat16* xs = reinterpret_cast<const __nv_bfloat16*>(x) + f0;
     float* zs = z + f0;
-    if (nblk == 2) {
-      HCS_CUDA(cudaFuncSetAttribute(k_spmm_tile_bf16<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      k_spmm_tile_bf16<2><<<grid, kTileThreads, smem, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr,
-                                                            (const uint32_t*)ent, n_rows, wh, xs, ldx, vec, d, zs, ldz,
-                                                            stages);
-    } else {
-      HCS_CUDA(cudaFuncSetAttribute(k_spmm_tile_bf16<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      k_spmm_tile_bf16<1><<<grid, kTileThreads, smem, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr,
-                                                            (const uint32_t*)ent, n_rows, wh, xs, ldx, vec, d, zs, ldz,
-                                                            stages);
-    }
-    HCS_LAUNCH_CHECK("k_spmm_tile_bf16");
+    int rc;
+    if (vec > 8) rc = launch_tile<16>(grid, st, tile_list, n_tile, chunk_ptr, gidx, ent_ptr, e, n_rows, wh, xs, ldx, vec, d, zs, ldz);
+    else if (vec > 4) rc = launch_tile<8>(grid, st, tile_list, n_tile, chunk_ptr, gidx, ent_ptr, e, n_rows, wh, xs, ldx, vec, d, zs, ldz);
+    else rc = launch_tile<4>(grid, st, tile_list, n_tile, chunk_ptr, gidx, ent_ptr, e, n_rows, wh, xs, ldx, vec, d, zs, ldz);
+    if (rc) return rc;
   }
   (void)x_rows;
   return HCS_OK;

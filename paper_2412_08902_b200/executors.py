@@ -247,17 +247,15 @@ class HybridPlan:
 
 
 def get_plan(windows, assignment: Assignment, precision: str) -> HybridPlan:
+    """Plans are cached per WindowSet, keyed by the assignment's code CONTENT."""
+    import hashlib
+
     dev = windows.csr.device
-    codes = assignment.device_codes(dev)
-    key = (precision, codes.data_ptr(), int(codes.numel()))
+    key = (precision, hashlib.sha1(assignment.codes.tobytes()).hexdigest())
     plan = windows._plans.get(key)
     if plan is None:
-        if assignment._host is not None:
-            key = (precision, assignment.codes.tobytes())
-            plan = windows._plans.get(key)
-        if plan is None:
-            plan = HybridPlan(windows, codes, precision)
-            windows._plans[key] = plan
+        plan = HybridPlan(windows, assignment.device_codes(dev), precision)
+        windows._plans[key] = plan
     return plan
 
 

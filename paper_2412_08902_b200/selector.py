@@ -60,10 +60,10 @@ def classify_windows(model, windows) -> Assignment:
             dev = windows.win_col_ptr.device
             W = windows.num_windows
             codes = torch.empty(W, dtype=torch.uint8, device=dev)
-            sel_t = torch.tensor(sel, dtype=torch.float64, device=dev)
+            sel_c = (_lib.ctypes.c_double * 7)(*sel)
             if W:
                 _lib.call("hcs_classify", windows.win_col_ptr.data_ptr(), windows.density.data_ptr(), W,
-                          sel_t.data_ptr(), codes.data_ptr(), _lib.stream())
+                          _lib.ctypes.addressof(sel_c), codes.data_ptr(), _lib.stream())
         return Assignment.from_device(codes)
     return Assignment.from_paths(classify(model, features(w)) for w in windows)
 

@@ -202,7 +202,7 @@ def partition(csr, window_height: int = WINDOW_HEIGHT, model=None) -> WindowSet:
     n, nnz = d.num_rows, d.nnz
     W = -(-n // window_height)
     sel = _selector_doubles(model if model is not None else default_model())
-    sel_t = torch.tensor(sel, dtype=torch.float64, device=dev)
+    sel_c = (_lib.ctypes.c_double * 7)(*sel)  # host array (read on the host by the ABI)
     ws_bytes = _lib.ctypes.c_size_t(0)
     L = _lib.lib()
     _lib.check(L.hcs_partition_workspace_bytes(n, d.num_cols, nnz, window_height, _lib.ctypes.byref(ws_bytes)))
@@ -213,7 +213,7 @@ def partition(csr, window_height: int = WINDOW_HEIGHT, model=None) -> WindowSet:
     codes = torch.empty(W, dtype=torch.uint8, device=dev)
     s = _lib.stream()
     _lib.check(L.hcs_partition_count(d.row_ptr.data_ptr(), d.col_idx.data_ptr() if nnz else None, n, d.num_cols, nnz,
-                                     window_height, sel_t.data_ptr(), wcp.data_ptr(), dens.data_ptr(), ci.data_ptr(),
+                                     window_height, _lib.ctypes.addressof(sel_c), wcp.data_ptr(), dens.data_ptr(), ci.data_ptr(),
                                      codes.data_ptr(), ws.data_ptr(), ws.numel(), s))
     total = int(wcp[-1].item()) if W else 0
     nzc = torch.empty(max(total, 1), dtype=torch.int32, device=dev)[:total]

@@ -1,0 +1,7 @@
+#!/bin/bash
+# one gpurun session: smoke, gpu tests, short bench
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -20
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -40
+timeout 600 python bench.py --steps 50 --warmup 5 --cpu-budget 8 --sweep-dims 2>&1 | tail -20
