@@ -29,10 +29,12 @@
 
 namespace hcs {
 
-constexpr int kProducers = 8;   // warps 0-7: X-row gathers
-constexpr int kBuilders = 2;    // warps 8-9: B slabs
-constexpr int kMmaWarp = 10;    // warp 10: tcgen05.mma issuer
-constexpr int kCtrlWarp = 11;   // warp 11: packed-entry staging + stage records
+constexpr int kProducers = 4;   // warps 0-3: X-row gathers (cp.async)
+constexpr int kIdxWarp = 4;     // warp 4: gather-index ring loader (TMA bulk copies)
+constexpr int kEntWarp = 5;     // warp 5: packed-entry loader (TMA bulk copies) + stage records
+constexpr int kBuilder0 = 6;    // warps 6-7: B-slab builders (alternate stages)
+constexpr int kBuilders = 2;
+constexpr int kMmaWarp = 8;     // warp 8: tcgen05.mma issuer
 constexpr int kEpiWarp0 = 12;   // warps 12-15: epilogue (TMEM lane quadrants 0-3)
 constexpr int kTileThreads = 16 * 32;
 constexpr int kEntCapPerChunk = 128;  // staged packed entries per chunk; the rest is read from global
@@ -136,17 +138,18 @@ struct TileCfg {
   static constexpr int STAGE_ENT = G * kEntCapPerChunk * 4;
   static constexpr int STAGE_BYTES = STAGE_A + STAGE_SLAB + STAGE_ENT;
   static constexpr int IDX_SLOT = G * 64 * 4;
-  static constexpr int STAGES = (200 * 1024 - 16 * IDX_SLOT) / STAGE_BYTES;
-  static constexpr int INFLIGHT = STAGES - 2;  // stages of gathers in flight per producer thread
-  static constexpr int IDX_DIST = INFLIGHT + 1;  // index prefetch distance (stages)
-  static constexpr int IDX_SLOTS = IDX_DIST + 1;
+  static constexpr int IDX_SLOTS = 16;           // gather-index ring (TMA loader runs up to 16 stages ahead)
+  static constexpr int STAGES = (205 * 1024 - IDX_SLOTS * IDX_SLOT) / STAGE_BYTES;
+  static constexpr int INFLIGHT = STAGES - 2;    // stages of gathers in flight per producer thread
   static constexpr int OFF_A = 0;
   static constexpr int OFF_SLAB = OFF_A + STAGES * STAGE_A;
   static constexpr int OFF_ENT = OFF_SLAB + STAGES * STAGE_SLAB;
   static constexpr int OFF_IDX = OFF_ENT + STAGES * STAGE_ENT;
   static constexpr int OFF_INFO = OFF_IDX + IDX_SLOTS * IDX_SLOT;
-  static constexpr int OFF_BAR = OFF_INFO + STAGES * 64;
-  static constexpr int SMEM = OFF_BAR + (3 * STAGES + 4) * 8 + 16 + 1024;  // + alignment slack
+  static constexpr int OFF_IDXG = OFF_INFO + STAGES * 64;   // int g per index slot
+  static constexpr int OFF_BAR = OFF_IDXG + IDX_SLOTS * 4;
+  static constexpr int NBAR = 3 * STAGES + 4 + 2 * IDX_SLOTS;
+  static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;  // + alignment slack
   static_assert(SMEM <= 227 * 1024, "tile kernel shared memory budget");
   static_assert(STAGES >= 4, "pipeline too shallow");
 };
@@ -156,7 +159,8 @@ struct TileCfg {
 struct StageInfo {
   int64_t ep[5];  // ent_ptr[c .. c+g]
   int32_t g;
-  int32_t flags;  // bit0: first stage of a window, bit1: last stage of a window
+  int16_t flags;  // bit0: first stage of a window, bit1: last stage of a window
+  int16_t skew;   // staged entry i lives at ent_stage[skew + i] (16-byte aligned bulk copy)
 };
 
 // number of stages of windows [tb0, tb1) (warp-cooperative)
@@ -185,19 +189,26 @@ __global__ void __launch_bounds__(kTileThreads, 1)
   uint64_t* empty = bars + 2 * S;  // S: MMAs of the stage done (tcgen05.commit)
   uint64_t* accf = bars + 3 * S;   // 2: accumulator ready for the epilogue
   uint64_t* acce = accf + 2;       // 2: accumulator drained (4 epilogue warps)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
+  uint64_t* idx_full = acce + 2;                 // IDX_SLOTS: index slot loaded (TMA tx)
+  uint64_t* idx_empty = idx_full + C::IDX_SLOTS;  // IDX_SLOTS: index slot read by all producers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(idx_empty + C::IDX_SLOTS);
   StageInfo* info = reinterpret_cast<StageInfo*>(smem + C::OFF_INFO);
+  int32_t* idx_g = reinterpret_cast<int32_t*>(smem + C::OFF_IDXG);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], kProducers + 1);  // producers + control warp
+      mbar_init(&full[s], kProducers + 1);  // producers + entry loader (arrive.expect_tx)
       mbar_init(&built[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&accf[b], 1);
       mbar_init(&acce[b], 4);
+    }
+    for (int i = 0; i < C::IDX_SLOTS; ++i) {
+      mbar_init(&idx_full[i], 1);
+      mbar_init(&idx_empty[i], kProducers);
     }
     fence_barrier_init();
   }
@@ -226,8 +237,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     const char* xl = reinterpret_cast<const char*>(x + v * 8);
     const int64_t ldxb = ldx * 2;
     const uint32_t vbytes = (v < vec) ? 16u : 0u;  // lanes past dim zero-fill
-    // per-iteration smem destination offsets (relative to the stage's A base)
-    uint32_t dofs[ITERS];
+    uint32_t dofs[ITERS];  // per-iteration smem destination offsets (relative to the stage's A base)
 #pragma unroll
     for (int it = 0; it < ITERS; ++it) {
       const int row = row0 + it * RPI + lrow;
@@ -237,51 +247,29 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       else d += (uint32_t)(r >> 3) * 512u + (uint32_t)(r & 7) * 64u + ((uint32_t)((vchunk ^ ((r & 7) >> 1)) & 3) << 4);
       dofs[it] = d;
     }
-    StageIter<G> cur, lead;
-    cur.init(chunk_ptr, tb0, tb1, lane);
-    lead.init(chunk_ptr, tb0, tb1, lane);
-    // index prefetch of one stage: this warp's ROWS_W indices -> ring slot (ROWS_W/4 lanes x 16 B)
-    auto prefetch_idx = [&](const StageIter<G>& it, int slot) {
-      if (lane < ROWS_W / 4) {
-        const bool ok = row0 + lane * 4 < it.g() * 64;
-        const uint32_t dst = sbase + C::OFF_IDX + slot * C::IDX_SLOT + (row0 + lane * 4) * 4;
-        cp_async16(dst, ok ? (const void*)(gidx + it.c * 64 + row0 + lane * 4) : (const void*)gidx, ok ? 16u : 0u,
-                   keep);
-      }
-    };
-    int lead_n = 0;
-    for (; lead_n < C::IDX_DIST && lead.valid(); ++lead_n) {
-      prefetch_idx(lead, lead_n % C::IDX_SLOTS);
-      lead.next(lane);
-    }
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncwarp();
-
-    int stage = 0, sig = 0, pending = 0, idx_slot = 0, lead_slot = C::IDX_DIST % C::IDX_SLOTS;
-    uint32_t phase = 0;
-    for (; cur.valid(); cur.next(lane)) {
-      const int g = cur.g();
-      mbar_wait(&empty[stage], phase ^ 1);
+    const int nst = (int)count_stages<G>(chunk_ptr, tb0, tb1, lane);
+    int stage = 0, sig = 0, pending = 0, islot = 0;
+    uint32_t phase = 0, iphase = 0;
+    for (int n = 0; n < nst; ++n) {
+      mbar_wait(&idx_full[islot], iphase);
+      const int g = idx_g[islot];
       const int32_t* idx_s =
-          reinterpret_cast<const int32_t*>(smem + C::OFF_IDX + idx_slot * C::IDX_SLOT) + row0 + lrow;
+          reinterpret_cast<const int32_t*>(smem + C::OFF_IDX + islot * C::IDX_SLOT) + row0 + lrow;
+      int gi[ITERS];
+#pragma unroll
+      for (int it = 0; it < ITERS; ++it) gi[it] = idx_s[it * RPI];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&idx_empty[islot]);
+      if (++islot == C::IDX_SLOTS) { islot = 0; iphase ^= 1; }
+      mbar_wait(&empty[stage], phase ^ 1);
       const uint32_t a_st = sbase + C::OFF_A + stage * C::STAGE_A;
       const int lim = g * 64 - row0 - lrow;  // rows it*RPI < lim are valid
 #pragma unroll
       for (int it = 0; it < ITERS; ++it) {
-        if (g == G || it * RPI < lim) {
-          const int gi = idx_s[it * RPI];
-          const char* src = xl + (int64_t)max(gi, 0) * ldxb;
-          cp_async16(a_st + dofs[it], src, gi >= 0 ? vbytes : 0u, keep);
+        if (G == 1 || it * RPI < lim) {
+          cp_async16(a_st + dofs[it], xl + (int64_t)max(gi[it], 0) * ldxb, gi[it] >= 0 ? vbytes : 0u, keep);
         }
       }
-      // gather indices IDX_DIST stages ahead (its ring slot was read one stage ago)
-      if (lead.valid()) {
-        prefetch_idx(lead, lead_slot);
-        lead.next(lane);
-      }
-      if (++lead_slot == C::IDX_SLOTS) lead_slot = 0;
-      if (++idx_slot == C::IDX_SLOTS) idx_slot = 0;
       cp_async_commit();
       if (++pending > C::INFLIGHT) {  // oldest in-flight stage has landed -> publish it
         cp_async_wait<C::INFLIGHT>();
@@ -300,13 +288,34 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       if (lane == 0) mbar_arrive(&full[sig]);
       if (++sig == S) sig = 0;
     }
-  } else if (warp == kCtrlWarp) {
-    // ================================================================ control: entries + stage records
+  } else if (warp == kIdxWarp) {
+    // ================================================================ gather-index loader (TMA)
+    const uint64_t strm = policy_evict_first();
+    StageIter<G> cur;
+    cur.init(chunk_ptr, tb0, tb1, lane);
+    int islot = 0;
+    uint32_t iphase = 0;
+    for (; cur.valid(); cur.next(lane)) {
+      const int g = cur.g();
+      mbar_wait(&idx_empty[islot], iphase ^ 1);
+      if (lane == 0) {
+        idx_g[islot] = g;
+        mbar_expect_tx(&idx_full[islot], (uint32_t)g * 256u);
+        tma_bulk_g2s(sbase + C::OFF_IDX + islot * C::IDX_SLOT, gidx + cur.c * 64, (uint32_t)g * 256u,
+                     &idx_full[islot], strm);
+      }
+      __syncwarp();
+      if (++islot == C::IDX_SLOTS) { islot = 0; iphase ^= 1; }
+    }
+  } else if (warp == kEntWarp) {
+    // ================================================================ entry loader (TMA) + stage records
+    const uint64_t strm = policy_evict_first();
+    const char* entb = reinterpret_cast<const char*>(ent);
     StageIter<G> cur;
     cur.init(chunk_ptr, tb0, tb1, lane);
     I64Window ep;
     ep.init(ent_ptr, tb0 < tb1 ? chunk_ptr[tb0] : 0, chunk_ptr[tb1] + 1, lane);
-    int stage = 0, sig = 0, pending = 0;
+    int stage = 0;
     uint32_t phase = 0;
     int64_t c0w = cur.valid() ? cur.c : 0;  // first chunk of the current window
     for (; cur.valid(); cur.next(lane)) {
@@ -317,37 +326,26 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       for (int j = 0; j <= G; ++j) epj[j] = ep.get(cur.c + (j <= g ? j : g));
       const bool first = cur.c == c0w, last = cur.last();
       if (last) c0w = cur.c_end;
+      // 16-byte aligned superset of the stage's entries, capped to the staging buffer
+      const int64_t b0 = (epj[0] * 4) & ~(int64_t)15;
+      const int64_t b1 = (epj[G] * 4 + 15) & ~(int64_t)15;
+      const uint32_t bytes = (uint32_t)(b1 - b0 < C::STAGE_ENT ? b1 - b0 : C::STAGE_ENT);
       mbar_wait(&empty[stage], phase ^ 1);
       if (lane == 0) {
 #pragma unroll
         for (int j = 0; j <= G; ++j) info[stage].ep[j] = epj[j];
         info[stage].g = g;
-        info[stage].flags = (first ? 1 : 0) | (last ? 2 : 0);
+        info[stage].flags = (int16_t)((first ? 1 : 0) | (last ? 2 : 0));
+        info[stage].skew = (int16_t)((epj[0] * 4 - b0) >> 2);
+        mbar_expect_tx(&full[stage], bytes);
+        if (bytes) tma_bulk_g2s(sbase + C::OFF_ENT + stage * C::STAGE_ENT, entb + b0, bytes, &full[stage], strm);
       }
-      const int ne = (int)(epj[G] - epj[0]);
-      const int cap = G * kEntCapPerChunk;
-      const int nstg = ne < cap ? ne : cap;
-      const uint32_t e_st = sbase + C::OFF_ENT + stage * C::STAGE_ENT;
-      for (int i = lane; i < nstg; i += 32) cp_async4(e_st + i * 4, ent + epj[0] + i);
-      cp_async_commit();
-      if (++pending > C::INFLIGHT) {
-        cp_async_wait<C::INFLIGHT>();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&full[sig]);
-        if (++sig == S) sig = 0;
-        --pending;
-      }
+      __syncwarp();
       if (++stage == S) { stage = 0; phase ^= 1; }
     }
-    cp_async_wait<0>();
-    __syncwarp();
-    for (; pending > 0; --pending) {
-      if (lane == 0) mbar_arrive(&full[sig]);
-      if (++sig == S) sig = 0;
-    }
-  } else if (warp < kProducers + kBuilders) {
+  } else if (warp >= kBuilder0 && warp < kBuilder0 + kBuilders) {
     // ================================================================ slab builders (alternate stages)
-    const int b = warp - kProducers;
+    const int b = warp - kBuilder0;
     const int64_t nst = count_stages<G>(chunk_ptr, tb0, tb1, lane);
     for (int64_t n = b; n < nst; n += kBuilders) {
       const int stage = (int)(n % S);
@@ -361,8 +359,9 @@ __global__ void __launch_bounds__(kTileThreads, 1)
 #pragma unroll
       for (int i = 0; i < G * 4; ++i) reinterpret_cast<int4*>(slab)[lane + 32 * i] = zero4;
       __syncwarp();
-      const uint32_t* es = reinterpret_cast<const uint32_t*>(smem + C::OFF_ENT + stage * C::STAGE_ENT);
-      const int cap = G * kEntCapPerChunk;
+      const int skew = inf.skew;
+      const uint32_t* es = reinterpret_cast<const uint32_t*>(smem + C::OFF_ENT + stage * C::STAGE_ENT) + skew;
+      const int cap = G * kEntCapPerChunk - skew;  // entries available in the staged copy
       for (int j = 0; j < g; ++j) {
         const int lo = (int)(inf.ep[j] - e0), hi = (int)(inf.ep[j + 1] - e0);
         uint8_t* sl = slab + j * 2048;

@@ -204,7 +204,8 @@ class HybridPlan:
         self.gidx = torch.empty(max(self.nchunks * TILE_CHUNK, 1), dtype=torch.int32, device=dev)
         self.ent_ptr = torch.zeros(self.nchunks + 1, dtype=torch.int64, device=dev)
         ent_words = self.nnz_tile if ent_dtype == _lib.DTYPE_BF16 else 2 * self.nnz_tile
-        self.ent = torch.empty(max(ent_words, 1), dtype=torch.int32, device=dev)
+        # +8 words: the tile kernel stages entries with 16-byte aligned bulk copies
+        self.ent = torch.zeros(max(ent_words, 1) + 8, dtype=torch.int32, device=dev)
         if self.n_tile:
             wsb = _lib.ctypes.c_size_t(0)
             _lib.check(_lib.lib().hcs_tile_plan_workspace_bytes(self.nnz_tile, self.nchunks, _lib.ctypes.byref(wsb)))
