@@ -99,6 +99,14 @@ int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk
 int hcs_normalize_values(int kind, const int64_t* row_ptr, const int32_t* col, const double* v_in, int64_t n,
                          double* workspace_deg, double* v_out, float* v_out32, void* stream);
 
+/* tile-path MMA engine: -1 auto (default), 0 tcgen05.mma (TMEM accumulators),
+ * 1 mma.sync m16n8k16 (register accumulators); both share the cp.async gather pipeline */
+int hcs_set_tile_engine(int engine);
+
+/* debug: per-CTA wait-time counters of the tile kernel (16 per CTA; enable=1 on,
+ * 0 off; host_out != NULL copies the first n counters and clears them) */
+int hcs_debug_tile_profile(int enable, unsigned long long* host_out, int n);
+
 /* elementwise helpers used by the Python layer (fp32 -> bf16 RNE, fp32 -> tf32 RNA) */
 int hcs_convert(const float* src, void* dst, int64_t n, int dst_kind, void* stream);
 

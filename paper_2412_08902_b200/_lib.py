@@ -46,6 +46,8 @@ _SIGS = {
                                      I64, P]),
     "hcs_convert": (ctypes.c_int, [P, P, I64, ctypes.c_int, P]),
     "hcs_normalize_values": (ctypes.c_int, [ctypes.c_int, P, P, P, I64, P, P, P, P]),
+    "hcs_debug_tile_profile": (ctypes.c_int, [ctypes.c_int, P, ctypes.c_int]),
+    "hcs_set_tile_engine": (ctypes.c_int, [ctypes.c_int]),
 }
 
 

@@ -37,7 +37,10 @@ constexpr int kBuilders = 2;
 constexpr int kMmaWarp = 8;     // warp 8: tcgen05.mma issuer
 constexpr int kEpiWarp0 = 12;   // warps 12-15: epilogue (TMEM lane quadrants 0-3)
 constexpr int kTileThreads = 16 * 32;
-constexpr int kEntCapPerChunk = 128;  // staged packed entries per chunk; the rest is read from global
+constexpr int kEntCapPerChunk = 128;
+#ifndef HCS_TILE_NOINC
+#define HCS_TILE_NOINC 1  // 1: cp.async.mbarrier.arrive.noinc completion, 0: commit/wait_group publish
+#endif  // staged packed entries per chunk; the rest is read from global
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes, uint64_t pol) {
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(dst), "l"(src),
@@ -47,11 +50,31 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32
 __device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
 }
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_trans(uint32_t (&r)[4], uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void hmma_16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
 // first t in [0, n] with a[t] >= v  (a non-decreasing, length n+1)
@@ -124,6 +147,19 @@ struct StageIter {
   }
 };
 
+// Optional wait-time instrumentation (hcs_debug_tile_profile): cycles spent in each
+// wait, accumulated per CTA into prof[blockIdx.x * 16 + slot].
+#define TPROF(slot, stmt)                                                        \
+  do {                                                                           \
+    if (prof) {                                                                  \
+      const long long _t0 = clock64();                                           \
+      stmt;                                                                      \
+      if (lane == 0) atomicAdd(&prof[blockIdx.x * 16 + (slot)], (unsigned long long)(clock64() - _t0)); \
+    } else {                                                                     \
+      stmt;                                                                      \
+    }                                                                            \
+  } while (0)
+
 template <int VEC>
 struct TileCfg {
   // VEC: 16-byte vectors per gathered row (dim <= 8*VEC)
@@ -139,14 +175,16 @@ struct TileCfg {
   static constexpr int STAGE_BYTES = STAGE_A + STAGE_SLAB + STAGE_ENT;
   static constexpr int IDX_SLOT = G * 64 * 4;
   static constexpr int IDX_SLOTS = 16;           // gather-index ring (TMA loader runs up to 16 stages ahead)
-  static constexpr int STAGES = (205 * 1024 - IDX_SLOTS * IDX_SLOT) / STAGE_BYTES;
+  static constexpr int RED_BYTES = 4 * 16 * 32 * 4;  // mma.sync K-split partial sums
+  static constexpr int STAGES = (205 * 1024 - IDX_SLOTS * IDX_SLOT - RED_BYTES) / STAGE_BYTES;
   static constexpr int INFLIGHT = STAGES - 2;    // stages of gathers in flight per producer thread
   static constexpr int OFF_A = 0;
   static constexpr int OFF_SLAB = OFF_A + STAGES * STAGE_A;
   static constexpr int OFF_ENT = OFF_SLAB + STAGES * STAGE_SLAB;
   static constexpr int OFF_IDX = OFF_ENT + STAGES * STAGE_ENT;
   static constexpr int OFF_INFO = OFF_IDX + IDX_SLOTS * IDX_SLOT;
-  static constexpr int OFF_IDXG = OFF_INFO + STAGES * 64;   // int g per index slot
+  static constexpr int OFF_RED = OFF_INFO + STAGES * 64;
+  static constexpr int OFF_IDXG = OFF_RED + RED_BYTES;   // int g per index slot
   static constexpr int OFF_BAR = OFF_IDXG + IDX_SLOTS * 4;
   static constexpr int NBAR = 3 * STAGES + 4 + 2 * IDX_SLOTS;
   static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;  // + alignment slack
@@ -173,12 +211,19 @@ __device__ __forceinline__ int64_t count_stages(const int64_t* __restrict__ chun
   return n;
 }
 
-template <int VEC>
+// ENGINE 0: tcgen05.mma (M=128 features x N=16 rows, TMEM accumulators, epilogue warps)
+// ENGINE 1: mma.sync m16n8k16 (ldmatrix-fed from the same smem stages; up to 4 compute
+//           warps own 32 features each, fp32 accumulators in registers).
+// Measured on B200 (tools/probe/mma_rate, hmma_rate): a tcgen05.mma has a ~45-cycle
+// floor per instruction for N <= 64, so the 16-row window shape runs ~8x below the
+// tensor-core peak, while HMMA.16816 sustains ~2 cycles per instruction per SM.
+template <int VEC, int ENGINE>
 __global__ void __launch_bounds__(kTileThreads, 1)
     k_spmm_tile_bf16(const int32_t* __restrict__ tile_list, int64_t T, const int64_t* __restrict__ chunk_ptr,
                      const int32_t* __restrict__ gidx, const int64_t* __restrict__ ent_ptr,
                      const uint32_t* __restrict__ ent, int64_t n_rows, int wh, const __nv_bfloat16* __restrict__ x,
-                     int64_t ldx, int vec, int dim, float* __restrict__ z, int64_t ldz) {
+                     int64_t ldx, int vec, int dim, float* __restrict__ z, int64_t ldz,
+                     unsigned long long* __restrict__ prof) {
   using C = TileCfg<VEC>;
   constexpr int S = C::STAGES, G = C::G;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -196,11 +241,14 @@ __global__ void __launch_bounds__(kTileThreads, 1)
   int32_t* idx_g = reinterpret_cast<int32_t*>(smem + C::OFF_IDXG);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long t_start = clock64();
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], kProducers + 1);  // producers + entry loader (arrive.expect_tx)
+      // producers (per-lane cp.async arrivals, or one publish per warp) + entry loader (arrive.expect_tx)
+      mbar_init(&full[s], (HCS_TILE_NOINC ? kProducers * 32 : kProducers) + 1);
       mbar_init(&built[s], 1);
-      mbar_init(&empty[s], 1);
+      // tcgen05.commit | all mma.sync compute warps (FS feature slices x KS K-splits)
+      mbar_init(&empty[s], ENGINE == 0 ? 1 : ((dim + 31) / 32) * ((dim + 31) / 32 >= 3 ? 1 : ((dim + 31) / 32 == 2 ? 2 : 4)));
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&accf[b], 1);
@@ -212,11 +260,11 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 0) tmem_alloc<32>(tmem_slot);
+  if (ENGINE == 0 && warp == 0) tmem_alloc<32>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = ENGINE == 0 ? *tmem_slot : 0u;
   const uint32_t sbase = smem_u32(smem);
   // contiguous, chunk-balanced range of tile windows for this CTA
   const int64_t Ctot = chunk_ptr[T];
@@ -251,7 +299,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     int stage = 0, sig = 0, pending = 0, islot = 0;
     uint32_t phase = 0, iphase = 0;
     for (int n = 0; n < nst; ++n) {
-      mbar_wait(&idx_full[islot], iphase);
+      TPROF(0, mbar_wait(&idx_full[islot], iphase));
       const int g = idx_g[islot];
       const int32_t* idx_s =
           reinterpret_cast<const int32_t*>(smem + C::OFF_IDX + islot * C::IDX_SLOT) + row0 + lrow;
@@ -261,7 +309,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&idx_empty[islot]);
       if (++islot == C::IDX_SLOTS) { islot = 0; iphase ^= 1; }
-      mbar_wait(&empty[stage], phase ^ 1);
+      TPROF(1, mbar_wait(&empty[stage], phase ^ 1));
       const uint32_t a_st = sbase + C::OFF_A + stage * C::STAGE_A;
       const int lim = g * 64 - row0 - lrow;  // rows it*RPI < lim are valid
 #pragma unroll
@@ -270,17 +318,23 @@ __global__ void __launch_bounds__(kTileThreads, 1)
           cp_async16(a_st + dofs[it], xl + (int64_t)max(gi[it], 0) * ldxb, gi[it] >= 0 ? vbytes : 0u, keep);
         }
       }
+#if HCS_TILE_NOINC
+      // each lane arrives on the stage's barrier once all its prior cp.async copies landed
+      cp_async_arrive_noinc(&full[stage]);
+#else
       cp_async_commit();
       if (++pending > C::INFLIGHT) {  // oldest in-flight stage has landed -> publish it
-        cp_async_wait<C::INFLIGHT>();
+        TPROF(2, cp_async_wait<C::INFLIGHT>());
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&full[sig]);
         if (++sig == S) sig = 0;
         --pending;
       }
+#endif
       if (++stage == S) { stage = 0; phase ^= 1; }
     }
+#if !HCS_TILE_NOINC
     cp_async_wait<0>();
     fence_proxy_async_smem();
     __syncwarp();
@@ -288,6 +342,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       if (lane == 0) mbar_arrive(&full[sig]);
       if (++sig == S) sig = 0;
     }
+#endif
   } else if (warp == kIdxWarp) {
     // ================================================================ gather-index loader (TMA)
     const uint64_t strm = policy_evict_first();
@@ -297,7 +352,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     uint32_t iphase = 0;
     for (; cur.valid(); cur.next(lane)) {
       const int g = cur.g();
-      mbar_wait(&idx_empty[islot], iphase ^ 1);
+      TPROF(3, mbar_wait(&idx_empty[islot], iphase ^ 1));
       if (lane == 0) {
         idx_g[islot] = g;
         mbar_expect_tx(&idx_full[islot], (uint32_t)g * 256u);
@@ -330,7 +385,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       const int64_t b0 = (epj[0] * 4) & ~(int64_t)15;
       const int64_t b1 = (epj[G] * 4 + 15) & ~(int64_t)15;
       const uint32_t bytes = (uint32_t)(b1 - b0 < C::STAGE_ENT ? b1 - b0 : C::STAGE_ENT);
-      mbar_wait(&empty[stage], phase ^ 1);
+      TPROF(4, mbar_wait(&empty[stage], phase ^ 1));
       if (lane == 0) {
 #pragma unroll
         for (int j = 0; j <= G; ++j) info[stage].ep[j] = epj[j];
@@ -343,17 +398,20 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       __syncwarp();
       if (++stage == S) { stage = 0; phase ^= 1; }
     }
-  } else if (warp >= kBuilder0 && warp < kBuilder0 + kBuilders) {
-    // ================================================================ slab builders (alternate stages)
-    const int b = warp - kBuilder0;
+  } else if ((warp >= kBuilder0 && warp < kBuilder0 + kBuilders) || (ENGINE == 1 && warp >= kEpiWarp0)) {
+    // ================================================================ slab builders (round-robin stages)
+    // tcgen05 engine: warps 6-7; mma.sync engine also uses the (otherwise idle) warps 12-15.
+    constexpr int NB = ENGINE == 1 ? kBuilders + 4 : kBuilders;
+    const int b = warp < kEpiWarp0 ? warp - kBuilder0 : kBuilders + (warp - kEpiWarp0);
     const int64_t nst = count_stages<G>(chunk_ptr, tb0, tb1, lane);
-    for (int64_t n = b; n < nst; n += kBuilders) {
+    for (int64_t n = b; n < nst; n += NB) {
       const int stage = (int)(n % S);
       const uint32_t phase = (uint32_t)((n / S) & 1);
-      mbar_wait(&full[stage], phase);
+      TPROF(5, mbar_wait(&full[stage], phase));
       const StageInfo& inf = info[stage];
       const int g = inf.g;
       const int64_t e0 = inf.ep[0];
+      const long long t_b0 = prof ? clock64() : 0;
       uint8_t* slab = smem + C::OFF_SLAB + stage * C::STAGE_SLAB;
       const int4 zero4 = make_int4(0, 0, 0, 0);
 #pragma unroll
@@ -373,9 +431,113 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       }
       fence_proxy_async_smem();
       __syncwarp();
+      if (prof && lane == 0) atomicAdd(&prof[blockIdx.x * 16 + 14], (unsigned long long)(clock64() - t_b0));
       if (lane == 0) mbar_arrive(&built[stage]);
     }
-  } else if (warp == kMmaWarp) {
+  } else if (ENGINE == 1 && warp >= kMmaWarp && warp < kMmaWarp + 4) {
+    // ================================================================ HMMA compute warps
+    // Warp cw owns feature slice fs = cw % FS (32 features) and the stage's chunks
+    // j == kp (mod KS), kp = cw / FS; with KS > 1 the partial window sums are reduced
+    // through shared memory in a fixed order (deterministic).
+    const int FS = (dim + 31) / 32;                  // 1..4 feature slices
+    const int KS = FS >= 3 ? 1 : (FS == 2 ? 2 : 4);  // K-split factor
+    const int cw = warp - kMmaWarp;
+    const int fs = cw % FS, kp = cw / FS;
+    const int ncw = FS * KS;
+    if (cw < ncw) {
+      const int f0 = fs * 32;
+      const int64_t nst = count_stages<G>(chunk_ptr, tb0, tb1, lane);
+      // lane-constant parts of the ldmatrix addresses
+      const int ar = lane & 15, akc = lane >> 4;                           // A: row, k-chunk offset
+      const int bk = (lane & 7) + ((lane >> 3) & 1) * 8, bfc = lane >> 4;  // B: k row, feature-chunk offset
+      auto a_tile_off = [&](int row, int fchunk) -> uint32_t {  // gathered-row layout (see producers)
+        const int jch = row >> 6, r = row & 63;
+        if (C::ROWB == 128)
+          return (uint32_t)(fchunk >> 3) * (uint32_t)(G * C::CHUNK_A) + (uint32_t)jch * C::CHUNK_A +
+                 (uint32_t)r * 128u + ((uint32_t)((fchunk & 7) ^ (r & 7)) << 4);
+        return (uint32_t)jch * C::CHUNK_A + (uint32_t)(r >> 3) * 512u + (uint32_t)(r & 7) * 64u +
+               ((uint32_t)((fchunk ^ ((r & 7) >> 1)) & 3) << 4);
+      };
+      float* red = reinterpret_cast<float*>(smem + C::OFF_RED);  // [KS][FS][16][32]
+      float acc[4][4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+      int64_t t = tb0;
+      int64_t wid_next = (t < tb1) ? tile_list[t] : 0;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t n = 0; n < nst; ++n) {
+        TPROF(6, mbar_wait(&built[stage], phase));
+        const int g = info[stage].g, flags = info[stage].flags;
+        const uint32_t a_st = sbase + C::OFF_A + stage * C::STAGE_A;
+        const uint32_t b_st = sbase + C::OFF_SLAB + stage * C::STAGE_SLAB;
+        // steps (j, ks) of this warp, software-pipelined: fragments of step s+1 load during the MMAs of s
+        const int nsteps = ((g - kp + KS - 1) / KS) * 4;  // chunks kp, kp+KS, ... below g, 4 K-steps each
+        (void)nsteps;
+        for (int j = kp; j < g; j += KS) {
+          const uint32_t sl = b_st + j * 2048;
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            uint32_t a[4], b0[4], b1[4];
+            const int kc = 2 * ks + akc;
+            ldsm_x4(a, sl + ar * 128 + (((kc ^ ar) & 7) << 4));
+            const int row = j * 64 + ks * 16 + bk;
+            ldsm_x4_trans(b0, a_st + a_tile_off(row, (f0 >> 3) + bfc));
+            ldsm_x4_trans(b1, a_st + a_tile_off(row, (f0 >> 3) + 2 + bfc));
+            hmma_16816(acc[0], a, b0[0], b0[1]);
+            hmma_16816(acc[1], a, b0[2], b0[3]);
+            hmma_16816(acc[2], a, b1[0], b1[1]);
+            hmma_16816(acc[3], a, b1[2], b1[3]);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (flags & 2) {  // window done: (reduce partials) rows -> Z, reset accumulators
+          const int64_t rs = wid_next * wh;
+          const int rows = (int)(n_rows - rs < wh ? n_rows - rs : wh);
+          ++t;
+          wid_next = (t < tb1) ? tile_list[t] : 0;
+          const int r0 = lane >> 2, cc = (lane & 3) * 2;
+          if (KS > 1) {
+            float* my = red + ((kp * FS + fs) * 16) * 32;
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+              *reinterpret_cast<float2*>(my + r0 * 32 + nt * 8 + cc) = make_float2(acc[nt][0], acc[nt][1]);
+              *reinterpret_cast<float2*>(my + (r0 + 8) * 32 + nt * 8 + cc) = make_float2(acc[nt][2], acc[nt][3]);
+            }
+            named_bar_sync(2, ncw * 32);
+            if (kp == 0) {
+#pragma unroll
+              for (int nt = 0; nt < 4; ++nt) {
+                for (int k = 1; k < KS; ++k) {
+                  const float* o = red + ((k * FS + fs) * 16) * 32;
+                  const float2 u = *reinterpret_cast<const float2*>(o + r0 * 32 + nt * 8 + cc);
+                  const float2 w = *reinterpret_cast<const float2*>(o + (r0 + 8) * 32 + nt * 8 + cc);
+                  acc[nt][0] += u.x; acc[nt][1] += u.y; acc[nt][2] += w.x; acc[nt][3] += w.y;
+                }
+              }
+            }
+          }
+          if (kp == 0) {
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) {
+              const int f = f0 + nt * 8 + cc;
+              if (f < dim) {
+                if (r0 < rows)
+                  *reinterpret_cast<float2*>(z + (rs + r0) * ldz + f) = make_float2(acc[nt][0], acc[nt][1]);
+                if (r0 + 8 < rows)
+                  *reinterpret_cast<float2*>(z + (rs + r0 + 8) * ldz + f) = make_float2(acc[nt][2], acc[nt][3]);
+              }
+            }
+          }
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
+          if (KS > 1) named_bar_sync(2, ncw * 32);  // partials consumed before the next window reuses them
+        }
+        if (++stage == S) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (ENGINE == 0 && warp == kMmaWarp) {
     // ================================================================ MMA issuer
     constexpr uint32_t idesc = umma_idesc(128, 16, 1, 1, 1, 0);
     // A: MN-major; NBLK == 2 -> second 64-feature block G*CHUNK_A bytes away.
@@ -386,12 +548,13 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     int stage = 0, acc = 0;
     uint32_t phase = 0, acc_phase = 0;
     for (int64_t n = 0; n < nst; ++n) {
-      mbar_wait(&built[stage], phase);
+      TPROF(6, mbar_wait(&built[stage], phase));
       const int g = info[stage].g, flags = info[stage].flags;
       const bool first = flags & 1, last = flags & 2;
-      if (first) mbar_wait(&acce[acc], acc_phase ^ 1);
+      if (first) TPROF(7, mbar_wait(&acce[acc], acc_phase ^ 1));
       fence_proxy_async_smem();
       tc_fence_after();
+      const long long t_mma0 = prof ? clock64() : 0;
       if (lane == 0) {
         const uint32_t a_st = sbase + C::OFF_A + stage * C::STAGE_A;
         const uint32_t b_st = sbase + C::OFF_SLAB + stage * C::STAGE_SLAB;
@@ -407,10 +570,11 @@ __global__ void __launch_bounds__(kTileThreads, 1)
         if (last) umma_commit(&accf[acc]);
       }
       __syncwarp();
+      if (prof && lane == 0) atomicAdd(&prof[blockIdx.x * 16 + 9], (unsigned long long)(clock64() - t_mma0));
       if (last && ++acc == 2) { acc = 0; acc_phase ^= 1; }
       if (++stage == S) { stage = 0; phase ^= 1; }
     }
-  } else if (warp >= kEpiWarp0) {
+  } else if (ENGINE == 0 && warp >= kEpiWarp0) {
     // ================================================================ epilogue
     const int q = warp & 3;  // TMEM lane quadrant accessible to this warp
     int acc = 0;
@@ -421,7 +585,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       const int64_t rs = w * wh;
       const int rows = (int)(n_rows - rs < wh ? n_rows - rs : wh);
       // one warp polls the mbarrier; the other three block on a named barrier (no spinning)
-      if (q == 0) mbar_wait(&accf[acc], acc_phase);
+      if (q == 0) TPROF(8, mbar_wait(&accf[acc], acc_phase));
       named_bar_sync(1, 128);
       tc_fence_after();
       uint32_t r[16];
@@ -439,20 +603,28 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
+  if (prof && lane == 0) {
+    atomicAdd(&prof[blockIdx.x * 16 + 10 + (warp < kProducers ? 0 : warp < kBuilder0 ? 1 : warp < kMmaWarp ? 2 : 3)],
+              (unsigned long long)(clock64() - t_start));
+  }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc<32>(tmem);
+  if (ENGINE == 0 && warp == 0) tmem_dealloc<32>(tmem);
+  if (prof && threadIdx.x == 0) atomicAdd(&prof[blockIdx.x * 16 + 15], (unsigned long long)(clock64() - t_start));
 }
 
-template <int VEC>
+static unsigned long long* g_tile_prof = nullptr;  // debug wait-time counters (nullptr = off)
+static int g_tile_engine = -1;                     // -1 auto, 0 tcgen05, 1 mma.sync
+
+template <int VEC, int ENGINE>
 static int launch_tile(int grid, cudaStream_t st, const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr,
                        const int32_t* gidx, const int64_t* ent_ptr, const uint32_t* ent, int64_t n_rows, int wh,
                        const __nv_bfloat16* x, int64_t ldx, int vec, int d, float* z, int64_t ldz) {
   using C = TileCfg<VEC>;
-  auto kern = k_spmm_tile_bf16<VEC>;
+  auto kern = k_spmm_tile_bf16<VEC, ENGINE>;
   HCS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   kern<<<grid, kTileThreads, C::SMEM, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, vec,
-                                            d, z, ldz);
+                                            d, z, ldz, g_tile_prof);
   HCS_LAUNCH_CHECK("k_spmm_tile_bf16");
   return HCS_OK;
 }
@@ -480,12 +652,49 @@ extern "C" int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int
     const int vec = (d + 7) / 8;
     const __nv_bfloat16* xs = reinterpret_cast<const __nv_bfloat16*>(x) + f0;
     float* zs = z + f0;
+    const int engine = g_tile_engine >= 0 ? g_tile_engine : 1;  // auto: HMMA (see kernel header)
     int rc;
-    if (vec > 8) rc = launch_tile<16>(grid, st, tile_list, n_tile, chunk_ptr, gidx, ent_ptr, e, n_rows, wh, xs, ldx, vec, d, zs, ldz);
-    else if (vec > 4) rc = launch_tile<8>(grid, st, tile_list, n_tile, chunk_ptr, gidx, ent_ptr, e, n_rows, wh, xs, ldx, vec, d, zs, ldz);
-    else rc = launch_tile<4>(grid, st, tile_list, n_tile, chunk_ptr, gidx, ent_ptr, e, n_rows, wh, xs, ldx, vec, d, zs, ldz);
+#define HCS_TILE_ARGS grid, st, tile_list, n_tile, chunk_ptr, gidx, ent_ptr, e, n_rows, wh, xs, ldx, vec, d, zs, ldz
+    if (engine == 0) {
+      if (vec > 8) rc = launch_tile<16, 0>(HCS_TILE_ARGS);
+      else if (vec > 4) rc = launch_tile<8, 0>(HCS_TILE_ARGS);
+      else rc = launch_tile<4, 0>(HCS_TILE_ARGS);
+    } else {
+      if (vec > 8) rc = launch_tile<16, 1>(HCS_TILE_ARGS);
+      else if (vec > 4) rc = launch_tile<8, 1>(HCS_TILE_ARGS);
+      else rc = launch_tile<4, 1>(HCS_TILE_ARGS);
+    }
+#undef HCS_TILE_ARGS
     if (rc) return rc;
   }
   (void)x_rows;
+  return HCS_OK;
+}
+
+// Debug: enable (1) / disable (0) the tile kernel's wait-time counters, or read
+// them (host_out != NULL: copies n counters, 16 per CTA, then clears them).
+extern "C" int hcs_debug_tile_profile(int enable, unsigned long long* host_out, int n) {
+  const int total = 16 * 1024;
+  if (enable && !hcs::g_tile_prof) {
+    HCS_CUDA(cudaMalloc(&hcs::g_tile_prof, total * sizeof(unsigned long long)));
+    HCS_CUDA(cudaMemset(hcs::g_tile_prof, 0, total * sizeof(unsigned long long)));
+  }
+  if (host_out && hcs::g_tile_prof) {
+    HCS_CUDA(cudaDeviceSynchronize());
+    HCS_CUDA(cudaMemcpy(host_out, hcs::g_tile_prof, std::min(n, total) * sizeof(unsigned long long),
+                        cudaMemcpyDeviceToHost));
+    HCS_CUDA(cudaMemset(hcs::g_tile_prof, 0, total * sizeof(unsigned long long)));
+  }
+  if (!enable && hcs::g_tile_prof) {
+    cudaFree(hcs::g_tile_prof);
+    hcs::g_tile_prof = nullptr;
+  }
+  return HCS_OK;
+}
+
+// Select the tile-path MMA engine: -1 auto (default), 0 tcgen05.mma, 1 mma.sync m16n8k16.
+extern "C" int hcs_set_tile_engine(int engine) {
+  HCS_REQUIRE(engine >= -1 && engine <= 1, HCS_EINVAL, "engine must be -1 (auto), 0 (tcgen05) or 1 (mma.sync)");
+  hcs::g_tile_engine = engine;
   return HCS_OK;
 }

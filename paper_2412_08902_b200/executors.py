@@ -353,3 +353,15 @@ def spmm_auto(csr, x, assignment_for, precision: str = "bf16", threads: int = 1)
 
     windows = partition(csr)
     return spmm_hybrid(windows, assignment_for(windows), x, precision=precision, threads=threads)
+
+
+_ENGINES = {"auto": -1, "tcgen05": 0, "mma_sync": 1}
+
+
+def set_tile_engine(engine: str = "auto") -> None:
+    """Select the tensor-core instruction family of the tile path: "tcgen05"
+    (tcgen05.mma, TMEM accumulators), "mma_sync" (mma.sync m16n8k16, register
+    accumulators) or "auto" (the measured-faster one for 16-row windows)."""
+    if engine not in _ENGINES:
+        raise ValueError(f"engine must be one of {sorted(_ENGINES)}, got {engine!r}")
+    _lib.call("hcs_set_tile_engine", _ENGINES[engine])

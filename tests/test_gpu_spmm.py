@@ -167,3 +167,20 @@ def test_large_powerlaw_tile_path_checksum(cuda_ok):
         exact = (a.values[lo:hi].double()[:, None] * xb[cols].double()).sum(0)
         scale = float(res.z.data.double().abs().max())
         assert float((res.z.data[r].double() - exact).abs().max()) / scale <= BF16_TOL
+
+
+@pytest.mark.parametrize("engine", ["tcgen05", "mma_sync"])
+@pytest.mark.parametrize("dim", [8, 32, 40, 64, 128, 200])
+def test_tile_engines_agree(cuda_ok, engine, dim):
+    """Both tensor-core engines of the tile path against the exact product."""
+    from paper_2412_08902_b200.executors import set_tile_engine
+
+    a = plaw8k_csr()
+    x = orc.random_dense(a.num_cols, dim, seed=dim)
+    ws = hc.partition(to_hc(a))
+    try:
+        set_tile_engine(engine)
+        res = hc.spmm_tile(ws, hc.DenseMatrix(x))
+    finally:
+        set_tile_engine("auto")
+    assert orc.max_rel_err(res.z.data, orc.spmm_exact(a, x)) <= BF16_TOL
