@@ -29,14 +29,13 @@
 
 namespace hcs {
 
-constexpr int kProducers = 4;   // warps 0-3: X-row gathers (cp.async)
+constexpr int kProducers = 4;   // warps 0-3: X-row gathers (cp.async); 8 measured no faster
 constexpr int kIdxWarp = 4;     // warp 4: gather-index ring loader (TMA bulk copies)
 constexpr int kEntWarp = 5;     // warp 5: packed-entry loader (TMA bulk copies) + stage records
-constexpr int kBuilder0 = 6;    // warps 6-7: B-slab builders (alternate stages)
-constexpr int kBuilders = 2;
-constexpr int kMmaWarp = 8;     // warp 8: tcgen05.mma issuer
-constexpr int kEpiWarp0 = 12;   // warps 12-15: epilogue (TMEM lane quadrants 0-3)
-constexpr int kTileThreads = 16 * 32;
+constexpr int kBuilder0 = 6;    // warp 6 (+ warp 7 with the mma.sync engine): B-slab builders
+constexpr int kMmaWarp = 7;     // warp 7: tcgen05.mma issuer (tcgen05 engine)
+constexpr int kEpiWarp0 = 8;    // warps 8-11: tcgen05 epilogue (TMEM lane quadrants 0-3) | mma.sync compute
+constexpr int kTileThreads = 12 * 32;
 constexpr int kEntCapPerChunk = 128;
 #ifndef HCS_TILE_NOINC
 #define HCS_TILE_NOINC 1  // 1: cp.async.mbarrier.arrive.noinc completion, 0: commit/wait_group publish
@@ -176,7 +175,7 @@ struct TileCfg {
   static constexpr int IDX_SLOT = G * 64 * 4;
   static constexpr int IDX_SLOTS = 16;           // gather-index ring (TMA loader runs up to 16 stages ahead)
   static constexpr int RED_BYTES = 4 * 16 * 32 * 4;  // mma.sync K-split partial sums
-  static constexpr int STAGES = (205 * 1024 - IDX_SLOTS * IDX_SLOT - RED_BYTES) / STAGE_BYTES;
+  static constexpr int STAGES = (223 * 1024 - IDX_SLOTS * IDX_SLOT - RED_BYTES) / STAGE_BYTES;
   static constexpr int INFLIGHT = STAGES - 2;    // stages of gathers in flight per producer thread
   static constexpr int OFF_A = 0;
   static constexpr int OFF_SLAB = OFF_A + STAGES * STAGE_A;
@@ -398,11 +397,11 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       __syncwarp();
       if (++stage == S) { stage = 0; phase ^= 1; }
     }
-  } else if ((warp >= kBuilder0 && warp < kBuilder0 + kBuilders) || (ENGINE == 1 && warp >= kEpiWarp0)) {
+  } else if (warp == kBuilder0 || (ENGINE == 1 && warp == kBuilder0 + 1)) {
     // ================================================================ slab builders (round-robin stages)
-    // tcgen05 engine: warps 6-7; mma.sync engine also uses the (otherwise idle) warps 12-15.
-    constexpr int NB = ENGINE == 1 ? kBuilders + 4 : kBuilders;
-    const int b = warp < kEpiWarp0 ? warp - kBuilder0 : kBuilders + (warp - kEpiWarp0);
+    // tcgen05 engine: warp 10; mma.sync engine: warps 10-11 (warp 11 issues tcgen05 otherwise).
+    constexpr int NB = ENGINE == 1 ? 2 : 1;
+    const int b = warp - kBuilder0;
     const int64_t nst = count_stages<G>(chunk_ptr, tb0, tb1, lane);
     for (int64_t n = b; n < nst; n += NB) {
       const int stage = (int)(n % S);
@@ -420,13 +419,39 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       const int skew = inf.skew;
       const uint32_t* es = reinterpret_cast<const uint32_t*>(smem + C::OFF_ENT + stage * C::STAGE_ENT) + skew;
       const int cap = G * kEntCapPerChunk - skew;  // entries available in the staged copy
-      for (int j = 0; j < g; ++j) {
-        const int lo = (int)(inf.ep[j] - e0), hi = (int)(inf.ep[j + 1] - e0);
-        uint8_t* sl = slab + j * 2048;
-        for (int i = lo + lane; i < hi; i += 32) {
-          const uint32_t w = (i < cap) ? es[i] : ent[e0 + i];
-          const uint32_t pos = w & 1023u;
-          *reinterpret_cast<uint16_t*>(sl + sw128_kmajor_off16(pos >> 6, pos & 63u)) = (uint16_t)(w >> 16);
+      // entry = bf16 value << 16 | byte offset in its chunk's swizzled slab (precomputed by the plan)
+      const int ne = (int)(inf.ep[g] - e0);
+      if (ne <= cap) {
+        // fast path: all entries staged; chunk j's slab starts 2 KB after chunk j-1's
+        int bq[G];  // first entry of chunk q (q >= g: past the end)
+#pragma unroll
+        for (int q = 0; q < G; ++q) bq[q] = q < g ? (int)(inf.ep[q] - e0) : ne;
+        for (int i0 = 0; i0 < ne; i0 += 128) {
+          uint32_t w[4];
+          int ii[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            ii[u] = i0 + u * 32 + lane;
+            w[u] = ii[u] < ne ? es[ii[u]] : 0u;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (ii[u] < ne) {
+              int j = 0;  // chunk of entry ii[u]: ep boundaries (g <= 4)
+#pragma unroll
+              for (int q = 1; q < G; ++q) j += ii[u] >= bq[q] ? 1 : 0;
+              *reinterpret_cast<uint16_t*>(slab + j * 2048 + (w[u] & 0x7FFu)) = (uint16_t)(w[u] >> 16);
+            }
+          }
+        }
+      } else {
+        for (int j = 0; j < g; ++j) {
+          const int lo = (int)(inf.ep[j] - e0), hi = (int)(inf.ep[j + 1] - e0);
+          uint8_t* sl = slab + j * 2048;
+          for (int i = lo + lane; i < hi; i += 32) {
+            const uint32_t w = (i < cap) ? es[i] : ent[e0 + i];
+            *reinterpret_cast<uint16_t*>(sl + (w & 0x7FFu)) = (uint16_t)(w >> 16);
+          }
         }
       }
       fence_proxy_async_smem();
@@ -434,14 +459,14 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       if (prof && lane == 0) atomicAdd(&prof[blockIdx.x * 16 + 14], (unsigned long long)(clock64() - t_b0));
       if (lane == 0) mbar_arrive(&built[stage]);
     }
-  } else if (ENGINE == 1 && warp >= kMmaWarp && warp < kMmaWarp + 4) {
+  } else if (ENGINE == 1 && warp >= kEpiWarp0) {
     // ================================================================ HMMA compute warps
     // Warp cw owns feature slice fs = cw % FS (32 features) and the stage's chunks
     // j == kp (mod KS), kp = cw / FS; with KS > 1 the partial window sums are reduced
     // through shared memory in a fixed order (deterministic).
     const int FS = (dim + 31) / 32;                  // 1..4 feature slices
     const int KS = FS >= 3 ? 1 : (FS == 2 ? 2 : 4);  // K-split factor
-    const int cw = warp - kMmaWarp;
+    const int cw = warp - kEpiWarp0;
     const int fs = cw % FS, kp = cw / FS;
     const int ncw = FS * KS;
     if (cw < ncw) {
@@ -476,18 +501,22 @@ __global__ void __launch_bounds__(kTileThreads, 1)
         (void)nsteps;
         for (int j = kp; j < g; j += KS) {
           const uint32_t sl = b_st + j * 2048;
+          // the 4 K-steps' fragments are all loaded before the MMAs (latency overlap)
+          uint32_t a[4][4], b0[4][4], b1[4][4];
 #pragma unroll
           for (int ks = 0; ks < 4; ++ks) {
-            uint32_t a[4], b0[4], b1[4];
             const int kc = 2 * ks + akc;
-            ldsm_x4(a, sl + ar * 128 + (((kc ^ ar) & 7) << 4));
+            ldsm_x4(a[ks], sl + ar * 128 + (((kc ^ ar) & 7) << 4));
             const int row = j * 64 + ks * 16 + bk;
-            ldsm_x4_trans(b0, a_st + a_tile_off(row, (f0 >> 3) + bfc));
-            ldsm_x4_trans(b1, a_st + a_tile_off(row, (f0 >> 3) + 2 + bfc));
-            hmma_16816(acc[0], a, b0[0], b0[1]);
-            hmma_16816(acc[1], a, b0[2], b0[3]);
-            hmma_16816(acc[2], a, b1[0], b1[1]);
-            hmma_16816(acc[3], a, b1[2], b1[3]);
+            ldsm_x4_trans(b0[ks], a_st + a_tile_off(row, (f0 >> 3) + bfc));
+            ldsm_x4_trans(b1[ks], a_st + a_tile_off(row, (f0 >> 3) + 2 + bfc));
+          }
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            hmma_16816(acc[0], a[ks], b0[ks][0], b0[ks][1]);
+            hmma_16816(acc[1], a[ks], b0[ks][2], b0[ks][3]);
+            hmma_16816(acc[2], a[ks], b1[ks][0], b1[ks][1]);
+            hmma_16816(acc[3], a[ks], b1[ks][2], b1[ks][3]);
           }
         }
         __syncwarp();
@@ -604,7 +633,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     }
   }
   if (prof && lane == 0) {
-    atomicAdd(&prof[blockIdx.x * 16 + 10 + (warp < kProducers ? 0 : warp < kBuilder0 ? 1 : warp < kMmaWarp ? 2 : 3)],
+    atomicAdd(&prof[blockIdx.x * 16 + 10 + (warp < kProducers ? 0 : warp < kBuilder0 ? 1 : warp < kEpiWarp0 ? 2 : 3)],
               (unsigned long long)(clock64() - t_start));
   }
   tc_fence_before();

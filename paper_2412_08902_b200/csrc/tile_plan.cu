@@ -5,7 +5,8 @@
 //
 // A chunk is 64 consecutive condensed columns of one window.  Per chunk we keep
 //   gidx[64]     : original column (= X row) of each condensed column, -1 = pad
-//   entries      : packed (value << 16 | r*64 + c) in (row, column) order
+//   entries      : packed (bf16 value << 16 | swizzled slab byte offset of (r, c)),
+//                  in (row, column) order
 // Entries are ordered deterministically by a radix sort on (chunk, position).
 #include <cub/cub.cuh>
 
@@ -67,7 +68,9 @@ __global__ void k_tile_emit(const uint64_t* __restrict__ keys, const uint32_t* _
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (; i < n; i += stride) {
     uint64_t k = keys[i];
-    uint32_t pos = (uint32_t)(k & 1023);
+    // slab byte offset of (row r, column c) in the 16 x 64 K-major 128B-swizzled B tile
+    const uint32_t rc = (uint32_t)(k & 1023);
+    uint32_t pos = sw128_kmajor_off16(rc >> 6, rc & 63u);
     if (ent_dtype == HCS_DTYPE_BF16) {
       uint32_t b = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(kv[i])));
       reinterpret_cast<uint32_t*>(ent)[i] = (b << 16) | pos;
