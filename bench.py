@@ -44,7 +44,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--dim", type=int, default=128)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--config", choices=["c2", "c1", "c5"], default="c2")
+    p.add_argument("--config", choices=["c2", "c1", "c3", "c5"], default="c2")
     p.add_argument("--precision", default="bf16")
     p.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU-baseline sampling")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -343,6 +343,68 @@ def cpu_baseline(adj, dim, budget):
                        f"extrapolated by nnz")}
 
 
+# ----------------------------------------------------------------------------- C3: 2-layer GCN epoch
+def run_c3(args):
+    """BASELINE configs[2]: 2-layer GCN (128 -> 64 -> 41) training on the Reddit-shaped graph
+    with the fused SpMM+GEMM kernels, forward + backward + SGD per step."""
+    import paper_2412_08902_b200 as hc
+    from paper_2412_08902_b200 import graphgen
+    from paper_2412_08902_b200.model import Gcn2
+    from paper_2412_08902_b200.shard import Shard
+
+    world, rank, local = dist_setup(args)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    adj, a, wl_name = make_graph("c2", args.seed)
+    n, nnz = a.num_rows, a.nnz
+    shard = None
+    if world > 1:
+        shard = Shard.from_operator(a, world, rank)
+        a_loc = shard.local_operator(a)
+    else:
+        a_loc = a
+    ws = hc.partition(a_loc)
+    x = graphgen.dense_features(n, 128, seed=1, dtype=torch.float32)
+    labels = torch.randint(0, 41, (n,), generator=torch.Generator(device=dev).manual_seed(2), device=dev)
+    model = Gcn2(128, 64, 41, seed=0)
+    steps, warmup = args.steps, max(args.warmup, 3)
+    for _ in range(warmup):
+        model.epoch(x, labels, ws, shard=shard)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    with sampler:
+        s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s_ev.record()
+        for _ in range(steps):
+            loss = model.epoch(x, labels, ws, shard=shard)
+        e_ev.record()
+        torch.cuda.synchronize()
+    ms = s_ev.elapsed_time(e_ev) / steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    # SpMM flops of one epoch: fwd L1 (N=128), fwd L2 (N=64), bwd L2 grad_X (N=41)
+    spmm_flops = 2.0 * nnz * (128 + 64 + 41)
+    gemm_flops = 2.0 * n * (128 * 64 + 64 * 41) * 2 + 2.0 * n * 41 * 64
+    out = {"metric": "GCN epoch ms (2-layer, fwd+bwd+SGD)", "value": ms, "unit": "ms", "n_gpus": world,
+           "steps": steps, "warmup": warmup, "ms_per_step": ms, "higher_is_better": False,
+           "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "bf16",
+           "data": "synthetic (seeded on-device generator; X ~ U[-1,1), random labels)",
+           "config": {"workload": wl_name + ", 2-layer GCN 128-64-41, fused SpMM+GEMM fwd/bwd, SGD",
+                      "n": n, "nnz": nnz, "parallelism": f"row-window shards x{world}" if world > 1 else "single GPU",
+                      "loss_last": float(loss.detach())},
+           "spmm_gflops": spmm_flops / (ms * 1e-3) / 1e9, "gemm_gflop_per_epoch": gemm_flops / 1e9,
+           "gpu_launches": None, "clocks": sampler.summary()}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -389,5 +451,7 @@ if __name__ == "__main__":
     a = parse()
     if a.impl == "reference":
         run_reference(a)
+    elif a.config == "c3":
+        run_c3(a)
     else:
         run_ours(a)

@@ -91,6 +91,22 @@ int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk
                   const int64_t* ent_ptr, const void* ent, int ent_dtype, int64_t n_rows, int32_t wh, const void* x,
                   int x_dtype, int64_t x_rows, int32_t dim, int64_t ldx, float* z, int64_t ldz, void* stream);
 
+/* ---------------------------------------------------------------- K6 / K7
+ * gnn.py:121-159 forward (fused mode) and gnn.py:162-205 backward (fused mode):
+ * the SpMM of the listed windows with the feature GEMM fused into the window
+ * epilogue:  out[rows] = (A_w X) M,  and z[rows] = A_w X when z != NULL
+ * (forward z_cache).  M is an fp32 [dim x d_out] row-major device matrix: W for the
+ * forward, W^T for the backward grad_X = (A^T G) W^T.  dim, d_out <= 128.
+ * hcs_gcn_tile takes the tile plan of K2 (bf16); hcs_gcn_scalar a window list. */
+int hcs_gcn_tile(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
+                 const int64_t* ent_ptr, const void* ent, int ent_dtype, int64_t n_rows, int32_t wh, const void* x,
+                 int x_dtype, int64_t x_rows, int32_t dim, int64_t ldx, float* z, int64_t ldz, const float* m,
+                 int32_t d_out, float* out, int64_t ldo, void* stream);
+int hcs_gcn_scalar(const int64_t* row_ptr, const int32_t* col_idx, const void* values, int values_dtype,
+                   int64_t n_rows, int32_t wh, const int32_t* win_list, int64_t n_list, const void* x, int x_dtype,
+                   int64_t x_rows, int32_t dim, int64_t ldx, float* z, int64_t ldz, const float* m, int32_t d_out,
+                   float* out, int64_t ldo, void* stream);
+
 /* ---------------------------------------------------------------- normalisation
  * gnn.py:68-95 normalize_adj values in float64 with the reference's operation
  * order (structure of A + I assembled by the caller).  kind 0 = gcn
@@ -102,6 +118,9 @@ int hcs_normalize_values(int kind, const int64_t* row_ptr, const int32_t* col, c
 /* tile-path MMA engine: -1 auto (default), 0 tcgen05.mma (TMEM accumulators),
  * 1 mma.sync m16n8k16 (register accumulators); both share the cp.async gather pipeline */
 int hcs_set_tile_engine(int engine);
+
+/* tile-path producer (X-row gather) warps per CTA: 4 (default), 8 or 16 */
+int hcs_set_tile_producers(int np);
 
 /* debug: per-CTA wait-time counters of the tile kernel (16 per CTA; enable=1 on,
  * 0 off; host_out != NULL copies the first n counters and clears them) */

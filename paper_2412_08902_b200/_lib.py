@@ -44,10 +44,15 @@ _SIGS = {
                                        I64, P]),
     "hcs_spmm_tile": (ctypes.c_int, [P, I64, P, P, P, P, ctypes.c_int, I64, I32, P, ctypes.c_int, I64, I32, I64, P,
                                      I64, P]),
+    "hcs_gcn_tile": (ctypes.c_int, [P, I64, P, P, P, P, ctypes.c_int, I64, I32, P, ctypes.c_int, I64, I32, I64, P,
+                                     I64, P, I32, P, I64, P]),
+    "hcs_gcn_scalar": (ctypes.c_int, [P, P, P, ctypes.c_int, I64, I32, P, I64, P, ctypes.c_int, I64, I32, I64, P,
+                                       I64, P, I32, P, I64, P]),
     "hcs_convert": (ctypes.c_int, [P, P, I64, ctypes.c_int, P]),
     "hcs_normalize_values": (ctypes.c_int, [ctypes.c_int, P, P, P, I64, P, P, P, P]),
     "hcs_debug_tile_profile": (ctypes.c_int, [ctypes.c_int, P, ctypes.c_int]),
     "hcs_set_tile_engine": (ctypes.c_int, [ctypes.c_int]),
+    "hcs_set_tile_producers": (ctypes.c_int, [ctypes.c_int]),
 }
 
 

@@ -44,12 +44,20 @@ __device__ __forceinline__ float load_val<__nv_bfloat16>(const __nv_bfloat16* p,
   return __uint_as_float(ld_stream_u16(p, pol) << 16);
 }
 
+constexpr int kFusedMaxDim = 128;  // fused GCN epilogue: d_in, d_out <= 128
+constexpr int kFusedMaxRows = 16;
+
 // grid: one block per listed window; 8 warps walk the window's rows.
-template <typename XT, typename VT>
+// FUSED (K6/K7 on CUDA cores): the window's rows are also kept in shared memory and
+// multiplied by M (fp32 [dim x d_out], W or W^T) before out[rows] is written; fp32 FMA.
+template <typename XT, typename VT, bool FUSED>
 __global__ void __launch_bounds__(256) k_spmm_scalar(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
                                                      const VT* __restrict__ val, int64_t n_rows, int wh,
                                                      const int32_t* __restrict__ win_list, const XT* __restrict__ x,
-                                                     int dim, int64_t ldx, float* __restrict__ z, int64_t ldz) {
+                                                     int dim, int64_t ldx, float* __restrict__ z, int64_t ldz,
+                                                     const float* __restrict__ mw, int d_out, float* __restrict__ out,
+                                                     int64_t ldo) {
+  __shared__ float zs[FUSED ? kFusedMaxRows : 1][FUSED ? kFusedMaxDim + 4 : 1];
   constexpr int E = XVec<XT>::kElems;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t keep = policy_evict_last();
@@ -100,7 +108,13 @@ __global__ void __launch_bounds__(256) k_spmm_scalar(const int64_t* __restrict__
           if ((g % (2 * s)) == 0 && g + s < G) acc[i] += o;
         }
       }
-      if (g == 0) {
+      if (FUSED && g == 0) {
+        const int f0 = (fs + v) * E;
+#pragma unroll
+        for (int i = 0; i < E; ++i)
+          if (f0 + i < dim) zs[r - rs][f0 + i] = acc[i];
+      }
+      if (g == 0 && z != nullptr) {
         float* zr = z + r * ldz + (int64_t)(fs + v) * E;
         const int f0 = (fs + v) * E;
         if (f0 + E <= dim) {
@@ -114,6 +128,16 @@ __global__ void __launch_bounds__(256) k_spmm_scalar(const int64_t* __restrict__
           for (int i = 0; i < E && f0 + i < dim; ++i) zr[i] = acc[i];
         }
       }
+    }
+  }
+  if (FUSED) {
+    __syncthreads();
+    const int nr = (int)(re - rs);
+    for (int i = threadIdx.x; i < nr * d_out; i += blockDim.x) {
+      const int r = i / d_out, j = i - r * d_out;
+      float a = 0.f;
+      for (int k = 0; k < dim; ++k) a = fmaf(zs[r][k], __ldg(mw + (int64_t)k * d_out + j), a);
+      out[(rs + r) * ldo + j] = a;
     }
   }
 }
@@ -139,17 +163,58 @@ extern "C" int hcs_spmm_scalar(const int64_t* row_ptr, const int32_t* col_idx, c
   cudaStream_t st = as_stream(stream);
   dim3 grid((unsigned)n_list);
   if (x_dtype == HCS_DTYPE_BF16 && values_dtype == HCS_DTYPE_BF16)
-    k_spmm_scalar<__nv_bfloat16, __nv_bfloat16><<<grid, 256, 0, st>>>(
-        row_ptr, col_idx, (const __nv_bfloat16*)values, n_rows, wh, win_list, (const __nv_bfloat16*)x, dim, ldx, z, ldz);
+    k_spmm_scalar<__nv_bfloat16, __nv_bfloat16, false><<<grid, 256, 0, st>>>(
+        row_ptr, col_idx, (const __nv_bfloat16*)values, n_rows, wh, win_list, (const __nv_bfloat16*)x, dim, ldx, z, ldz,
+        nullptr, 0, nullptr, 0);
   else if (x_dtype == HCS_DTYPE_BF16 && values_dtype == HCS_DTYPE_F32)
-    k_spmm_scalar<__nv_bfloat16, float><<<grid, 256, 0, st>>>(row_ptr, col_idx, (const float*)values, n_rows, wh,
-                                                             win_list, (const __nv_bfloat16*)x, dim, ldx, z, ldz);
+    k_spmm_scalar<__nv_bfloat16, float, false><<<grid, 256, 0, st>>>(
+        row_ptr, col_idx, (const float*)values, n_rows, wh, win_list, (const __nv_bfloat16*)x, dim, ldx, z, ldz, nullptr,
+        0, nullptr, 0);
   else if (x_dtype == HCS_DTYPE_F32 && values_dtype == HCS_DTYPE_F32)
-    k_spmm_scalar<float, float><<<grid, 256, 0, st>>>(row_ptr, col_idx, (const float*)values, n_rows, wh, win_list,
-                                                     (const float*)x, dim, ldx, z, ldz);
+    k_spmm_scalar<float, float, false><<<grid, 256, 0, st>>>(row_ptr, col_idx, (const float*)values, n_rows, wh,
+                                                            win_list, (const float*)x, dim, ldx, z, ldz, nullptr, 0,
+                                                            nullptr, 0);
   else
     return set_error(HCS_EINVAL, "unsupported dtype combination x=%d values=%d", x_dtype, values_dtype);
   HCS_LAUNCH_CHECK("k_spmm_scalar");
+  (void)x_rows;
+  return HCS_OK;
+}
+
+// K6/K7 on CUDA cores: scalar windows with the fused GCN epilogue (see k_spmm_scalar).
+// z may be NULL (backward: no z_cache).  M: fp32 [dim x d_out] device matrix.
+extern "C" int hcs_gcn_scalar(const int64_t* row_ptr, const int32_t* col_idx, const void* values, int values_dtype,
+                              int64_t n_rows, int32_t wh, const int32_t* win_list, int64_t n_list, const void* x,
+                              int x_dtype, int64_t x_rows, int32_t dim, int64_t ldx, float* z, int64_t ldz,
+                              const float* m, int32_t d_out, float* out, int64_t ldo, void* stream) {
+  HCS_REQUIRE(wh > 0 && wh <= kFusedMaxRows, HCS_EINVAL, "fused GCN path supports window heights 1..%d",
+              kFusedMaxRows);
+  HCS_REQUIRE(dim > 0 && dim <= kFusedMaxDim, HCS_EINVAL, "fused GCN path needs 1 <= d_in <= %d (got %d)",
+              kFusedMaxDim, dim);
+  HCS_REQUIRE(d_out > 0 && d_out <= kFusedMaxDim, HCS_EINVAL, "fused GCN path needs 1 <= d_out <= %d (got %d)",
+              kFusedMaxDim, d_out);
+  HCS_REQUIRE(n_list >= 0 && n_list < (1LL << 31), HCS_EINVAL, "bad window list length");
+  HCS_REQUIRE(m != nullptr && out != nullptr && ldo >= d_out, HCS_EINVAL, "fused GCN: bad M / out arguments");
+  const int E = (x_dtype == HCS_DTYPE_BF16) ? 8 : 4;
+  HCS_REQUIRE(ldx % E == 0 && ldx >= ((dim + E - 1) / E) * E, HCS_EINVAL,
+              "ldx must be a multiple of %d covering dim rounded up to 16 bytes", E);
+  HCS_REQUIRE(z == nullptr || (ldz >= dim && (ldz % 4) == 0 && ((uintptr_t)z & 15) == 0), HCS_EINVAL,
+              "bad z_cache layout");
+  HCS_REQUIRE(((uintptr_t)x & 15) == 0, HCS_EINVAL, "x must be 16-byte aligned");
+  if (n_list == 0) return HCS_OK;
+  cudaStream_t st = as_stream(stream);
+  dim3 grid((unsigned)n_list);
+  if (x_dtype == HCS_DTYPE_BF16 && values_dtype == HCS_DTYPE_BF16)
+    k_spmm_scalar<__nv_bfloat16, __nv_bfloat16, true><<<grid, 256, 0, st>>>(
+        row_ptr, col_idx, (const __nv_bfloat16*)values, n_rows, wh, win_list, (const __nv_bfloat16*)x, dim, ldx, z, ldz,
+        m, d_out, out, ldo);
+  else if (x_dtype == HCS_DTYPE_F32 && values_dtype == HCS_DTYPE_F32)
+    k_spmm_scalar<float, float, true><<<grid, 256, 0, st>>>(row_ptr, col_idx, (const float*)values, n_rows, wh,
+                                                           win_list, (const float*)x, dim, ldx, z, ldz, m, d_out, out,
+                                                           ldo);
+  else
+    return set_error(HCS_EINVAL, "unsupported dtype combination x=%d values=%d", x_dtype, values_dtype);
+  HCS_LAUNCH_CHECK("k_spmm_scalar<fused>");
   (void)x_rows;
   return HCS_OK;
 }

@@ -29,13 +29,27 @@
 
 namespace hcs {
 
-constexpr int kProducers = 4;   // warps 0-3: X-row gathers (cp.async); 8 measured no faster
-constexpr int kIdxWarp = 4;     // warp 4: gather-index ring loader (TMA bulk copies)
-constexpr int kEntWarp = 5;     // warp 5: packed-entry loader (TMA bulk copies) + stage records
-constexpr int kBuilder0 = 6;    // warp 6 (+ warp 7 with the mma.sync engine): B-slab builders
-constexpr int kMmaWarp = 7;     // warp 7: tcgen05.mma issuer (tcgen05 engine)
-constexpr int kEpiWarp0 = 8;    // warps 8-11: tcgen05 epilogue (TMEM lane quadrants 0-3) | mma.sync compute
-constexpr int kTileThreads = 12 * 32;
+// Warp roles (NP producer warps; NP in {4, 8, 16}):
+//   [0, NP)        producers: X-row gathers (cp.async)
+//   NP             gather-index ring loader (TMA bulk copies)
+//   NP+1           packed-entry loader (TMA bulk copies) + stage records
+//   NP+2, NP+3     B-slab builders (round-robin stages)
+//   NP+4 .. NP+7   tcgen05 epilogue (TMEM lane quadrants 0-3) | mma.sync compute warps
+//   NP+8           tcgen05.mma issuer (tcgen05 engine only)
+// Gather throughput from L2 scales with the number of issuing warps
+// (profiles/r01_probe_gather_smem.txt), hence NP > 4.
+template <int NP, int ENGINE>
+struct Roles {
+  static constexpr int kProducers = NP;
+  static constexpr int kIdxWarp = NP;
+  static constexpr int kEntWarp = NP + 1;
+  static constexpr int kBuilder0 = NP + 2;
+  static constexpr int kBuilders = 2;
+  static constexpr int kEpiWarp0 = NP + 4;
+  static constexpr int kMmaWarp = NP + 8;
+  static constexpr int kThreads = (NP + 8 + (ENGINE == 0 ? 1 : 0)) * 32;
+  static_assert(kEpiWarp0 % 4 == 0, "epilogue warps must form an aligned warpgroup");
+};
 constexpr int kEntCapPerChunk = 128;
 #ifndef HCS_TILE_NOINC
 #define HCS_TILE_NOINC 1  // 1: cp.async.mbarrier.arrive.noinc completion, 0: commit/wait_group publish
@@ -159,7 +173,14 @@ struct StageIter {
     }                                                                            \
   } while (0)
 
-template <int VEC>
+// Fused GCN epilogue (K6/K7): the window's aggregated 16 x d_in tile is multiplied
+// on chip by a d_in x d_out matrix M (W forward, W^T backward).  M^T is kept in
+// shared memory as bf16 [kMaxOut][kLdw]; partial products of the feature-slice
+// warps are summed in a fixed order through a 16 x kMaxOut fp32 buffer.
+constexpr int kMaxOut = 128;
+constexpr int kLdw = 128 + 8;  // bf16 elements per M^T row (padding breaks bank conflicts)
+
+template <int VEC, bool FUSED = false>
 struct TileCfg {
   // VEC: 16-byte vectors per gathered row (dim <= 8*VEC)
   static constexpr int ROWB = VEC <= 4 ? 64 : 128;             // smem bytes per gathered row per MN block
@@ -175,7 +196,9 @@ struct TileCfg {
   static constexpr int IDX_SLOT = G * 64 * 4;
   static constexpr int IDX_SLOTS = 16;           // gather-index ring (TMA loader runs up to 16 stages ahead)
   static constexpr int RED_BYTES = 4 * 16 * 32 * 4;  // mma.sync K-split partial sums
-  static constexpr int STAGES = (223 * 1024 - IDX_SLOTS * IDX_SLOT - RED_BYTES) / STAGE_BYTES;
+  static constexpr int W_BYTES = FUSED ? kMaxOut * kLdw * 2 : 0;  // M^T, bf16
+  static constexpr int REDF_BYTES = FUSED ? 16 * kMaxOut * 4 : 0;  // fused partial sums
+  static constexpr int STAGES = (223 * 1024 - IDX_SLOTS * IDX_SLOT - RED_BYTES - W_BYTES - REDF_BYTES) / STAGE_BYTES;
   static constexpr int INFLIGHT = STAGES - 2;    // stages of gathers in flight per producer thread
   static constexpr int OFF_A = 0;
   static constexpr int OFF_SLAB = OFF_A + STAGES * STAGE_A;
@@ -183,7 +206,9 @@ struct TileCfg {
   static constexpr int OFF_IDX = OFF_ENT + STAGES * STAGE_ENT;
   static constexpr int OFF_INFO = OFF_IDX + IDX_SLOTS * IDX_SLOT;
   static constexpr int OFF_RED = OFF_INFO + STAGES * 64;
-  static constexpr int OFF_IDXG = OFF_RED + RED_BYTES;   // int g per index slot
+  static constexpr int OFF_W = OFF_RED + RED_BYTES;
+  static constexpr int OFF_REDF = OFF_W + W_BYTES;
+  static constexpr int OFF_IDXG = OFF_REDF + REDF_BYTES;   // int g per index slot
   static constexpr int OFF_BAR = OFF_IDXG + IDX_SLOTS * 4;
   static constexpr int NBAR = 3 * STAGES + 4 + 2 * IDX_SLOTS;
   static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;  // + alignment slack
@@ -216,14 +241,23 @@ __device__ __forceinline__ int64_t count_stages(const int64_t* __restrict__ chun
 // Measured on B200 (tools/probe/mma_rate, hmma_rate): a tcgen05.mma has a ~45-cycle
 // floor per instruction for N <= 64, so the 16-row window shape runs ~8x below the
 // tensor-core peak, while HMMA.16816 sustains ~2 cycles per instruction per SM.
-template <int VEC, int ENGINE>
-__global__ void __launch_bounds__(kTileThreads, 1)
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);  // RNE
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+template <int VEC, int ENGINE, int NP, bool FUSED>
+__global__ void __launch_bounds__(Roles<NP, ENGINE>::kThreads, 1)
     k_spmm_tile_bf16(const int32_t* __restrict__ tile_list, int64_t T, const int64_t* __restrict__ chunk_ptr,
                      const int32_t* __restrict__ gidx, const int64_t* __restrict__ ent_ptr,
                      const uint32_t* __restrict__ ent, int64_t n_rows, int wh, const __nv_bfloat16* __restrict__ x,
                      int64_t ldx, int vec, int dim, float* __restrict__ z, int64_t ldz,
-                     unsigned long long* __restrict__ prof) {
-  using C = TileCfg<VEC>;
+                     unsigned long long* __restrict__ prof, const float* __restrict__ mw, int d_out,
+                     float* __restrict__ out, int64_t ldo) {
+  using C = TileCfg<VEC, FUSED>;
+  using R = Roles<NP, ENGINE>;
+  constexpr int kProducers = R::kProducers, kIdxWarp = R::kIdxWarp, kEntWarp = R::kEntWarp;
+  constexpr int kBuilder0 = R::kBuilder0, kEpiWarp0 = R::kEpiWarp0, kMmaWarp = R::kMmaWarp;
   constexpr int S = C::STAGES, G = C::G;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -260,6 +294,14 @@ __global__ void __launch_bounds__(kTileThreads, 1)
     fence_barrier_init();
   }
   if (ENGINE == 0 && warp == 0) tmem_alloc<32>(tmem_slot);
+  if (FUSED) {
+    // M is [dim x d_out] fp32 row-major; smem holds M^T as bf16 [kMaxOut][kLdw], zero-padded
+    __nv_bfloat16* wt = reinterpret_cast<__nv_bfloat16*>(smem + C::OFF_W);
+    for (int i = threadIdx.x; i < kMaxOut * kLdw; i += blockDim.x) {
+      const int n = i / kLdw, k = i % kLdw;
+      wt[i] = __float2bfloat16_rn((n < d_out && k < dim) ? mw[(int64_t)k * d_out + n] : 0.f);
+    }
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -397,10 +439,9 @@ __global__ void __launch_bounds__(kTileThreads, 1)
       __syncwarp();
       if (++stage == S) { stage = 0; phase ^= 1; }
     }
-  } else if (warp == kBuilder0 || (ENGINE == 1 && warp == kBuilder0 + 1)) {
+  } else if (warp >= kBuilder0 && warp < kBuilder0 + R::kBuilders) {
     // ================================================================ slab builders (round-robin stages)
-    // tcgen05 engine: warp 10; mma.sync engine: warps 10-11 (warp 11 issues tcgen05 otherwise).
-    constexpr int NB = ENGINE == 1 ? 2 : 1;
+    constexpr int NB = R::kBuilders;
     const int b = warp - kBuilder0;
     const int64_t nst = count_stages<G>(chunk_ptr, tb0, tb1, lane);
     for (int64_t n = b; n < nst; n += NB) {
@@ -547,7 +588,7 @@ __global__ void __launch_bounds__(kTileThreads, 1)
               }
             }
           }
-          if (kp == 0) {
+          if (kp == 0 && z != nullptr) {
 #pragma unroll
             for (int nt = 0; nt < 4; ++nt) {
               const int f = f0 + nt * 8 + cc;
@@ -558,6 +599,49 @@ __global__ void __launch_bounds__(kTileThreads, 1)
                   *reinterpret_cast<float2*>(z + (rs + r0 + 8) * ldz + f) = make_float2(acc[nt][2], acc[nt][3]);
               }
             }
+          }
+          if (FUSED && kp == 0) {
+            // out[16 x d_out] = Zw[16 x dim] . M: this warp's 32 features are two k16 steps whose
+            // A fragments are exactly its accumulator fragments (n-tiles 2j, 2j+1); partials of
+            // the FS feature-slice warps are summed in slice order 0..FS-1 (deterministic).
+            uint32_t af[2][4];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              af[j][0] = pack_bf16(acc[2 * j][0], acc[2 * j][1]);
+              af[j][1] = pack_bf16(acc[2 * j][2], acc[2 * j][3]);
+              af[j][2] = pack_bf16(acc[2 * j + 1][0], acc[2 * j + 1][1]);
+              af[j][3] = pack_bf16(acc[2 * j + 1][2], acc[2 * j + 1][3]);
+            }
+            const uint32_t* wt = reinterpret_cast<const uint32_t*>(smem + C::OFF_W);
+            float* redf = reinterpret_cast<float*>(smem + C::OFF_REDF);  // [16][kMaxOut]
+            const int g8 = lane >> 2, t4 = lane & 3;
+            const int ntiles = (d_out + 7) >> 3;
+            for (int ph = 0; ph < FS; ++ph) {
+              if (ph == fs) {
+                for (int n8 = 0; n8 < ntiles; ++n8) {
+                  float c[4] = {0.f, 0.f, 0.f, 0.f};
+                  const uint32_t* wrow = wt + ((n8 * 8 + g8) * kLdw + f0) / 2 + t4;
+                  hmma_16816(c, af[0], wrow[0], wrow[4]);
+                  hmma_16816(c, af[1], wrow[8], wrow[12]);
+                  float2* p0 = reinterpret_cast<float2*>(redf + g8 * kMaxOut + n8 * 8 + 2 * t4);
+                  float2* p1 = reinterpret_cast<float2*>(redf + (g8 + 8) * kMaxOut + n8 * 8 + 2 * t4);
+                  if (ph == 0) {
+                    *p0 = make_float2(c[0], c[1]);
+                    *p1 = make_float2(c[2], c[3]);
+                  } else {
+                    const float2 u = *p0, w = *p1;
+                    *p0 = make_float2(u.x + c[0], u.y + c[1]);
+                    *p1 = make_float2(w.x + c[2], w.y + c[3]);
+                  }
+                }
+              }
+              named_bar_sync(3, FS * 32);
+            }
+            for (int i = fs * 32 + lane; i < rows * d_out; i += FS * 32) {
+              const int r = i / d_out, j = i - r * d_out;
+              out[(rs + r) * ldo + j] = redf[r * kMaxOut + j];
+            }
+            named_bar_sync(3, FS * 32);  // redf consumed before the next window overwrites it
           }
 #pragma unroll
           for (int nt = 0; nt < 4; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.f;
@@ -644,16 +728,18 @@ __global__ void __launch_bounds__(kTileThreads, 1)
 
 static unsigned long long* g_tile_prof = nullptr;  // debug wait-time counters (nullptr = off)
 static int g_tile_engine = -1;                     // -1 auto, 0 tcgen05, 1 mma.sync
+static int g_tile_producers = 4;                   // producer warps per CTA: 4, 8 or 16
 
-template <int VEC, int ENGINE>
+template <int VEC, int ENGINE, int NP, bool FUSED = false>
 static int launch_tile(int grid, cudaStream_t st, const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr,
                        const int32_t* gidx, const int64_t* ent_ptr, const uint32_t* ent, int64_t n_rows, int wh,
-                       const __nv_bfloat16* x, int64_t ldx, int vec, int d, float* z, int64_t ldz) {
-  using C = TileCfg<VEC>;
-  auto kern = k_spmm_tile_bf16<VEC, ENGINE>;
+                       const __nv_bfloat16* x, int64_t ldx, int vec, int d, float* z, int64_t ldz,
+                       const float* mw = nullptr, int d_out = 0, float* out = nullptr, int64_t ldo = 0) {
+  using C = TileCfg<VEC, FUSED>;
+  auto kern = k_spmm_tile_bf16<VEC, ENGINE, NP, FUSED>;
   HCS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-  kern<<<grid, kTileThreads, C::SMEM, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, vec,
-                                            d, z, ldz, g_tile_prof);
+  kern<<<grid, Roles<NP, ENGINE>::kThreads, C::SMEM, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, vec,
+                                            d, z, ldz, g_tile_prof, mw, d_out, out, ldo);
   HCS_LAUNCH_CHECK("k_spmm_tile_bf16");
   return HCS_OK;
 }
@@ -684,20 +770,61 @@ extern "C" int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int
     const int engine = g_tile_engine >= 0 ? g_tile_engine : 1;  // auto: HMMA (see kernel header)
     int rc;
 #define HCS_TILE_ARGS grid, st, tile_list, n_tile, chunk_ptr, gidx, ent_ptr, e, n_rows, wh, xs, ldx, vec, d, zs, ldz
+#define HCS_TILE_NP(V, E)                                                         \
+    (g_tile_producers == 4 ? launch_tile<V, E, 4>(HCS_TILE_ARGS)                  \
+     : g_tile_producers == 16 ? launch_tile<V, E, 16>(HCS_TILE_ARGS)              \
+                              : launch_tile<V, E, 8>(HCS_TILE_ARGS))
     if (engine == 0) {
-      if (vec > 8) rc = launch_tile<16, 0>(HCS_TILE_ARGS);
-      else if (vec > 4) rc = launch_tile<8, 0>(HCS_TILE_ARGS);
-      else rc = launch_tile<4, 0>(HCS_TILE_ARGS);
+      if (vec > 8) rc = HCS_TILE_NP(16, 0);
+      else if (vec > 4) rc = HCS_TILE_NP(8, 0);
+      else rc = HCS_TILE_NP(4, 0);
     } else {
-      if (vec > 8) rc = launch_tile<16, 1>(HCS_TILE_ARGS);
-      else if (vec > 4) rc = launch_tile<8, 1>(HCS_TILE_ARGS);
-      else rc = launch_tile<4, 1>(HCS_TILE_ARGS);
+      if (vec > 8) rc = HCS_TILE_NP(16, 1);
+      else if (vec > 4) rc = HCS_TILE_NP(8, 1);
+      else rc = HCS_TILE_NP(4, 1);
     }
+#undef HCS_TILE_NP
 #undef HCS_TILE_ARGS
     if (rc) return rc;
   }
   (void)x_rows;
   return HCS_OK;
+}
+
+// K6/K7: tile path with the fused GCN epilogue: out = (A_w X) M per TILE window, plus
+// z = A_w X when z != NULL (the forward z_cache).  M: fp32 [dim x d_out] row-major device
+// matrix (W forward, W^T backward); dim <= 128, d_out <= 128.  mma.sync engine.
+extern "C" int hcs_gcn_tile(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
+                            const int64_t* ent_ptr, const void* ent, int ent_dtype, int64_t n_rows, int32_t wh,
+                            const void* x, int x_dtype, int64_t x_rows, int32_t dim, int64_t ldx, float* z,
+                            int64_t ldz, const float* m, int32_t d_out, float* out, int64_t ldo, void* stream) {
+  HCS_REQUIRE(wh > 0 && wh <= 16, HCS_EINVAL, "tile path supports window heights 1..16 (got %d)", wh);
+  HCS_REQUIRE(dim > 0 && dim <= kMaxOut, HCS_EINVAL, "fused GCN tile path needs 1 <= d_in <= %d (got %d)", kMaxOut,
+              dim);
+  HCS_REQUIRE(d_out > 0 && d_out <= kMaxOut, HCS_EINVAL, "fused GCN tile path needs 1 <= d_out <= %d (got %d)",
+              kMaxOut, d_out);
+  HCS_REQUIRE(x_dtype == HCS_DTYPE_BF16 && ent_dtype == HCS_DTYPE_BF16, HCS_EINVAL,
+              "tile path: only bf16 operands are implemented in this build");
+  HCS_REQUIRE(ldx % 8 == 0 && ldx >= ((dim + 7) / 8) * 8, HCS_EINVAL, "ldx must be a multiple of 8 covering dim");
+  HCS_REQUIRE(((uintptr_t)x & 15) == 0, HCS_EINVAL, "x must be 16-byte aligned");
+  HCS_REQUIRE(m != nullptr && out != nullptr && ldo >= d_out, HCS_EINVAL, "fused GCN: bad M / out arguments");
+  if (n_tile == 0) return HCS_OK;
+  cudaStream_t st = as_stream(stream);
+  const int grid = (int)std::min<int64_t>(n_tile, num_sms());
+  const uint32_t* e = (const uint32_t*)ent;
+  const int vec = (dim + 7) / 8;
+  const __nv_bfloat16* xs = reinterpret_cast<const __nv_bfloat16*>(x);
+  float* zs = z;
+  const int d = dim;
+#define HCS_GCN_ARGS grid, st, tile_list, n_tile, chunk_ptr, gidx, ent_ptr, e, n_rows, wh, xs, ldx, vec, d, zs, ldz, \
+                     m, d_out, out, ldo
+  int rc;
+  if (vec > 8) rc = launch_tile<16, 1, 4, true>(HCS_GCN_ARGS);
+  else if (vec > 4) rc = launch_tile<8, 1, 4, true>(HCS_GCN_ARGS);
+  else rc = launch_tile<4, 1, 4, true>(HCS_GCN_ARGS);
+#undef HCS_GCN_ARGS
+  (void)x_rows;
+  return rc;
 }
 
 // Debug: enable (1) / disable (0) the tile kernel's wait-time counters, or read
@@ -718,6 +845,13 @@ extern "C" int hcs_debug_tile_profile(int enable, unsigned long long* host_out, 
     cudaFree(hcs::g_tile_prof);
     hcs::g_tile_prof = nullptr;
   }
+  return HCS_OK;
+}
+
+// Producer (X-row gather) warps per CTA of the tile kernel: 4, 8 or 16.
+extern "C" int hcs_set_tile_producers(int np) {
+  HCS_REQUIRE(np == 4 || np == 8 || np == 16, HCS_EINVAL, "producer warps must be 4, 8 or 16 (got %d)", np);
+  hcs::g_tile_producers = np;
   return HCS_OK;
 }
 

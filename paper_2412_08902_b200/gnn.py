@@ -132,6 +132,8 @@ def transpose_csr(a: DeviceCsr) -> DeviceCsr:
     """A^T on the device (gnn.py:181-182)."""
     if getattr(a, "symmetric", False):
         return a
+    if "transpose" in a._derived:
+        return a._derived["transpose"]
     dev = a.device
     n_r, n_c = a.num_rows, a.num_cols
     rows = torch.repeat_interleave(torch.arange(n_r, device=dev), a.row_ptr[1:] - a.row_ptr[:-1])
@@ -144,6 +146,7 @@ def transpose_csr(a: DeviceCsr) -> DeviceCsr:
     out = DeviceCsr(n_c, n_r, row_ptr, c, a.values[order])
     if getattr(a, "values_f64", None) is not None:
         out.values_f64 = a.values_f64[order]
+    a._derived["transpose"] = out
     return out
 
 

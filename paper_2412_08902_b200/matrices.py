@@ -199,6 +199,8 @@ class DeviceCsr:
     host_values_f64: np.ndarray | None = field(default=None, repr=False)
     values_f64: torch.Tensor | None = field(default=None, repr=False)  # exact operator values (device)
     symmetric: bool = False  # A == A^T known by construction (e.g. gcn-normalised undirected graph)
+    # derived device structures cached per operator (partitions keyed by (height, selector), A^T)
+    _derived: dict = field(default_factory=dict, repr=False)
 
     @property
     def nnz(self) -> int:

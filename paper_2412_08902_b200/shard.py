@@ -61,3 +61,55 @@ def allgather_rows(local: torch.Tensor, ranges, n_rows: int, wh: int = 16, group
     dist.all_gather_into_tensor(recv, send, group=group)
     parts = [recv[i * maxr: i * maxr + rows[i]] for i in range(world)]
     return torch.cat(parts, 0)
+
+
+class _GatherRows(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, local, shard):
+        ctx.shard = shard
+        return shard.all_gather_rows(local)
+
+    @staticmethod
+    def backward(ctx, g):
+        s = ctx.shard
+        return g[s.row0:s.row1].contiguous(), None
+
+
+class Shard:
+    """This rank's contiguous row range [row0, row1) of a row-window-sharded operator plus
+    the collectives the sharded GCN needs: all-gather of output rows between
+    layers (ragged, padded to the largest shard) and all-reduce(sum) of grad_W."""
+
+    def __init__(self, ranges, rank: int, n_rows: int, wh: int = 16, group=None):
+        self.ranges = ranges
+        self.rank = rank
+        self.world = len(ranges)
+        self.n_rows = n_rows
+        self.wh = wh
+        self.group = group
+        self.row0 = min(ranges[rank][0] * wh, n_rows)
+        self.row1 = min(ranges[rank][1] * wh, n_rows)
+
+    @classmethod
+    def from_operator(cls, a: DeviceCsr, world: int, rank: int, wh: int = 16, group=None) -> "Shard":
+        return cls(shard_window_ranges(a.row_ptr, a.num_rows, world, wh), rank, a.num_rows, wh, group)
+
+    def local_operator(self, a: DeviceCsr) -> DeviceCsr:
+        return row_slice(a, self.row0, self.row1)
+
+    def all_gather_rows(self, local: torch.Tensor) -> torch.Tensor:
+        return allgather_rows(local.contiguous(), self.ranges, self.n_rows, self.wh, self.group)
+
+    def all_gather_rows_autograd(self, local: torch.Tensor) -> torch.Tensor:
+        return _GatherRows.apply(local, self)
+
+    def all_reduce(self, t: torch.Tensor) -> None:
+        import torch.distributed as dist
+
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+
+    def embed_rows(self, local: torch.Tensor) -> torch.Tensor:
+        """A full-height tensor holding `local` in this rank's rows (zeros elsewhere)."""
+        full = torch.zeros((self.n_rows,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+        full[self.row0:self.row1] = local
+        return full

@@ -198,10 +198,14 @@ def partition(csr, window_height: int = WINDOW_HEIGHT, model=None) -> WindowSet:
     from .selector import default_model
 
     dev = _lib.require_cuda()
+    cached = isinstance(csr, DeviceCsr)
     d = to_device_csr(csr, dev)
     n, nnz = d.num_rows, d.nnz
     W = -(-n // window_height)
     sel = _selector_doubles(model if model is not None else default_model())
+    key = ("windows", window_height, sel)
+    if cached and key in d._derived:  # same device operator: windows are a pure function of it
+        return d._derived[key]
     sel_c = (_lib.ctypes.c_double * 7)(*sel)  # host array (read on the host by the ABI)
     ws_bytes = _lib.ctypes.c_size_t(0)
     L = _lib.lib()
@@ -221,7 +225,10 @@ def partition(csr, window_height: int = WINDOW_HEIGHT, model=None) -> WindowSet:
     if nnz:
         _lib.check(L.hcs_partition_fill(d.row_ptr.data_ptr(), d.col_idx.data_ptr(), n, d.num_cols, nnz, window_height,
                                         wcp.data_ptr(), nzc.data_ptr(), cond.data_ptr(), ws.data_ptr(), ws.numel(), s))
-    return WindowSet(d, window_height, wcp, nzc, cond, dens, ci, codes, sel)
+    out = WindowSet(d, window_height, wcp, nzc, cond, dens, ci, codes, sel)
+    if cached:
+        d._derived[key] = out
+    return out
 
 
 def features(window) -> WindowFeatures:
