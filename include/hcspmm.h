@@ -107,6 +107,18 @@ int hcs_gcn_scalar(const int64_t* row_ptr, const int32_t* col_idx, const void* v
                    int64_t x_rows, int32_t dim, int64_t ldx, float* z, int64_t ldz, const float* m, int32_t d_out,
                    float* out, int64_t ldo, void* stream);
 
+/* ---------------------------------------------------------------- K8 LOA
+ * layout.py:186-263 build_windows_optimized (paper Alg. 6): greedy 16-vertex groups
+ * maximising the window's entries-per-column ratio.  order: the sort_by_min_neighbor
+ * permutation (layout.py:99-109, int32 [n], device); outputs out_order int32 [n]
+ * (groups concatenated), gptr int64 [n+1] (group offsets) and *ngroups (device
+ * int64).  One persistent CTA runs the sequential loop; bit-exact with the reference.
+ * workspace: hcs_loa_workspace_bytes (global bitmaps when n is too large for smem). */
+int hcs_loa_workspace_bytes(int64_t n, size_t* bytes);
+int hcs_loa(const int64_t* row_ptr, const int32_t* col_idx, int64_t n, int32_t vw, int32_t group_size,
+            const int32_t* order, int32_t* out_order, int64_t* gptr, int64_t* ngroups, void* workspace,
+            size_t ws_bytes, void* stream);
+
 /* ---------------------------------------------------------------- normalisation
  * gnn.py:68-95 normalize_adj values in float64 with the reference's operation
  * order (structure of A + I assembled by the caller).  kind 0 = gcn
