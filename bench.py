@@ -44,7 +44,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--dim", type=int, default=128)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--config", choices=["c2", "c1", "c3", "c5"], default="c2")
+    p.add_argument("--config", choices=["c2", "c1", "c3", "c4", "c5"], default="c2")
     p.add_argument("--precision", default="bf16")
     p.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU-baseline sampling")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -405,6 +405,67 @@ def run_c3(args):
         dist.destroy_process_group()
 
 
+# ----------------------------------------------------------------------------- C4: LOA on / off
+def run_c4(args):
+    """BASELINE configs[3]: the Reddit-shaped graph with LOA layout reorganisation (vw=128)
+    enabled vs disabled: core-selection split, mean density / CI of non-empty windows
+    (the reference's cmd_loa metrics, cli.py:421-431) and the hybrid SpMM time before/after.
+    LOA runs on the raw undirected adjacency, normalize_adj afterwards (cli.py:501-504)."""
+    import paper_2412_08902_b200 as hc
+    from paper_2412_08902_b200 import graphgen, layout
+    from paper_2412_08902_b200.executors import DeviceOperand, get_plan
+    from paper_2412_08902_b200.gnn import normalize_adj
+    from paper_2412_08902_b200.matrices import Graph
+
+    world, rank, local = dist_setup(args)
+    adj, a, wl_name = make_graph("c2", args.seed)
+    n = a.num_rows
+    g = Graph(n, adj, True)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    torch.cuda.synchronize()
+    ev[0].record()
+    grouping = layout.build_windows_optimized(g, vw=128)
+    ev[1].record()
+    torch.cuda.synchronize()
+    loa_ms = ev[0].elapsed_time(ev[1])
+    t0 = time.perf_counter()
+    g2, perm = layout.reorder(g, grouping)
+    torch.cuda.synchronize()
+    reorder_s = time.perf_counter() - t0
+    a2 = normalize_adj(g2, "gcn")
+    dim = args.dim
+    x = graphgen.dense_features(n, dim, seed=1)
+    res = {}
+    for name, op, xx in (("before", a, x), ("after", a2, x[torch.from_numpy(np.argsort(perm)).cuda()])):
+        ws = hc.partition(op)
+        asg = hc.classify_windows(hc.default_model(), ws)
+        live = ws.ncols() > 0
+        plan = get_plan(ws, asg, "bf16")
+        xop = DeviceOperand(xx.contiguous(), dim, dim, 1)
+        z = torch.empty((n, dim), dtype=torch.float32, device="cuda")
+        for _ in range(max(args.warmup, 3)):
+            plan.run(xop, z, dim)
+        torch.cuda.synchronize()
+        ev[0].record()
+        for _ in range(args.steps):
+            plan.run(xop, z, dim)
+        ev[1].record()
+        torch.cuda.synchronize()
+        ms = ev[0].elapsed_time(ev[1]) / args.steps
+        res[name] = {"tile_windows": asg.count(hc.Path.TILE), "scalar_windows": asg.count(hc.Path.SCALAR),
+                     "mean_density": float(ws.density[live].mean()), "mean_ci": float(ws.ci[live].mean()),
+                     "sum_ncols": int(ws.ncols().sum()), "spmm_ms": ms,
+                     "spmm_gflops": 2.0 * op.nnz * dim / (ms * 1e-3) / 1e9}
+    out = {"metric": "LOA on/off: SpMM GFLOP/s after LOA", "value": res["after"]["spmm_gflops"], "unit": "GFLOP/s",
+           "n_gpus": 1, "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": res["after"]["spmm_ms"],
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+           "data": "synthetic (seeded on-device generator)",
+           "config": {"workload": wl_name + f", LOA vw=128 on vs off, hybrid SpMM dim {dim}", "n": n, "nnz": a.nnz},
+           "loa_ms": loa_ms, "reorder_s": reorder_s, "groups": len(grouping), "before": res["before"],
+           "after": res["after"]}
+    print(json.dumps(out), flush=True)
+
+
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -453,5 +514,7 @@ if __name__ == "__main__":
         run_reference(a)
     elif a.config == "c3":
         run_c3(a)
+    elif a.config == "c4":
+        run_c4(a)
     else:
         run_ours(a)
