@@ -126,8 +126,13 @@ def dist_setup(args):
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("HCS_BENCH_SHARED_GPU") == "1":
+            # test mode for a 1-GPU box: every rank on cuda:0, gloo collectives
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     return world, rank, local
@@ -202,17 +207,23 @@ def run_ours(args):
         if world > 1:
             import torch.distributed as dist
 
+            # exchange between layers: the next layer consumes bf16 features, so rows travel
+            # as bf16 (padded to the largest shard for all_gather_into_tensor)
             rows_per = [min(r[1] * 16, n) - r[0] * 16 for r in ranges]
             maxrows = max(rows_per)
-            send = torch.zeros((maxrows, ldz), dtype=torch.float32, device=dev)
-            gathered = torch.empty((world * maxrows, ldz), dtype=torch.float32, device=dev)
+            send = torch.zeros((maxrows, dim), dtype=torch.bfloat16, device=dev)
+            gathered = torch.empty((world * maxrows, dim), dtype=torch.bfloat16, device=dev)
+            gloo = dist.get_backend() != "nccl"
         tev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
 
         def step(i=None):
             plan.run(xop, z, ldz, tile_events=tev[i] if i is not None else None)
             if world > 1:
-                send[: z.shape[0]].copy_(z)
-                dist.all_gather_into_tensor(gathered, send)
+                send[: z.shape[0]].copy_(z[:, :dim])
+                if gloo:
+                    dist.all_gather(list(gathered.chunk(world)), send)
+                else:
+                    dist.all_gather_into_tensor(gathered, send)
 
         for _ in range(warmup):
             step()
@@ -232,7 +243,7 @@ def run_ours(args):
         ms = s_ev.elapsed_time(e_ev) / steps
         tile_ms = statistics.mean(a.elapsed_time(b) for a, b in tev) if plan.n_tile else 0.0
         if world > 1:
-            t = torch.tensor([ms, tile_ms], device=dev, dtype=torch.float64)
+            t = torch.tensor([ms, tile_ms], device=dev if not gloo else "cpu", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms, tile_ms = float(t[0]), float(t[1])
         e2e = None
@@ -273,7 +284,7 @@ def run_ours(args):
     gather_bytes = sum_ncols * dim * s  # L2 -> SM X-row gather traffic of the tile path (diagnostic)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and world == 1:
         with open(tpath) as fh:
             tr = json.load(fh).get(f"{args.config}_dim{dim}")
         traffic = tr
@@ -294,7 +305,7 @@ def run_ours(args):
             "workload": wl_name + f", hybrid SpMM, feature dim {dim}",
             "n": n, "nnz": nnz, "dim": dim, "windows": len(ws),
             "tile_windows": plan.stats.windows_tile, "scalar_windows": plan.stats.windows_scalar,
-            "sum_ncols": sum_ncols, "aggregate_ci": nnz / max(sum_ncols, 1),
+            "sum_ncols": sum_ncols, "aggregate_ci": local_a.nnz / max(sum_ncols, 1),
             "parallelism": f"row-window shards x{world}" if world > 1 else "single GPU",
             "l2_policy": "inputs larger than L2 (CSR stream 0.69 GB); X kept resident with L2 evict_last hints",
             "preprocess_ms": {"graph_gen_s": t_gen, "partition_select": t_partition_ms, "tile_plan": t_plan_ms},
@@ -302,7 +313,7 @@ def run_ours(args):
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "k_spmm_tile_bf16 (tcgen05)" if plan.n_tile else "k_spmm_scalar",
+                     "kernel": "k_spmm_tile_bf16 (mma.sync engine)" if plan.n_tile else "k_spmm_scalar",
                      "kernel_ms": tile_ms, "algorithmic_bytes": tile_bytes,
                      "l2_gather_GBps": gather_bytes / (tile_ms * 1e-3) / 1e9 if tile_ms > 0 else None},
         "gpu_launches": plan.launches_per_run(dim) * args.steps,
@@ -384,7 +395,7 @@ def run_c3(args):
         torch.cuda.synchronize()
     ms = s_ev.elapsed_time(e_ev) / steps
     if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        t = torch.tensor([ms], device=dev if dist.get_backend() == "nccl" else "cpu", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t[0])
     # SpMM flops of one epoch: fwd L1 (N=128), fwd L2 (N=64), bwd L2 grad_X (N=41)

@@ -159,6 +159,11 @@ def stage_operand(x, precision: str, device, tf32_round: bool = False) -> tuple[
               and t.data_ptr() % 16 == 0 and not tf32_round)
     if direct:
         return DeviceOperand(t, dim, ld, code), was_host
+    if was_host and t.dtype == want and ld == dim and t.is_contiguous() and not tf32_round:
+        # host operand already in the compute dtype: one (async when pinned) H2D copy
+        buf = torch.empty((rows, ld), dtype=want, device=device)
+        buf.copy_(t, non_blocking=True)
+        return DeviceOperand(buf, dim, ld, code), was_host
     buf = torch.zeros((rows, ld), dtype=want, device=device)
     if rows and dim:
         src = t.to(device=device, non_blocking=True)
@@ -287,10 +292,12 @@ def _wrap_result(z: torch.Tensor, dim: int, was_host, stats: ExecStats) -> SpmmR
     """Host inputs give host outputs (numpy for numpy/DenseMatrix input, a CPU tensor
     for a CPU tensor input), device inputs give device outputs."""
     out = z[:, :dim]
-    if was_host == "torch":
-        return SpmmResult(DenseMatrix(out.to("cpu")), stats)
     if was_host:
-        return SpmmResult(DenseMatrix(out.cpu().numpy()), stats)
+        # D2H into pinned memory (torch's caching host allocator reuses the buffer)
+        host = torch.empty(tuple(out.shape), dtype=out.dtype, pin_memory=True)
+        host.copy_(out, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return SpmmResult(DenseMatrix(host if was_host == "torch" else host.numpy()), stats)
     return SpmmResult(DenseMatrix(out if out.is_contiguous() else out.contiguous()), stats)
 
 

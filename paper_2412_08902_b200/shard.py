@@ -58,7 +58,10 @@ def allgather_rows(local: torch.Tensor, ranges, n_rows: int, wh: int = 16, group
     send = torch.zeros((maxr, d), dtype=local.dtype, device=local.device)
     send[: local.shape[0]] = local
     recv = torch.empty((world * maxr, d), dtype=local.dtype, device=local.device)
-    dist.all_gather_into_tensor(recv, send, group=group)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(recv, send, group=group)
+    else:  # gloo (CPU tests): list form
+        dist.all_gather(list(recv.chunk(world)), send, group=group)
     parts = [recv[i * maxr: i * maxr + rows[i]] for i in range(world)]
     return torch.cat(parts, 0)
 
