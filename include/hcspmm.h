@@ -83,13 +83,20 @@ int hcs_spmm_scalar(const int64_t* row_ptr, const int32_t* col_idx, const void* 
                     int64_t x_rows, int32_t dim, int64_t ldx, float* z, int64_t ldz, void* stream);
 
 /* ---------------------------------------------------------------- K4
- * executors.py:111-141 tile_window for every window of a tile plan:
- * tcgen05.mma (bf16 kind::f16) with the gathered X rows as the MN-major A
- * operand (cp.async 16-byte row gathers, 128B swizzle) and the 16-row condensed
- * slab as the K-major B operand; fp32 accumulators in TMEM. */
+ * executors.py:111-141 tile_window for every window of a tile plan.  Engines
+ * (hcs_set_tile_engine): 2 = default, warp-independent workers (each warp owns a
+ * balanced range of (window, 32-feature slice, 64-column chunk) work with its own
+ * cp.async ring and mma.sync m16n8k16, fp32 register accumulators; cut windows are
+ * summed in warp order by a fix-up launch -> deterministic); 1 = warp-specialised
+ * cp.async/TMA pipeline with mma.sync; 0 = the same pipeline with tcgen05.mma
+ * (M = 128 features, N = 16 rows, TMEM accumulators).
+ * workspace: >= hcs_tile_scratch_floats() floats (engine 2 partial sums; unused by 0/1);
+ * one workspace must not be shared by launches that can run concurrently. */
+int hcs_tile_scratch_floats(int64_t* floats);
 int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
                   const int64_t* ent_ptr, const void* ent, int ent_dtype, int64_t n_rows, int32_t wh, const void* x,
-                  int x_dtype, int64_t x_rows, int32_t dim, int64_t ldx, float* z, int64_t ldz, void* stream);
+                  int x_dtype, int64_t x_rows, int32_t dim, int64_t ldx, float* z, int64_t ldz, void* workspace,
+                  size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------- K6 / K7
  * gnn.py:121-159 forward (fused mode) and gnn.py:162-205 backward (fused mode):
@@ -127,9 +134,13 @@ int hcs_loa(const int64_t* row_ptr, const int32_t* col_idx, int64_t n, int32_t v
 int hcs_normalize_values(int kind, const int64_t* row_ptr, const int32_t* col, const double* v_in, int64_t n,
                          double* workspace_deg, double* v_out, float* v_out32, void* stream);
 
-/* tile-path MMA engine: -1 auto (default), 0 tcgen05.mma (TMEM accumulators),
- * 1 mma.sync m16n8k16 (register accumulators); both share the cp.async gather pipeline */
+/* tile-path engine: -1 auto (= 2), 0 tcgen05.mma pipeline, 1 mma.sync pipeline,
+ * 2 warp-independent mma.sync workers (see K4) */
 int hcs_set_tile_engine(int engine);
+
+/* debug: tile-kernel experiment switches (bit0 skip MMA, bit1 skip slab build,
+ * bit2 skip X gathers; results are wrong when set), 0 = normal */
+int hcs_debug_tile_switches(int bits);
 
 /* tile-path producer (X-row gather) warps per CTA: 4 (default), 8 or 16 */
 int hcs_set_tile_producers(int np);

@@ -52,13 +52,25 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
+#ifndef HCS_MBAR_SUSPEND_HINT
+#define HCS_MBAR_SUSPEND_HINT 0  // 0: try_wait without a suspend-time hint (hardware default)
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
+#if HCS_MBAR_SUSPEND_HINT
   asm volatile(
       "{\n .reg .pred P1;\n HCS_WAIT_%=:\n"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
       "@P1 bra HCS_DONE_%=;\n bra HCS_WAIT_%=;\n HCS_DONE_%=:\n }" ::"r"(smem_u32(b)),
-      "r"(phase), "r"(0x989680)
+      "r"(phase), "r"(HCS_MBAR_SUSPEND_HINT)
       : "memory");
+#else
+  asm volatile(
+      "{\n .reg .pred P1;\n HCS_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra HCS_DONE_%=;\n bra HCS_WAIT_%=;\n HCS_DONE_%=:\n }" ::"r"(smem_u32(b)),
+      "r"(phase)
+      : "memory");
+#endif
 }
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -26,6 +26,7 @@
 // pointers) is prefetched far ahead because loads complete in issue order behind
 // the gathers in the SM's L1TEX queue.
 #include "common.cuh"
+#include "mma_helpers.cuh"
 
 namespace hcs {
 
@@ -54,41 +55,6 @@ constexpr int kEntCapPerChunk = 128;
 #ifndef HCS_TILE_NOINC
 #define HCS_TILE_NOINC 1  // 1: cp.async.mbarrier.arrive.noinc completion, 0: commit/wait_group publish
 #endif  // staged packed entries per chunk; the rest is read from global
-
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes, uint64_t pol) {
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(dst), "l"(src),
-               "r"(src_bytes), "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-__device__ __forceinline__ void named_bar_sync(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(addr));
-}
-__device__ __forceinline__ void ldsm_x4_trans(uint32_t (&r)[4], uint32_t addr) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(addr));
-}
-__device__ __forceinline__ void hmma_16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
 
 // first t in [0, n] with a[t] >= v  (a non-decreasing, length n+1)
 __device__ __forceinline__ int64_t lower_bound_i64(const int64_t* __restrict__ a, int64_t n, int64_t v) {
@@ -241,10 +207,6 @@ __device__ __forceinline__ int64_t count_stages(const int64_t* __restrict__ chun
 // Measured on B200 (tools/probe/mma_rate, hmma_rate): a tcgen05.mma has a ~45-cycle
 // floor per instruction for N <= 64, so the 16-row window shape runs ~8x below the
 // tensor-core peak, while HMMA.16816 sustains ~2 cycles per instruction per SM.
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-  const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);  // RNE
-  return *reinterpret_cast<const uint32_t*>(&h);
-}
 
 template <int VEC, int ENGINE, int NP, bool FUSED>
 __global__ void __launch_bounds__(Roles<NP, ENGINE>::kThreads, 1)
@@ -253,7 +215,7 @@ __global__ void __launch_bounds__(Roles<NP, ENGINE>::kThreads, 1)
                      const uint32_t* __restrict__ ent, int64_t n_rows, int wh, const __nv_bfloat16* __restrict__ x,
                      int64_t ldx, int vec, int dim, float* __restrict__ z, int64_t ldz,
                      unsigned long long* __restrict__ prof, const float* __restrict__ mw, int d_out,
-                     float* __restrict__ out, int64_t ldo) {
+                     float* __restrict__ out, int64_t ldo, int dbg) {
   using C = TileCfg<VEC, FUSED>;
   using R = Roles<NP, ENGINE>;
   constexpr int kProducers = R::kProducers, kIdxWarp = R::kIdxWarp, kEntWarp = R::kEntWarp;
@@ -356,7 +318,8 @@ __global__ void __launch_bounds__(Roles<NP, ENGINE>::kThreads, 1)
 #pragma unroll
       for (int it = 0; it < ITERS; ++it) {
         if (G == 1 || it * RPI < lim) {
-          cp_async16(a_st + dofs[it], xl + (int64_t)max(gi[it], 0) * ldxb, gi[it] >= 0 ? vbytes : 0u, keep);
+          if (!(dbg & 4))
+            cp_async16(a_st + dofs[it], xl + (int64_t)max(gi[it], 0) * ldxb, gi[it] >= 0 ? vbytes : 0u, keep);
         }
       }
 #if HCS_TILE_NOINC
@@ -396,9 +359,13 @@ __global__ void __launch_bounds__(Roles<NP, ENGINE>::kThreads, 1)
       TPROF(3, mbar_wait(&idx_empty[islot], iphase ^ 1));
       if (lane == 0) {
         idx_g[islot] = g;
+        if (dbg & 16) {
+          mbar_arrive(&idx_full[islot]);
+        } else {
         mbar_expect_tx(&idx_full[islot], (uint32_t)g * 256u);
         tma_bulk_g2s(sbase + C::OFF_IDX + islot * C::IDX_SLOT, gidx + cur.c * 64, (uint32_t)g * 256u,
                      &idx_full[islot], strm);
+        }
       }
       __syncwarp();
       if (++islot == C::IDX_SLOTS) { islot = 0; iphase ^= 1; }
@@ -433,8 +400,9 @@ __global__ void __launch_bounds__(Roles<NP, ENGINE>::kThreads, 1)
         info[stage].g = g;
         info[stage].flags = (int16_t)((first ? 1 : 0) | (last ? 2 : 0));
         info[stage].skew = (int16_t)((epj[0] * 4 - b0) >> 2);
-        mbar_expect_tx(&full[stage], bytes);
-        if (bytes) tma_bulk_g2s(sbase + C::OFF_ENT + stage * C::STAGE_ENT, entb + b0, bytes, &full[stage], strm);
+        if (dbg & 8) mbar_arrive(&full[stage]);
+        else mbar_expect_tx(&full[stage], bytes);
+        if (bytes && !(dbg & 8)) tma_bulk_g2s(sbase + C::OFF_ENT + stage * C::STAGE_ENT, entb + b0, bytes, &full[stage], strm);
       }
       __syncwarp();
       if (++stage == S) { stage = 0; phase ^= 1; }
@@ -462,7 +430,8 @@ __global__ void __launch_bounds__(Roles<NP, ENGINE>::kThreads, 1)
       const int cap = G * kEntCapPerChunk - skew;  // entries available in the staged copy
       // entry = bf16 value << 16 | byte offset in its chunk's swizzled slab (precomputed by the plan)
       const int ne = (int)(inf.ep[g] - e0);
-      if (ne <= cap) {
+      if (dbg & 2) {
+      } else if (ne <= cap) {
         // fast path: all entries staged; chunk j's slab starts 2 KB after chunk j-1's
         int bq[G];  // first entry of chunk q (q >= g: past the end)
 #pragma unroll
@@ -540,7 +509,7 @@ __global__ void __launch_bounds__(Roles<NP, ENGINE>::kThreads, 1)
         // steps (j, ks) of this warp, software-pipelined: fragments of step s+1 load during the MMAs of s
         const int nsteps = ((g - kp + KS - 1) / KS) * 4;  // chunks kp, kp+KS, ... below g, 4 K-steps each
         (void)nsteps;
-        for (int j = kp; j < g; j += KS) {
+        for (int j = kp; j < ((dbg & 1) ? 0 : g); j += KS) {
           const uint32_t sl = b_st + j * 2048;
           // the 4 K-steps' fragments are all loaded before the MMAs (latency overlap)
           uint32_t a[4][4], b0[4][4], b1[4][4];
@@ -728,6 +697,7 @@ __global__ void __launch_bounds__(Roles<NP, ENGINE>::kThreads, 1)
 
 static unsigned long long* g_tile_prof = nullptr;  // debug wait-time counters (nullptr = off)
 static int g_tile_engine = -1;                     // -1 auto, 0 tcgen05, 1 mma.sync
+static int g_tile_debug = 0;                       // experiment switches (bit0 no MMA, bit1 no build, bit2 no gather)
 static int g_tile_producers = 4;                   // producer warps per CTA: 4, 8 or 16
 
 template <int VEC, int ENGINE, int NP, bool FUSED = false>
@@ -739,7 +709,7 @@ static int launch_tile(int grid, cudaStream_t st, const int32_t* tile_list, int6
   auto kern = k_spmm_tile_bf16<VEC, ENGINE, NP, FUSED>;
   HCS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
   kern<<<grid, Roles<NP, ENGINE>::kThreads, C::SMEM, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, vec,
-                                            d, z, ldz, g_tile_prof, mw, d_out, out, ldo);
+                                            d, z, ldz, g_tile_prof, mw, d_out, out, ldo, g_tile_debug);
   HCS_LAUNCH_CHECK("k_spmm_tile_bf16");
   return HCS_OK;
 }
@@ -748,10 +718,17 @@ static int launch_tile(int grid, cudaStream_t st, const int32_t* tile_list, int6
 
 using namespace hcs;
 
+namespace hcs {
+int spmm_tile_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
+                   const int64_t* ent_ptr, const uint32_t* ent, int64_t n_rows, int wh, const __nv_bfloat16* x,
+                   int64_t ldx, int dim, float* z, int64_t ldz, float* scratch, int64_t scratch_floats,
+                   cudaStream_t st);
+}  // namespace hcs
+
 extern "C" int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
                              const int64_t* ent_ptr, const void* ent, int ent_dtype, int64_t n_rows, int32_t wh,
                              const void* x, int x_dtype, int64_t x_rows, int32_t dim, int64_t ldx, float* z,
-                             int64_t ldz, void* stream) {
+                             int64_t ldz, void* workspace, size_t ws_bytes, void* stream) {
   HCS_REQUIRE(wh > 0 && wh <= 16, HCS_EINVAL, "tile path supports window heights 1..16 (got %d)", wh);
   HCS_REQUIRE(dim > 0, HCS_EINVAL, "dim must be positive");
   HCS_REQUIRE(x_dtype == HCS_DTYPE_BF16 && ent_dtype == HCS_DTYPE_BF16, HCS_EINVAL,
@@ -762,12 +739,19 @@ extern "C" int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int
   cudaStream_t st = as_stream(stream);
   const int grid = (int)std::min<int64_t>(n_tile, num_sms());
   const uint32_t* e = (const uint32_t*)ent;
+  const int eng = g_tile_engine >= 0 ? g_tile_engine : 2;  // auto: warp-independent kernel
+  if (eng == 2) {
+    HCS_REQUIRE(((uintptr_t)z & 7) == 0 && ldz % 2 == 0, HCS_EINVAL, "z must be 8-byte aligned with even ldz");
+    return spmm_tile_warp(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, (const uint32_t*)ent, n_rows, wh,
+                          (const __nv_bfloat16*)x, ldx, dim, z, ldz, (float*)workspace,
+                          (int64_t)(ws_bytes / sizeof(float)), st);
+  }
   for (int f0 = 0; f0 < dim; f0 += 128) {
     const int d = std::min(128, dim - f0);
     const int vec = (d + 7) / 8;
     const __nv_bfloat16* xs = reinterpret_cast<const __nv_bfloat16*>(x) + f0;
     float* zs = z + f0;
-    const int engine = g_tile_engine >= 0 ? g_tile_engine : 1;  // auto: HMMA (see kernel header)
+    const int engine = eng;
     int rc;
 #define HCS_TILE_ARGS grid, st, tile_list, n_tile, chunk_ptr, gidx, ent_ptr, e, n_rows, wh, xs, ldx, vec, d, zs, ldz
 #define HCS_TILE_NP(V, E)                                                         \
@@ -848,6 +832,13 @@ extern "C" int hcs_debug_tile_profile(int enable, unsigned long long* host_out, 
   return HCS_OK;
 }
 
+// Experiment switches of the tile kernel (results are wrong when set): bit0 skip MMAs,
+// bit1 skip slab builds, bit2 skip X-row gathers.  0 = normal operation.
+extern "C" int hcs_debug_tile_switches(int bits) {
+  hcs::g_tile_debug = bits;
+  return HCS_OK;
+}
+
 // Producer (X-row gather) warps per CTA of the tile kernel: 4, 8 or 16.
 extern "C" int hcs_set_tile_producers(int np) {
   HCS_REQUIRE(np == 4 || np == 8 || np == 16, HCS_EINVAL, "producer warps must be 4, 8 or 16 (got %d)", np);
@@ -857,7 +848,8 @@ extern "C" int hcs_set_tile_producers(int np) {
 
 // Select the tile-path MMA engine: -1 auto (default), 0 tcgen05.mma, 1 mma.sync m16n8k16.
 extern "C" int hcs_set_tile_engine(int engine) {
-  HCS_REQUIRE(engine >= -1 && engine <= 1, HCS_EINVAL, "engine must be -1 (auto), 0 (tcgen05) or 1 (mma.sync)");
+  HCS_REQUIRE(engine >= -1 && engine <= 2, HCS_EINVAL,
+              "engine must be -1 (auto), 0 (tcgen05), 1 (mma.sync pipeline) or 2 (warp-independent mma.sync)");
   hcs::g_tile_engine = engine;
   return HCS_OK;
 }

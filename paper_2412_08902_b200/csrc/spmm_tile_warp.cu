@@ -1,0 +1,348 @@
+// K4 (default engine): warp-independent tensor-core tile path (executors.py:111-141
+// tile_window) on sm_100a.
+//
+// Measured on B200 (profiles/r01_tile_switches_c2.txt): the warp-specialised
+// producer/builder/MMA pipeline of spmm_tile.cu spends ~3.8 ms of its 5.0 ms
+// (C2, N = 128) in per-chunk cross-warp hand-offs alone.  Here every warp is an
+// independent worker with its own cp.async ring, so no barrier is shared between
+// warps on the per-chunk path:
+//
+//   unit  = (TILE window t, 32-feature slice f); a window's condensed columns are
+//           processed in the K2 plan's 64-column chunks (tile_plan.cu);
+//   warp  = a contiguous, exactly balanced range [a, b) of the flattened
+//           (unit, chunk) sequence; ranges may cut a unit, whose partial sums then
+//           go to two scratch slots per warp and are added in warp order by
+//           k_tile_warp_fixup (deterministic, no float atomics);
+//   chunk = gather 64 X-row slices of 64 B (cp.async 16 B, L2 evict_last, 3-stage
+//           ring per warp, XOR-swizzled for conflict-free ldmatrix.trans), build the
+//           16 x 64 bf16 slab from the packed entries (prefetched into registers one
+//           chunk ahead), then 4 k16 steps x 4 n8 tiles of mma.sync m16n8k16 with
+//           fp32 accumulators in registers;
+//   store = the window's 16 x 32 fp32 slice straight to Z.
+// The slab of a chunk is rebuilt by each of the window's FS slice-warps (cheap:
+// ~70 entries); the X traffic is the same Σncols·N·2 bytes as before.
+#include "common.cuh"
+#include "mma_helpers.cuh"
+
+namespace hcs {
+
+constexpr int kWarpTileWarps = 16;   // warps per CTA
+constexpr int kWarpTileStages = 3;   // cp.async ring depth per warp
+constexpr int kWarpStageBytes = 64 * 64;  // 64 gathered rows x 64 B (one 32-feature slice)
+constexpr int kWarpSlabBytes = 16 * 64 * 2;
+constexpr int kWarpSmemPerWarp = kWarpTileStages * kWarpStageBytes + kWarpSlabBytes;
+constexpr int kWarpTileSmem = kWarpTileWarps * kWarpSmemPerWarp + 128;
+constexpr int kWarpEntRegs = 4;      // packed entries per lane held in registers (128 per chunk)
+constexpr int kSlotFloats = 16 * 32;  // one 16 x 32 fp32 partial
+
+// Position in the flattened (unit, chunk) sequence of one warp.
+struct ChunkPos {
+  int64_t t;     // index into tile_list
+  int64_t base;  // chunk_ptr[t]
+  int64_t fi;    // flattened index
+  int32_t f, j, nj;
+};
+
+__device__ __forceinline__ int64_t ldg64(const int64_t* p) { return __ldg(p); }
+
+// unit containing flattened chunk index v (0 <= v < FS * chunk_ptr[T])
+__device__ __forceinline__ ChunkPos locate(const int64_t* __restrict__ chunk_ptr, int64_t T, int FS, int64_t v) {
+  int64_t lo = 0, hi = T;  // largest t with FS*chunk_ptr[t] <= v
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (FS * ldg64(chunk_ptr + mid) <= v) lo = mid; else hi = mid;
+  }
+  ChunkPos p;
+  p.t = lo;
+  p.base = ldg64(chunk_ptr + lo);
+  p.nj = (int32_t)(ldg64(chunk_ptr + lo + 1) - p.base);
+  const int64_t rem = v - FS * p.base;
+  p.f = (int32_t)(rem / p.nj);
+  p.j = (int32_t)(rem - (int64_t)p.f * p.nj);
+  p.fi = v;
+  return p;
+}
+
+__device__ __forceinline__ void advance(ChunkPos& p, const int64_t* __restrict__ chunk_ptr, int64_t T, int FS) {
+  ++p.fi;
+  if (++p.j < p.nj) return;
+  p.j = 0;
+  if (++p.f < FS) return;
+  p.f = 0;
+  ++p.t;
+  p.base += p.nj;
+  p.nj = p.t < T ? (int32_t)(ldg64(chunk_ptr + p.t + 1) - p.base) : 1;  // past the end: never used
+}
+
+__device__ __forceinline__ void warp_range(int64_t total, int64_t nwarps, int64_t gw, int64_t& a, int64_t& b) {
+  a = (total * gw) / nwarps;
+  b = (total * (gw + 1)) / nwarps;
+}
+
+__device__ __forceinline__ void store_slice(float* __restrict__ z, int64_t ldz, int64_t rs, int rows, int dim, int f,
+                                            const float (&acc)[4][4], int lane) {
+  const int r0 = lane >> 2, cc = (lane & 3) * 2;
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt) {
+    const int col = f * 32 + nt * 8 + cc;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = r0 + 8 * h;
+      if (r < rows) {
+        float* zp = z + (rs + r) * ldz + col;
+        if (col + 1 < dim) {
+          *reinterpret_cast<float2*>(zp) = make_float2(acc[nt][2 * h], acc[nt][2 * h + 1]);
+        } else if (col < dim) {
+          zp[0] = acc[nt][2 * h];
+        }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kWarpTileWarps * 32, 1)
+    k_tile_warp(const int32_t* __restrict__ tile_list, int64_t T, const int64_t* __restrict__ chunk_ptr,
+                const int32_t* __restrict__ gidx, const int64_t* __restrict__ ent_ptr,
+                const uint32_t* __restrict__ ent, int64_t n_rows, int wh, const __nv_bfloat16* __restrict__ x,
+                int64_t ldx, int dim, int FS, float* __restrict__ z, int64_t ldz, float* __restrict__ scratch) {
+  extern __shared__ uint8_t wsmem_raw[];
+  uint8_t* wsmem = (uint8_t*)(((uintptr_t)wsmem_raw + 127) & ~(uintptr_t)127);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * kWarpTileWarps;
+  const int64_t gw = (int64_t)blockIdx.x * kWarpTileWarps + warp;
+  const int64_t total = (int64_t)FS * chunk_ptr[T];
+  int64_t a, b;
+  warp_range(total, nwarps, gw, a, b);
+  if (a >= b) return;
+
+  const uint32_t stage0 = smem_u32(wsmem + warp * kWarpSmemPerWarp);
+  const uint32_t slab = stage0 + kWarpTileStages * kWarpStageBytes;
+  uint8_t* slab_p = wsmem + warp * kWarpSmemPerWarp + kWarpTileStages * kWarpStageBytes;
+  const uint64_t keep = policy_evict_last();
+  const char* xb = reinterpret_cast<const char*>(x);
+  const int64_t ldxb = ldx * 2;
+  // gather lane mapping: 4 lanes x 16 B per 64-B row slice, 8 rows per instruction
+  const int grow = lane >> 2, gv = lane & 3;
+  // ldmatrix lane mapping (A: slab rows, B: gathered rows k, 8-feature chunks)
+  const int ar = lane & 15, akc = lane >> 4;
+  const int bk = (lane & 7) + ((lane >> 3) & 1) * 8, bfc = lane >> 4;
+
+  // pipeline positions: p0 = chunk being computed, p1, p2 (gathers in flight), p3 (indices prefetched)
+  ChunkPos p0 = locate(chunk_ptr, T, FS, a);
+  ChunkPos p1 = p0, p2, p3;
+  advance(p1, chunk_ptr, T, FS);
+  p2 = p1;
+  advance(p2, chunk_ptr, T, FS);
+  p3 = p2;
+  advance(p3, chunk_ptr, T, FS);
+  bool in_head = p0.j != 0;  // our first unit (t, f) began in an earlier warp's range
+
+  auto load_gidx = [&](const ChunkPos& p, int (&g)[8]) {
+    if (p.fi < b) {
+      const int32_t* gp = gidx + (p.base + p.j) * 64 + grow;
+#pragma unroll
+      for (int it = 0; it < 8; ++it) g[it] = __ldg(gp + 8 * it);
+    }
+  };
+  auto issue = [&](const ChunkPos& p, const int (&g)[8], int slot) {
+    if (p.fi < b) {
+      const int feat = p.f * 32 + gv * 8;
+      const uint32_t vb = feat < dim ? 16u : 0u;
+      const char* src = xb + (int64_t)feat * 2;
+      const uint32_t dst = stage0 + slot * kWarpStageBytes;
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const int row = grow + 8 * it;
+        const int gi = g[it];
+        cp_async16(dst + row * 64 + ((gv ^ ((row >> 1) & 3)) << 4), src + (int64_t)max(gi, 0) * ldxb,
+                   gi >= 0 ? vb : 0u, keep);
+      }
+    }
+    cp_async_commit();
+  };
+  auto load_ep = [&](const ChunkPos& p, int64_t& e0, int64_t& e1) {
+    if (p.fi < b) {
+      const int64_t c = p.base + p.j;
+      e0 = __ldg(ent_ptr + c);
+      e1 = __ldg(ent_ptr + c + 1);
+    } else {
+      e0 = e1 = 0;
+    }
+  };
+  auto load_ent = [&](int64_t e0, int64_t e1, uint32_t (&e)[kWarpEntRegs]) {
+#pragma unroll
+    for (int q = 0; q < kWarpEntRegs; ++q) {
+      const int64_t i = e0 + lane + 32 * q;
+      e[q] = i < e1 ? __ldg(ent + i) : 0u;
+    }
+  };
+
+  int g_a[8], g_b[8];
+  // prologue: gathers of p0, p1 in flight; indices of p2; entries of p0; entry pointers of p1
+  load_gidx(p0, g_a);
+  load_gidx(p1, g_b);
+  issue(p0, g_a, 0);
+  issue(p1, g_b, 1);
+  int g2[8];
+  load_gidx(p2, g2);
+  int64_t ep0a, ep0b, ep1a, ep1b;
+  load_ep(p0, ep0a, ep0b);
+  load_ep(p1, ep1a, ep1b);
+  uint32_t e0r[kWarpEntRegs], e1r[kWarpEntRegs];
+  load_ent(ep0a, ep0b, e0r);
+
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+
+  int s0 = 0;  // ring slot of p0
+  for (; p0.fi < b;) {
+    // 1. gathers of p2 (slot s0+2), then indices of p3 for the next iteration
+    const int s2 = s0 >= 1 ? s0 - 1 : s0 + 2;
+    issue(p2, g2, s2);
+    load_gidx(p3, g2);
+    // 2. entries of p1 (used next iteration), entry pointers of p2
+    load_ent(ep1a, ep1b, e1r);
+    int64_t ep2a, ep2b;
+    load_ep(p2, ep2a, ep2b);
+    // 3. slab of p0: zero, scatter packed entries (bf16 value << 16 | swizzled byte offset)
+    {
+      const int4 zero4 = make_int4(0, 0, 0, 0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) reinterpret_cast<int4*>(slab_p)[lane + 32 * q] = zero4;
+      __syncwarp();
+      const int ne = (int)(ep0b - ep0a);
+#pragma unroll
+      for (int q = 0; q < kWarpEntRegs; ++q)
+        if (lane + 32 * q < ne) *reinterpret_cast<uint16_t*>(slab_p + (e0r[q] & 0x7FFu)) = (uint16_t)(e0r[q] >> 16);
+      for (int i = 32 * kWarpEntRegs + lane; i < ne; i += 32) {  // rare: > 128 entries in a chunk
+        const uint32_t w = __ldg(ent + ep0a + i);
+        *reinterpret_cast<uint16_t*>(slab_p + (w & 0x7FFu)) = (uint16_t)(w >> 16);
+      }
+    }
+    // 4. p0's gathers landed (the two newest groups may still be in flight)
+    cp_async_wait<2>();
+    __syncwarp();
+    // 5. 64 x 32 slice: 4 k16 steps x 4 n8 tiles
+    {
+      const uint32_t st = stage0 + s0 * kWarpStageBytes;
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        uint32_t af[4], b01[4], b23[4];
+        const int kc = 2 * ks + akc;
+        ldsm_x4(af, slab + ar * 128 + (((kc ^ ar) & 7) << 4));
+        const int k = ks * 16 + bk;
+        const uint32_t rowa = st + k * 64;
+        const int sw = (k >> 1) & 3;
+        ldsm_x4_trans(b01, rowa + ((bfc ^ sw) << 4));
+        ldsm_x4_trans(b23, rowa + (((2 + bfc) ^ sw) << 4));
+        hmma_16816(acc[0], af, b01[0], b01[1]);
+        hmma_16816(acc[1], af, b01[2], b01[3]);
+        hmma_16816(acc[2], af, b23[0], b23[1]);
+        hmma_16816(acc[3], af, b23[2], b23[3]);
+      }
+    }
+    __syncwarp();
+    // 6. end of our part of the unit: Z (whole unit) or a scratch slot (split unit)
+    const bool unit_done = p0.j + 1 == p0.nj;
+    if (unit_done || p0.fi + 1 == b) {
+      const int64_t rs = (int64_t)__ldg(tile_list + p0.t) * wh;
+      const int rows = (int)(n_rows - rs < wh ? n_rows - rs : wh);
+      if (!in_head && unit_done) {
+        store_slice(z, ldz, rs, rows, dim, p0.f, acc, lane);
+      } else {
+        float* slot = scratch + (gw * 2 + (in_head ? 0 : 1)) * kSlotFloats;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) slot[(nt * 4 + q) * 32 + lane] = acc[nt][q];
+      }
+      in_head = false;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+    }
+    // 7. rotate the pipeline
+    p0 = p1;
+    p1 = p2;
+    p2 = p3;
+    advance(p3, chunk_ptr, T, FS);
+#pragma unroll
+    for (int q = 0; q < kWarpEntRegs; ++q) e0r[q] = e1r[q];
+    ep0a = ep1a;
+    ep0b = ep1b;
+    ep1a = ep2a;
+    ep1b = ep2b;
+    s0 = s0 == kWarpTileStages - 1 ? 0 : s0 + 1;
+  }
+  cp_async_wait<0>();
+}
+
+// Sums the partial slots of units cut by warp-range boundaries, in warp order.
+__global__ void k_tile_warp_fixup(const int32_t* __restrict__ tile_list, int64_t T,
+                                  const int64_t* __restrict__ chunk_ptr, int64_t n_rows, int wh, int dim, int FS,
+                                  float* __restrict__ z, int64_t ldz, const float* __restrict__ scratch,
+                                  int64_t nwarps) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (gw >= nwarps) return;
+  const int64_t total = (int64_t)FS * chunk_ptr[T];
+  int64_t a, b;
+  warp_range(total, nwarps, gw, a, b);
+  if (a >= b) return;
+  const ChunkPos last = locate(chunk_ptr, T, FS, b - 1);
+  const int64_t ustart = (int64_t)FS * last.base + (int64_t)last.f * last.nj;
+  const int64_t uend = ustart + last.nj;
+  if (!(uend > b && ustart >= a)) return;  // not the warp that opens a split unit
+  float acc[4][4];
+  const float* s = scratch + (gw * 2 + 1) * kSlotFloats;
+#pragma unroll
+  for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[nt][q] = s[(nt * 4 + q) * 32 + lane];
+  for (int64_t k = gw + 1; k < nwarps; ++k) {
+    int64_t ak, bk;
+    warp_range(total, nwarps, k, ak, bk);
+    if (ak >= bk) continue;
+    const float* sk = scratch + (k * 2 + 0) * kSlotFloats;
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[nt][q] += sk[(nt * 4 + q) * 32 + lane];
+    if (uend <= bk) break;
+  }
+  const int64_t rs = (int64_t)tile_list[last.t] * wh;
+  const int rows = (int)(n_rows - rs < wh ? n_rows - rs : wh);
+  store_slice(z, ldz, rs, rows, dim, last.f, acc, lane);
+}
+
+int spmm_tile_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
+                   const int64_t* ent_ptr, const uint32_t* ent, int64_t n_rows, int wh, const __nv_bfloat16* x,
+                   int64_t ldx, int dim, float* z, int64_t ldz, float* scratch, int64_t scratch_floats,
+                   cudaStream_t st) {
+  const int FS = (dim + 31) / 32;
+  const int grid = num_sms();
+  const int64_t nwarps = (int64_t)grid * kWarpTileWarps;
+  HCS_REQUIRE(scratch != nullptr && scratch_floats >= nwarps * 2 * kSlotFloats, HCS_EINVAL,
+              "tile scratch too small (%lld floats, need %lld)", (long long)scratch_floats,
+              (long long)(nwarps * 2 * kSlotFloats));
+  HCS_CUDA(cudaFuncSetAttribute(k_tile_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, kWarpTileSmem));
+  k_tile_warp<<<grid, kWarpTileWarps * 32, kWarpTileSmem, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent,
+                                                                n_rows, wh, x, ldx, dim, FS, z, ldz, scratch);
+  HCS_LAUNCH_CHECK("k_tile_warp");
+  const int fix_threads = 256;
+  const int fix_blocks = (int)((nwarps * 32 + fix_threads - 1) / fix_threads);
+  k_tile_warp_fixup<<<fix_blocks, fix_threads, 0, st>>>(tile_list, n_tile, chunk_ptr, n_rows, wh, dim, FS, z, ldz,
+                                                         scratch, nwarps);
+  HCS_LAUNCH_CHECK("k_tile_warp_fixup");
+  return HCS_OK;
+}
+
+int64_t tile_warp_scratch_floats() { return (int64_t)num_sms() * kWarpTileWarps * 2 * kSlotFloats; }
+
+}  // namespace hcs
+
+extern "C" int hcs_tile_scratch_floats(int64_t* floats) {
+  HCS_REQUIRE(floats != nullptr, HCS_EINVAL, "floats is NULL");
+  *floats = hcs::tile_warp_scratch_floats();
+  return HCS_OK;
+}

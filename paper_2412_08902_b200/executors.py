@@ -226,8 +226,17 @@ class HybridPlan:
         else:
             self.scalar_vals, self.scalar_vals_code = csr.values, _lib.DTYPE_F32
 
+    def scratch(self) -> torch.Tensor:
+        """Partial-sum slots of the tile kernel (engine 2); one per plan, stream-ordered use."""
+        if getattr(self, "_scratch", None) is None:
+            n = _lib.ctypes.c_int64(0)
+            _lib.check(_lib.lib().hcs_tile_scratch_floats(_lib.ctypes.byref(n)))
+            self._scratch = torch.empty(max(int(n.value), 1), dtype=torch.float32, device=self.tile_list.device)
+        return self._scratch
+
     def launches_per_run(self, dim: int) -> int:
-        return (-(-dim // 128) if self.n_tile else 0) + (1 if self.scalar_list.numel() else 0)
+        """Kernels of one run(): engine 2 = tile kernel + fix-up, plus the scalar kernel."""
+        return (2 if self.n_tile else 0) + (1 if self.scalar_list.numel() else 0)
 
     def run(self, xop: DeviceOperand, z: torch.Tensor, ldz: int, stream=None, tile_events=None) -> None:
         """Launch K4 (tile windows) then K3 (scalar + empty windows) on the current stream.
@@ -239,10 +248,11 @@ class HybridPlan:
         if self.n_tile:
             if self.precision != "bf16":
                 raise NotImplementedError("tf32 tile kernel not built in this revision; use precision='bf16'")
+            scratch = self.scratch()
             _lib.call("hcs_spmm_tile", self.tile_list.data_ptr(), self.n_tile, self.chunk_ptr.data_ptr(),
                       self.gidx.data_ptr(), self.ent_ptr.data_ptr(), self.ent.data_ptr(), self.ent_dtype,
                       csr.num_rows, self.windows.window_height, xop.t.data_ptr(), xop.dtype_code, xop.rows, xop.dim,
-                      xop.ld, z.data_ptr(), ldz, s)
+                      xop.ld, z.data_ptr(), ldz, scratch.data_ptr(), scratch.numel() * 4, s)
         if tile_events is not None:
             tile_events[1].record()
         if self.scalar_list.numel():
@@ -362,13 +372,13 @@ def spmm_auto(csr, x, assignment_for, precision: str = "bf16", threads: int = 1)
     return spmm_hybrid(windows, assignment_for(windows), x, precision=precision, threads=threads)
 
 
-_ENGINES = {"auto": -1, "tcgen05": 0, "mma_sync": 1}
+_ENGINES = {"auto": -1, "tcgen05": 0, "mma_sync": 1, "warp": 2}
 
 
 def set_tile_engine(engine: str = "auto") -> None:
-    """Select the tensor-core instruction family of the tile path: "tcgen05"
-    (tcgen05.mma, TMEM accumulators), "mma_sync" (mma.sync m16n8k16, register
-    accumulators) or "auto" (the measured-faster one for 16-row windows)."""
+    """Select the tile-path kernel: "warp" (warp-independent mma.sync workers; the
+    default, "auto"), "mma_sync" / "tcgen05" (the warp-specialised cp.async pipeline
+    with mma.sync m16n8k16 or tcgen05.mma + TMEM accumulators)."""
     if engine not in _ENGINES:
         raise ValueError(f"engine must be one of {sorted(_ENGINES)}, got {engine!r}")
     _lib.call("hcs_set_tile_engine", _ENGINES[engine])

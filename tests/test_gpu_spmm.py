@@ -169,7 +169,7 @@ def test_large_powerlaw_tile_path_checksum(cuda_ok):
         assert float((res.z.data[r].double() - exact).abs().max()) / scale <= BF16_TOL
 
 
-@pytest.mark.parametrize("engine", ["tcgen05", "mma_sync"])
+@pytest.mark.parametrize("engine", ["tcgen05", "mma_sync", "warp"])
 @pytest.mark.parametrize("dim", [8, 32, 40, 64, 128, 200])
 def test_tile_engines_agree(cuda_ok, engine, dim):
     """Both tensor-core engines of the tile path against the exact product."""

@@ -14,6 +14,9 @@ plan = get_plan(ws, asg, "bf16")
 names = ["prod wait idx_full", "prod wait empty", "prod wait_group(publish)", "idx wait idx_empty",
          "ent wait empty", "builder wait full", "mma wait built", "mma wait acce", "epi wait accf", "mma issue block",
          "prod total", "loaders total", "builders total", "mma+epi total", "builder build", "cta total"]
+sw = int(os.environ.get("SWITCHES", "0"))
+_lib.call("hcs_debug_tile_switches", sw)
+print("switches", sw)
 for dim in [int(d) for d in (sys.argv[1:] or ["128", "32"])]:
     x = graphgen.dense_features(a.num_rows, dim, seed=1)
     xop = DeviceOperand(x, dim, dim, _lib.DTYPE_BF16)
