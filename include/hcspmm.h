@@ -93,6 +93,8 @@ int hcs_spmm_scalar(const int64_t* row_ptr, const int32_t* col_idx, const void* 
  * workspace: >= hcs_tile_scratch_floats() floats (engine 2 partial sums; unused by 0/1);
  * one workspace must not be shared by launches that can run concurrently. */
 int hcs_tile_scratch_floats(int64_t* floats);
+/* engine 2 row-slice width in 16-B vectors: 0 auto (8 for dim > 32, else 4), 4 or 8 */
+int hcs_set_tile_slice(int vectors);
 int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
                   const int64_t* ent_ptr, const void* ent, int ent_dtype, int64_t n_rows, int32_t wh, const void* x,
                   int x_dtype, int64_t x_rows, int32_t dim, int64_t ldx, float* z, int64_t ldz, void* workspace,

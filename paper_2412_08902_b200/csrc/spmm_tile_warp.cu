@@ -26,14 +26,44 @@
 
 namespace hcs {
 
-constexpr int kWarpTileWarps = 16;   // warps per CTA
 constexpr int kWarpTileStages = 3;   // cp.async ring depth per warp
-constexpr int kWarpStageBytes = 64 * 64;  // 64 gathered rows x 64 B (one 32-feature slice)
 constexpr int kWarpSlabBytes = 16 * 64 * 2;
-constexpr int kWarpSmemPerWarp = kWarpTileStages * kWarpStageBytes + kWarpSlabBytes;
-constexpr int kWarpTileSmem = kWarpTileWarps * kWarpSmemPerWarp + 128;
 constexpr int kWarpEntRegs = 4;      // packed entries per lane held in registers (128 per chunk)
-constexpr int kSlotFloats = 16 * 32;  // one 16 x 32 fp32 partial
+
+// SWV = 16-byte vectors per gathered row slice: 4 (32 features) or 8 (64 features).
+template <int SWV>
+struct WarpCfg {
+  static constexpr int kFeat = 8 * SWV;                  // features per slice
+  static constexpr int kRowBytes = 16 * SWV;             // bytes per gathered row slice
+  static constexpr int kStageBytes = 64 * kRowBytes;     // 64 rows (one chunk)
+  static constexpr int kWarps = SWV == 4 ? 16 : 8;       // warps per CTA (smem-limited)
+  static constexpr int kPerWarp = kWarpTileStages * kStageBytes + kWarpSlabBytes;
+  static constexpr int kSmem = kWarps * kPerWarp + 128;
+  static constexpr int kIssue = 2 * SWV;                 // cp.async instructions per chunk
+  static constexpr int kSlot = 16 * kFeat;               // floats of one 16 x kFeat partial
+  static_assert(kSmem <= 227 * 1024, "smem");
+  // XOR swizzle of 16-B vector v of row r (conflict-free ldmatrix.trans over 8 consecutive rows)
+  __device__ static __forceinline__ int swz(int r, int v) {
+    return SWV == 4 ? (v ^ ((r >> 1) & 3)) : (v ^ (r & 7));
+  }
+};
+
+// read-once plan data: L2 evict_first so it does not displace the X rows
+__device__ __forceinline__ int32_t ld_plan_s32(const int32_t* p, uint64_t pol) {
+  int32_t r;
+  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ uint32_t ld_plan_u32(const uint32_t* p, uint64_t pol) {
+  uint32_t r;
+  asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ int64_t ld_plan_s64(const int64_t* p, uint64_t pol) {
+  int64_t r;
+  asm volatile("ld.global.nc.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(pol));
+  return r;
+}
 
 // Position in the flattened (unit, chunk) sequence of one warp.
 struct ChunkPos {
@@ -79,12 +109,13 @@ __device__ __forceinline__ void warp_range(int64_t total, int64_t nwarps, int64_
   b = (total * (gw + 1)) / nwarps;
 }
 
+template <int SWV>
 __device__ __forceinline__ void store_slice(float* __restrict__ z, int64_t ldz, int64_t rs, int rows, int dim, int f,
-                                            const float (&acc)[4][4], int lane) {
+                                            const float (&acc)[SWV][4], int lane) {
   const int r0 = lane >> 2, cc = (lane & 3) * 2;
 #pragma unroll
-  for (int nt = 0; nt < 4; ++nt) {
-    const int col = f * 32 + nt * 8 + cc;
+  for (int nt = 0; nt < SWV; ++nt) {
+    const int col = f * (8 * SWV) + nt * 8 + cc;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int r = r0 + 8 * h;
@@ -100,11 +131,15 @@ __device__ __forceinline__ void store_slice(float* __restrict__ z, int64_t ldz, 
   }
 }
 
-__global__ void __launch_bounds__(kWarpTileWarps * 32, 1)
+template <int SWV>
+__global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
     k_tile_warp(const int32_t* __restrict__ tile_list, int64_t T, const int64_t* __restrict__ chunk_ptr,
                 const int32_t* __restrict__ gidx, const int64_t* __restrict__ ent_ptr,
                 const uint32_t* __restrict__ ent, int64_t n_rows, int wh, const __nv_bfloat16* __restrict__ x,
                 int64_t ldx, int dim, int FS, float* __restrict__ z, int64_t ldz, float* __restrict__ scratch) {
+  using C = WarpCfg<SWV>;
+  constexpr int kWarpTileWarps = C::kWarps, kWarpStageBytes = C::kStageBytes, kWarpSmemPerWarp = C::kPerWarp;
+  constexpr int NI = C::kIssue, RPI = 32 / SWV;
   extern __shared__ uint8_t wsmem_raw[];
   uint8_t* wsmem = (uint8_t*)(((uintptr_t)wsmem_raw + 127) & ~(uintptr_t)127);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -119,10 +154,11 @@ __global__ void __launch_bounds__(kWarpTileWarps * 32, 1)
   const uint32_t slab = stage0 + kWarpTileStages * kWarpStageBytes;
   uint8_t* slab_p = wsmem + warp * kWarpSmemPerWarp + kWarpTileStages * kWarpStageBytes;
   const uint64_t keep = policy_evict_last();
+  const uint64_t once = policy_evict_first();
   const char* xb = reinterpret_cast<const char*>(x);
   const int64_t ldxb = ldx * 2;
-  // gather lane mapping: 4 lanes x 16 B per 64-B row slice, 8 rows per instruction
-  const int grow = lane >> 2, gv = lane & 3;
+  // gather lane mapping: SWV lanes x 16 B per row slice, RPI rows per instruction
+  const int grow = lane / SWV, gv = lane % SWV;
   // ldmatrix lane mapping (A: slab rows, B: gathered rows k, 8-feature chunks)
   const int ar = lane & 15, akc = lane >> 4;
   const int bk = (lane & 7) + ((lane >> 3) & 1) * 8, bfc = lane >> 4;
@@ -137,24 +173,24 @@ __global__ void __launch_bounds__(kWarpTileWarps * 32, 1)
   advance(p3, chunk_ptr, T, FS);
   bool in_head = p0.j != 0;  // our first unit (t, f) began in an earlier warp's range
 
-  auto load_gidx = [&](const ChunkPos& p, int (&g)[8]) {
+  auto load_gidx = [&](const ChunkPos& p, int (&g)[NI]) {
     if (p.fi < b) {
       const int32_t* gp = gidx + (p.base + p.j) * 64 + grow;
 #pragma unroll
-      for (int it = 0; it < 8; ++it) g[it] = __ldg(gp + 8 * it);
+      for (int it = 0; it < NI; ++it) g[it] = ld_plan_s32(gp + RPI * it, once);
     }
   };
-  auto issue = [&](const ChunkPos& p, const int (&g)[8], int slot) {
+  auto issue = [&](const ChunkPos& p, const int (&g)[NI], int slot) {
     if (p.fi < b) {
-      const int feat = p.f * 32 + gv * 8;
+      const int feat = p.f * C::kFeat + gv * 8;
       const uint32_t vb = feat < dim ? 16u : 0u;
       const char* src = xb + (int64_t)feat * 2;
       const uint32_t dst = stage0 + slot * kWarpStageBytes;
 #pragma unroll
-      for (int it = 0; it < 8; ++it) {
-        const int row = grow + 8 * it;
+      for (int it = 0; it < NI; ++it) {
+        const int row = grow + RPI * it;
         const int gi = g[it];
-        cp_async16(dst + row * 64 + ((gv ^ ((row >> 1) & 3)) << 4), src + (int64_t)max(gi, 0) * ldxb,
+        cp_async16(dst + row * C::kRowBytes + (C::swz(row, gv) << 4), src + (int64_t)max(gi, 0) * ldxb,
                    gi >= 0 ? vb : 0u, keep);
       }
     }
@@ -163,8 +199,8 @@ __global__ void __launch_bounds__(kWarpTileWarps * 32, 1)
   auto load_ep = [&](const ChunkPos& p, int64_t& e0, int64_t& e1) {
     if (p.fi < b) {
       const int64_t c = p.base + p.j;
-      e0 = __ldg(ent_ptr + c);
-      e1 = __ldg(ent_ptr + c + 1);
+      e0 = ld_plan_s64(ent_ptr + c, once);
+      e1 = ld_plan_s64(ent_ptr + c + 1, once);
     } else {
       e0 = e1 = 0;
     }
@@ -173,17 +209,17 @@ __global__ void __launch_bounds__(kWarpTileWarps * 32, 1)
 #pragma unroll
     for (int q = 0; q < kWarpEntRegs; ++q) {
       const int64_t i = e0 + lane + 32 * q;
-      e[q] = i < e1 ? __ldg(ent + i) : 0u;
+      e[q] = i < e1 ? ld_plan_u32(ent + i, once) : 0u;
     }
   };
 
-  int g_a[8], g_b[8];
+  int g_a[NI], g_b[NI];
   // prologue: gathers of p0, p1 in flight; indices of p2; entries of p0; entry pointers of p1
   load_gidx(p0, g_a);
   load_gidx(p1, g_b);
   issue(p0, g_a, 0);
   issue(p1, g_b, 1);
-  int g2[8];
+  int g2[NI];
   load_gidx(p2, g2);
   int64_t ep0a, ep0b, ep1a, ep1b;
   load_ep(p0, ep0a, ep0b);
@@ -191,9 +227,9 @@ __global__ void __launch_bounds__(kWarpTileWarps * 32, 1)
   uint32_t e0r[kWarpEntRegs], e1r[kWarpEntRegs];
   load_ent(ep0a, ep0b, e0r);
 
-  float acc[4][4];
+  float acc[SWV][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+  for (int i = 0; i < SWV; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
 
   int s0 = 0;  // ring slot of p0
   for (; p0.fi < b;) {
@@ -216,7 +252,7 @@ __global__ void __launch_bounds__(kWarpTileWarps * 32, 1)
       for (int q = 0; q < kWarpEntRegs; ++q)
         if (lane + 32 * q < ne) *reinterpret_cast<uint16_t*>(slab_p + (e0r[q] & 0x7FFu)) = (uint16_t)(e0r[q] >> 16);
       for (int i = 32 * kWarpEntRegs + lane; i < ne; i += 32) {  // rare: > 128 entries in a chunk
-        const uint32_t w = __ldg(ent + ep0a + i);
+        const uint32_t w = ld_plan_u32(ent + ep0a + i, once);
         *reinterpret_cast<uint16_t*>(slab_p + (w & 0x7FFu)) = (uint16_t)(w >> 16);
       }
     }
@@ -228,18 +264,18 @@ __global__ void __launch_bounds__(kWarpTileWarps * 32, 1)
       const uint32_t st = stage0 + s0 * kWarpStageBytes;
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) {
-        uint32_t af[4], b01[4], b23[4];
+        uint32_t af[4];
         const int kc = 2 * ks + akc;
         ldsm_x4(af, slab + ar * 128 + (((kc ^ ar) & 7) << 4));
         const int k = ks * 16 + bk;
-        const uint32_t rowa = st + k * 64;
-        const int sw = (k >> 1) & 3;
-        ldsm_x4_trans(b01, rowa + ((bfc ^ sw) << 4));
-        ldsm_x4_trans(b23, rowa + (((2 + bfc) ^ sw) << 4));
-        hmma_16816(acc[0], af, b01[0], b01[1]);
-        hmma_16816(acc[1], af, b01[2], b01[3]);
-        hmma_16816(acc[2], af, b23[0], b23[1]);
-        hmma_16816(acc[3], af, b23[2], b23[3]);
+        const uint32_t rowa = st + k * C::kRowBytes;
+#pragma unroll
+        for (int pr = 0; pr < SWV / 2; ++pr) {
+          uint32_t bb[4];
+          ldsm_x4_trans(bb, rowa + (C::swz(k, 2 * pr + bfc) << 4));
+          hmma_16816(acc[2 * pr], af, bb[0], bb[1]);
+          hmma_16816(acc[2 * pr + 1], af, bb[2], bb[3]);
+        }
       }
     }
     __syncwarp();
@@ -249,17 +285,17 @@ __global__ void __launch_bounds__(kWarpTileWarps * 32, 1)
       const int64_t rs = (int64_t)__ldg(tile_list + p0.t) * wh;
       const int rows = (int)(n_rows - rs < wh ? n_rows - rs : wh);
       if (!in_head && unit_done) {
-        store_slice(z, ldz, rs, rows, dim, p0.f, acc, lane);
+        store_slice<SWV>(z, ldz, rs, rows, dim, p0.f, acc, lane);
       } else {
-        float* slot = scratch + (gw * 2 + (in_head ? 0 : 1)) * kSlotFloats;
+        float* slot = scratch + (gw * 2 + (in_head ? 0 : 1)) * C::kSlot;
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
+        for (int nt = 0; nt < SWV; ++nt)
 #pragma unroll
           for (int q = 0; q < 4; ++q) slot[(nt * 4 + q) * 32 + lane] = acc[nt][q];
       }
       in_head = false;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+      for (int i = 0; i < SWV; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
     }
     // 7. rotate the pipeline
     p0 = p1;
@@ -278,6 +314,7 @@ __global__ void __launch_bounds__(kWarpTileWarps * 32, 1)
 }
 
 // Sums the partial slots of units cut by warp-range boundaries, in warp order.
+template <int SWV>
 __global__ void k_tile_warp_fixup(const int32_t* __restrict__ tile_list, int64_t T,
                                   const int64_t* __restrict__ chunk_ptr, int64_t n_rows, int wh, int dim, int FS,
                                   float* __restrict__ z, int64_t ldz, const float* __restrict__ scratch,
@@ -293,53 +330,81 @@ __global__ void k_tile_warp_fixup(const int32_t* __restrict__ tile_list, int64_t
   const int64_t ustart = (int64_t)FS * last.base + (int64_t)last.f * last.nj;
   const int64_t uend = ustart + last.nj;
   if (!(uend > b && ustart >= a)) return;  // not the warp that opens a split unit
-  float acc[4][4];
-  const float* s = scratch + (gw * 2 + 1) * kSlotFloats;
+  constexpr int kSlot = WarpCfg<SWV>::kSlot;
+  float acc[SWV][4];
+  const float* s = scratch + (gw * 2 + 1) * kSlot;
 #pragma unroll
-  for (int nt = 0; nt < 4; ++nt)
+  for (int nt = 0; nt < SWV; ++nt)
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[nt][q] = s[(nt * 4 + q) * 32 + lane];
   for (int64_t k = gw + 1; k < nwarps; ++k) {
     int64_t ak, bk;
     warp_range(total, nwarps, k, ak, bk);
     if (ak >= bk) continue;
-    const float* sk = scratch + (k * 2 + 0) * kSlotFloats;
+    const float* sk = scratch + (k * 2 + 0) * kSlot;
 #pragma unroll
-    for (int nt = 0; nt < 4; ++nt)
+    for (int nt = 0; nt < SWV; ++nt)
 #pragma unroll
       for (int q = 0; q < 4; ++q) acc[nt][q] += sk[(nt * 4 + q) * 32 + lane];
     if (uend <= bk) break;
   }
   const int64_t rs = (int64_t)tile_list[last.t] * wh;
   const int rows = (int)(n_rows - rs < wh ? n_rows - rs : wh);
-  store_slice(z, ldz, rs, rows, dim, last.f, acc, lane);
+  store_slice<SWV>(z, ldz, rs, rows, dim, last.f, acc, lane);
+}
+
+static int g_warp_swv = 0;  // 0 auto, 4 or 8 (16-B vectors per row slice)
+
+template <int SWV>
+static int launch_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
+                       const int64_t* ent_ptr, const uint32_t* ent, int64_t n_rows, int wh, const __nv_bfloat16* x,
+                       int64_t ldx, int dim, float* z, int64_t ldz, float* scratch, int64_t scratch_floats,
+                       cudaStream_t st) {
+  using C = WarpCfg<SWV>;
+  const int FS = (dim + C::kFeat - 1) / C::kFeat;
+  const int grid = num_sms();
+  const int64_t nwarps = (int64_t)grid * C::kWarps;
+  HCS_REQUIRE(scratch != nullptr && scratch_floats >= nwarps * 2 * C::kSlot, HCS_EINVAL,
+              "tile scratch too small (%lld floats, need %lld)", (long long)scratch_floats,
+              (long long)(nwarps * 2 * C::kSlot));
+  HCS_CUDA(cudaFuncSetAttribute(k_tile_warp<SWV>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+  k_tile_warp<SWV><<<grid, C::kWarps * 32, C::kSmem, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows,
+                                                            wh, x, ldx, dim, FS, z, ldz, scratch);
+  HCS_LAUNCH_CHECK("k_tile_warp");
+  const int fix_threads = 256;
+  const int fix_blocks = (int)((nwarps * 32 + fix_threads - 1) / fix_threads);
+  k_tile_warp_fixup<SWV><<<fix_blocks, fix_threads, 0, st>>>(tile_list, n_tile, chunk_ptr, n_rows, wh, dim, FS, z,
+                                                              ldz, scratch, nwarps);
+  HCS_LAUNCH_CHECK("k_tile_warp_fixup");
+  return HCS_OK;
 }
 
 int spmm_tile_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
                    const int64_t* ent_ptr, const uint32_t* ent, int64_t n_rows, int wh, const __nv_bfloat16* x,
                    int64_t ldx, int dim, float* z, int64_t ldz, float* scratch, int64_t scratch_floats,
                    cudaStream_t st) {
-  const int FS = (dim + 31) / 32;
-  const int grid = num_sms();
-  const int64_t nwarps = (int64_t)grid * kWarpTileWarps;
-  HCS_REQUIRE(scratch != nullptr && scratch_floats >= nwarps * 2 * kSlotFloats, HCS_EINVAL,
-              "tile scratch too small (%lld floats, need %lld)", (long long)scratch_floats,
-              (long long)(nwarps * 2 * kSlotFloats));
-  HCS_CUDA(cudaFuncSetAttribute(k_tile_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, kWarpTileSmem));
-  k_tile_warp<<<grid, kWarpTileWarps * 32, kWarpTileSmem, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent,
-                                                                n_rows, wh, x, ldx, dim, FS, z, ldz, scratch);
-  HCS_LAUNCH_CHECK("k_tile_warp");
-  const int fix_threads = 256;
-  const int fix_blocks = (int)((nwarps * 32 + fix_threads - 1) / fix_threads);
-  k_tile_warp_fixup<<<fix_blocks, fix_threads, 0, st>>>(tile_list, n_tile, chunk_ptr, n_rows, wh, dim, FS, z, ldz,
-                                                         scratch, nwarps);
-  HCS_LAUNCH_CHECK("k_tile_warp_fixup");
-  return HCS_OK;
+  // 64-feature slices halve the per-feature slab work once a window has >= 2 slices of 32
+  const int swv = g_warp_swv ? g_warp_swv : (dim > 32 ? 8 : 4);
+  if (swv == 8)
+    return launch_warp<8>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim, z, ldz, scratch,
+                          scratch_floats, st);
+  return launch_warp<4>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim, z, ldz, scratch,
+                        scratch_floats, st);
 }
 
-int64_t tile_warp_scratch_floats() { return (int64_t)num_sms() * kWarpTileWarps * 2 * kSlotFloats; }
+int64_t tile_warp_scratch_floats() {
+  return std::max<int64_t>((int64_t)num_sms() * WarpCfg<4>::kWarps * 2 * WarpCfg<4>::kSlot,
+                           (int64_t)num_sms() * WarpCfg<8>::kWarps * 2 * WarpCfg<8>::kSlot);
+}
 
 }  // namespace hcs
+
+// Row-slice width of the warp-independent tile kernel: 0 auto, 4 (32 features) or 8 (64).
+extern "C" int hcs_set_tile_slice(int vectors) {
+  HCS_REQUIRE(vectors == 0 || vectors == 4 || vectors == 8, HCS_EINVAL, "slice must be 0, 4 or 8 (got %d)", vectors);
+  hcs::g_warp_swv = vectors;
+  return HCS_OK;
+}
 
 extern "C" int hcs_tile_scratch_floats(int64_t* floats) {
   HCS_REQUIRE(floats != nullptr, HCS_EINVAL, "floats is NULL");

@@ -184,3 +184,22 @@ def test_tile_engines_agree(cuda_ok, engine, dim):
     finally:
         set_tile_engine("auto")
     assert orc.max_rel_err(res.z.data, orc.spmm_exact(a, x)) <= BF16_TOL
+
+
+@pytest.mark.parametrize("vectors", [4, 8])
+@pytest.mark.parametrize("dim", [8, 32, 41, 64, 96, 128, 200])
+def test_warp_kernel_slice_widths(cuda_ok, vectors, dim):
+    """Engine 2 with 32- and 64-feature row slices; deterministic across repeats."""
+    from paper_2412_08902_b200 import _lib
+
+    a = plaw8k_csr()
+    x = orc.random_dense(a.num_cols, dim, seed=dim + 1)
+    ws = hc.partition(to_hc(a))
+    try:
+        _lib.call("hcs_set_tile_slice", vectors)
+        r1 = hc.spmm_tile(ws, hc.DenseMatrix(x))
+        r2 = hc.spmm_tile(ws, hc.DenseMatrix(x))
+    finally:
+        _lib.call("hcs_set_tile_slice", 0)
+    assert orc.max_rel_err(r1.z.data, orc.spmm_exact(a, x)) <= BF16_TOL
+    assert np.array_equal(r1.z.data, r2.z.data)

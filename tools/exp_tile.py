@@ -25,7 +25,10 @@ for dim in dims:
     for eng in engines:
         set_tile_engine(eng)
         for np_ in nps:
-            _lib.call("hcs_set_tile_producers", np_)
+            if eng == "warp":
+                _lib.call("hcs_set_tile_slice", np_ if np_ in (4, 8) else 0)
+            else:
+                _lib.call("hcs_set_tile_producers", np_)
             for _ in range(3): plan.run(xop, z, dim)
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize(); s.record()
