@@ -40,6 +40,25 @@ __device__ __forceinline__ void hmma_16816(float (&c)[4], const uint32_t (&a)[4]
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
+// mma.sync m16n8k8 tf32 -> fp32 (operands already RNA-rounded to tf32)
+__device__ __forceinline__ void mma_tf32_1688(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+// byte offset of fp32 element (row r, column c) in a 16 x 64 fp32 slab (256-B rows,
+// 16-B chunks XOR-swizzled by the row's low 3 bits: conflict-free ldmatrix.x4 of tf32 A tiles)
+__host__ __device__ __forceinline__ uint32_t tf32_slab_off(uint32_t r, uint32_t c) {
+  const uint32_t ch = c >> 2;
+  return r * 256u + (((ch & 8u) | ((ch ^ r) & 7u)) << 4) + (c & 3u) * 4u;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);  // RNE
   return *reinterpret_cast<const uint32_t*>(&h);

@@ -723,6 +723,9 @@ int spmm_tile_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chun
                    const int64_t* ent_ptr, const uint32_t* ent, int64_t n_rows, int wh, const __nv_bfloat16* x,
                    int64_t ldx, int dim, float* z, int64_t ldz, float* scratch, int64_t scratch_floats,
                    cudaStream_t st);
+int spmm_tile_warp_tf32(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
+                        const int64_t* ent_ptr, const uint2* ent, int64_t n_rows, int wh, const float* x, int64_t ldx,
+                        int dim, float* z, int64_t ldz, float* scratch, int64_t scratch_floats, cudaStream_t st);
 }  // namespace hcs
 
 extern "C" int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
@@ -731,10 +734,19 @@ extern "C" int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int
                              int64_t ldz, void* workspace, size_t ws_bytes, void* stream) {
   HCS_REQUIRE(wh > 0 && wh <= 16, HCS_EINVAL, "tile path supports window heights 1..16 (got %d)", wh);
   HCS_REQUIRE(dim > 0, HCS_EINVAL, "dim must be positive");
-  HCS_REQUIRE(x_dtype == HCS_DTYPE_BF16 && ent_dtype == HCS_DTYPE_BF16, HCS_EINVAL,
-              "tile path: only bf16 operands are implemented in this build");
-  HCS_REQUIRE(ldx % 8 == 0 && ldx >= ((dim + 7) / 8) * 8, HCS_EINVAL, "ldx must be a multiple of 8 covering dim");
   HCS_REQUIRE(((uintptr_t)x & 15) == 0, HCS_EINVAL, "x must be 16-byte aligned");
+  HCS_REQUIRE(x_dtype == ent_dtype, HCS_EINVAL, "x and plan dtypes differ (%d vs %d)", x_dtype, ent_dtype);
+  if (x_dtype == HCS_DTYPE_F32) {
+    // tf32 tensor-core path (warp-independent kernel only)
+    HCS_REQUIRE(ldx % 4 == 0 && ldx >= ((dim + 3) / 4) * 4, HCS_EINVAL, "ldx must be a multiple of 4 covering dim");
+    HCS_REQUIRE(((uintptr_t)z & 7) == 0 && ldz % 2 == 0, HCS_EINVAL, "z must be 8-byte aligned with even ldz");
+    if (n_tile == 0) return HCS_OK;
+    return spmm_tile_warp_tf32(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, (const uint2*)ent, n_rows, wh,
+                               (const float*)x, ldx, dim, z, ldz, (float*)workspace,
+                               (int64_t)(ws_bytes / sizeof(float)), as_stream(stream));
+  }
+  HCS_REQUIRE(x_dtype == HCS_DTYPE_BF16, HCS_EINVAL, "tile path: x dtype must be bf16 or f32 (tf32)");
+  HCS_REQUIRE(ldx % 8 == 0 && ldx >= ((dim + 7) / 8) * 8, HCS_EINVAL, "ldx must be a multiple of 8 covering dim");
   if (n_tile == 0) return HCS_OK;
   cudaStream_t st = as_stream(stream);
   const int grid = (int)std::min<int64_t>(n_tile, num_sms());

@@ -353,6 +353,202 @@ __global__ void k_tile_warp_fixup(const int32_t* __restrict__ tile_list, int64_t
   store_slice<SWV>(z, ldz, rs, rows, dim, last.f, acc, lane);
 }
 
+// ---------------------------------------------------------------- tf32 variant
+// Same schedule and fix-up; fp32 X rows (32-feature slices of 128 B), 16 x 64 fp32 slab,
+// mma.sync m16n8k8 tf32 (X and values RNA-rounded to tf32 by the caller / plan).
+// B fragments are read with conflict-free 32-bit loads (16-B chunk XOR 2*(row&3)).
+constexpr int kTfWarps = 8;
+constexpr int kTfRow = 128;
+constexpr int kTfStage = 64 * kTfRow;
+constexpr int kTfSlab = 16 * 64 * 4;
+constexpr int kTfPerWarp = kWarpTileStages * kTfStage + kTfSlab;
+constexpr int kTfSmem = kTfWarps * kTfPerWarp + 128;
+static_assert(kTfSmem <= 227 * 1024, "smem");
+__device__ __forceinline__ int swz_tf(int k, int v) { return v ^ ((2 * k) & 6); }
+
+__global__ void __launch_bounds__(kTfWarps * 32, 1)
+    k_tile_warp_tf32(const int32_t* __restrict__ tile_list, int64_t T, const int64_t* __restrict__ chunk_ptr,
+                     const int32_t* __restrict__ gidx, const int64_t* __restrict__ ent_ptr,
+                     const uint2* __restrict__ ent, int64_t n_rows, int wh, const float* __restrict__ x, int64_t ldx,
+                     int dim, int FS, float* __restrict__ z, int64_t ldz, float* __restrict__ scratch) {
+  constexpr int NI = 16, RPI = 4;
+  extern __shared__ uint8_t tsmem_raw[];
+  uint8_t* tsmem = (uint8_t*)(((uintptr_t)tsmem_raw + 127) & ~(uintptr_t)127);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nwarps = (int64_t)gridDim.x * kTfWarps;
+  const int64_t gw = (int64_t)blockIdx.x * kTfWarps + warp;
+  const int64_t total = (int64_t)FS * chunk_ptr[T];
+  int64_t a, b;
+  warp_range(total, nwarps, gw, a, b);
+  if (a >= b) return;
+  const uint32_t stage0 = smem_u32(tsmem + warp * kTfPerWarp);
+  const uint32_t slab = stage0 + kWarpTileStages * kTfStage;
+  uint8_t* slab_p = tsmem + warp * kTfPerWarp + kWarpTileStages * kTfStage;
+  const uint64_t keep = policy_evict_last();
+  const uint64_t once = policy_evict_first();
+  const char* xb = reinterpret_cast<const char*>(x);
+  const int64_t ldxb = ldx * 4;
+  const int grow = lane >> 3, gv = lane & 7;
+  const int g8 = lane >> 2, t4 = lane & 3;
+  const int arow = (lane & 7) + ((lane >> 3) & 1) * 8, ach = lane >> 4;
+
+  ChunkPos p0 = locate(chunk_ptr, T, FS, a);
+  ChunkPos p1 = p0, p2, p3;
+  advance(p1, chunk_ptr, T, FS);
+  p2 = p1;
+  advance(p2, chunk_ptr, T, FS);
+  p3 = p2;
+  advance(p3, chunk_ptr, T, FS);
+  bool in_head = p0.j != 0;
+
+  auto load_gidx = [&](const ChunkPos& p, int (&g)[NI]) {
+    if (p.fi < b) {
+      const int32_t* gp = gidx + (p.base + p.j) * 64 + grow;
+#pragma unroll
+      for (int it = 0; it < NI; ++it) g[it] = ld_plan_s32(gp + RPI * it, once);
+    }
+  };
+  auto issue = [&](const ChunkPos& p, const int (&g)[NI], int slot) {
+    if (p.fi < b) {
+      const int feat = p.f * 32 + gv * 4;
+      const uint32_t vb = feat < dim ? 16u : 0u;
+      const char* src = xb + (int64_t)feat * 4;
+      const uint32_t dst = stage0 + slot * kTfStage;
+#pragma unroll
+      for (int it = 0; it < NI; ++it) {
+        const int row = grow + RPI * it;
+        const int gi = g[it];
+        cp_async16(dst + row * kTfRow + (swz_tf(row, gv) << 4), src + (int64_t)max(gi, 0) * ldxb, gi >= 0 ? vb : 0u,
+                   keep);
+      }
+    }
+    cp_async_commit();
+  };
+  auto load_ep = [&](const ChunkPos& p, int64_t& e0, int64_t& e1) {
+    if (p.fi < b) {
+      const int64_t c = p.base + p.j;
+      e0 = ld_plan_s64(ent_ptr + c, once);
+      e1 = ld_plan_s64(ent_ptr + c + 1, once);
+    } else {
+      e0 = e1 = 0;
+    }
+  };
+  auto load_ent = [&](int64_t e0, int64_t e1, uint2 (&e)[kWarpEntRegs]) {
+#pragma unroll
+    for (int q = 0; q < kWarpEntRegs; ++q) {
+      const int64_t i = e0 + lane + 32 * q;
+      e[q] = i < e1 ? __ldg(ent + i) : make_uint2(0u, 0u);
+    }
+  };
+
+  int g_a[NI], g_b[NI], g2[NI];
+  load_gidx(p0, g_a);
+  load_gidx(p1, g_b);
+  issue(p0, g_a, 0);
+  issue(p1, g_b, 1);
+  load_gidx(p2, g2);
+  int64_t ep0a, ep0b, ep1a, ep1b;
+  load_ep(p0, ep0a, ep0b);
+  load_ep(p1, ep1a, ep1b);
+  uint2 e0r[kWarpEntRegs], e1r[kWarpEntRegs];
+  load_ent(ep0a, ep0b, e0r);
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+  int s0 = 0;
+  for (; p0.fi < b;) {
+    const int s2 = s0 >= 1 ? s0 - 1 : s0 + 2;
+    issue(p2, g2, s2);
+    load_gidx(p3, g2);
+    load_ent(ep1a, ep1b, e1r);
+    int64_t ep2a, ep2b;
+    load_ep(p2, ep2a, ep2b);
+    {
+      const int4 zero4 = make_int4(0, 0, 0, 0);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) reinterpret_cast<int4*>(slab_p)[lane + 32 * q] = zero4;
+      __syncwarp();
+      const int ne = (int)(ep0b - ep0a);
+#pragma unroll
+      for (int q = 0; q < kWarpEntRegs; ++q)
+        if (lane + 32 * q < ne) *reinterpret_cast<uint32_t*>(slab_p + e0r[q].x) = e0r[q].y;
+      for (int i = 32 * kWarpEntRegs + lane; i < ne; i += 32) {
+        const uint2 w = __ldg(ent + ep0a + i);
+        *reinterpret_cast<uint32_t*>(slab_p + w.x) = w.y;
+      }
+    }
+    cp_async_wait<2>();
+    __syncwarp();
+    {
+      const uint32_t st = stage0 + s0 * kTfStage;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        uint32_t af[4];
+        const int ch = 2 * ks + ach;
+        ldsm_x4(af, slab + arow * 256 + ((((ch & 8) | ((ch ^ arow) & 7))) << 4));
+        const int k0 = ks * 8 + t4, k1 = k0 + 4;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          const int n = nt * 8 + g8;
+          const uint32_t b0 = lds32(st + k0 * kTfRow + (swz_tf(k0, n >> 2) << 4) + (n & 3) * 4);
+          const uint32_t b1 = lds32(st + k1 * kTfRow + (swz_tf(k1, n >> 2) << 4) + (n & 3) * 4);
+          mma_tf32_1688(acc[nt], af, b0, b1);
+        }
+      }
+    }
+    __syncwarp();
+    const bool unit_done = p0.j + 1 == p0.nj;
+    if (unit_done || p0.fi + 1 == b) {
+      const int64_t rs = (int64_t)__ldg(tile_list + p0.t) * wh;
+      const int rows = (int)(n_rows - rs < wh ? n_rows - rs : wh);
+      if (!in_head && unit_done) {
+        store_slice<4>(z, ldz, rs, rows, dim, p0.f, acc, lane);
+      } else {
+        float* slot = scratch + (gw * 2 + (in_head ? 0 : 1)) * WarpCfg<4>::kSlot;
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) slot[(nt * 4 + q) * 32 + lane] = acc[nt][q];
+      }
+      in_head = false;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+    }
+    p0 = p1;
+    p1 = p2;
+    p2 = p3;
+    advance(p3, chunk_ptr, T, FS);
+#pragma unroll
+    for (int q = 0; q < kWarpEntRegs; ++q) e0r[q] = e1r[q];
+    ep0a = ep1a;
+    ep0b = ep1b;
+    ep1a = ep2a;
+    ep1b = ep2b;
+    s0 = s0 == kWarpTileStages - 1 ? 0 : s0 + 1;
+  }
+  cp_async_wait<0>();
+}
+
+int spmm_tile_warp_tf32(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
+                        const int64_t* ent_ptr, const uint2* ent, int64_t n_rows, int wh, const float* x, int64_t ldx,
+                        int dim, float* z, int64_t ldz, float* scratch, int64_t scratch_floats, cudaStream_t st) {
+  const int FS = (dim + 31) / 32;
+  const int grid = num_sms();
+  const int64_t nwarps = (int64_t)grid * kTfWarps;
+  HCS_REQUIRE(scratch != nullptr && scratch_floats >= nwarps * 2 * WarpCfg<4>::kSlot, HCS_EINVAL,
+              "tile scratch too small");
+  HCS_CUDA(cudaFuncSetAttribute(k_tile_warp_tf32, cudaFuncAttributeMaxDynamicSharedMemorySize, kTfSmem));
+  k_tile_warp_tf32<<<grid, kTfWarps * 32, kTfSmem, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh,
+                                                         x, ldx, dim, FS, z, ldz, scratch);
+  HCS_LAUNCH_CHECK("k_tile_warp_tf32");
+  const int fix_threads = 256;
+  const int fix_blocks = (int)((nwarps * 32 + fix_threads - 1) / fix_threads);
+  k_tile_warp_fixup<4><<<fix_blocks, fix_threads, 0, st>>>(tile_list, n_tile, chunk_ptr, n_rows, wh, dim, FS, z, ldz,
+                                                            scratch, nwarps);
+  HCS_LAUNCH_CHECK("k_tile_warp_fixup");
+  return HCS_OK;
+}
+
 static int g_warp_swv = 0;  // 0 auto, 4 or 8 (16-B vectors per row slice)
 
 template <int SWV>

@@ -11,6 +11,7 @@
 #include <cub/cub.cuh>
 
 #include "common.cuh"
+#include "mma_helpers.cuh"
 
 namespace hcs {
 
@@ -75,7 +76,10 @@ __global__ void k_tile_emit(const uint64_t* __restrict__ keys, const uint32_t* _
       uint32_t b = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(__uint_as_float(kv[i])));
       reinterpret_cast<uint32_t*>(ent)[i] = (b << 16) | pos;
     } else {
-      reinterpret_cast<uint2*>(ent)[i] = make_uint2(pos, kv[i]);
+      // tf32 tile path: byte offset in the 16 x 64 fp32 slab, value RNA-rounded to tf32
+      uint32_t t;
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(__uint_as_float(kv[i])));
+      reinterpret_cast<uint2*>(ent)[i] = make_uint2(tf32_slab_off(rc >> 6, rc & 63u), t);
     }
     if (i == 0 || (keys[i - 1] >> 10) != (k >> 10)) ent_ptr[k >> 10] = i;
     if (i == n - 1) ent_ptr[nchunks] = n;

@@ -246,8 +246,6 @@ class HybridPlan:
         if tile_events is not None:
             tile_events[0].record()
         if self.n_tile:
-            if self.precision != "bf16":
-                raise NotImplementedError("tf32 tile kernel not built in this revision; use precision='bf16'")
             scratch = self.scratch()
             _lib.call("hcs_spmm_tile", self.tile_list.data_ptr(), self.n_tile, self.chunk_ptr.data_ptr(),
                       self.gidx.data_ptr(), self.ent_ptr.data_ptr(), self.ent.data_ptr(), self.ent_dtype,

@@ -38,13 +38,13 @@ def fused_aggregate_update(windows, assignment, x, m: torch.Tensor, precision: s
     if int(m.shape[0]) != dim:
         raise ValueError(f"X has {dim} features, weight expects {int(m.shape[0])}")
     n = ws.num_rows
-    if dim > FUSED_MAX_DIM or d_out > FUSED_MAX_DIM:
+    if dim > FUSED_MAX_DIM or d_out > FUSED_MAX_DIM or (plan.n_tile and precision != "bf16"):
+        # outside the fused kernels' on-chip budget, or tf32 tile windows (the fused tile
+        # epilogue is bf16-only): SpMM kernels, then a cuBLAS GEMM on the device
         z, ldz = _alloc_z(n, dim, dev)
         plan.run(xop, z, ldz)
         zz = z[:, :dim]
         return zz @ m, (zz if want_z else None)
-    if plan.n_tile and precision != "bf16":
-        raise NotImplementedError("tf32 tile kernel not built in this revision; use precision='bf16'")
     z, ldz = _alloc_z(n, dim, dev) if want_z else (None, 0)
     out = torch.empty((n, d_out), dtype=torch.float32, device=dev)
     csr = ws.csr

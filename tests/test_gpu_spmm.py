@@ -203,3 +203,34 @@ def test_warp_kernel_slice_widths(cuda_ok, vectors, dim):
         _lib.call("hcs_set_tile_slice", 0)
     assert orc.max_rel_err(r1.z.data, orc.spmm_exact(a, x)) <= BF16_TOL
     assert np.array_equal(r1.z.data, r2.z.data)
+
+
+TF32_TOL = 1e-3
+
+
+@pytest.mark.parametrize("name", ["windows_cora", "windows_corpus_block125", "windows_corpus_clique64", "windows_rand6",
+                                  "windows_rand9", "windows_corpus_star256"])
+def test_tf32_matches_reference(cuda_ok, name):
+    """precision='tf32' (RNA-rounded tf32 tensor-core inputs, fp32 accumulate): <= 1e-3 vs the
+    reference's f32 / exact results (BASELINE north_star)."""
+    g = load_golden(name)
+    csr = golden_csr(g)
+    x = orc.random_dense(csr.num_cols, int(g["dim"]), int(g["xseed"]))
+    ws = hc.partition(to_hc(csr))
+    asg = hc.classify_windows(hc.default_model(), ws)
+    res = hc.spmm_hybrid(ws, asg, hc.DenseMatrix(x), precision="tf32")
+    assert orc.max_rel_err(res.z.data, g["z_f64"]) <= TF32_TOL
+    assert orc.max_rel_err(res.z.data, g["z_f32"]) <= TF32_TOL
+    t = hc.spmm_tile(ws, hc.DenseMatrix(x), precision="tf32")
+    assert orc.max_rel_err(t.z.data, g["z_f64"]) <= TF32_TOL
+
+
+@pytest.mark.parametrize("dim", [1, 5, 32, 41, 64, 128, 200])
+def test_tf32_tile_dims_plaw(cuda_ok, dim):
+    a = plaw8k_csr()
+    x = orc.random_dense(a.num_cols, dim, seed=dim + 3)
+    ws = hc.partition(to_hc(a))
+    r1 = hc.spmm_tile(ws, hc.DenseMatrix(x), precision="tf32")
+    r2 = hc.spmm_tile(ws, hc.DenseMatrix(x), precision="tf32")
+    assert orc.max_rel_err(r1.z.data, orc.spmm_exact(a, x)) <= TF32_TOL
+    assert np.array_equal(r1.z.data, r2.z.data)
