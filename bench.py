@@ -313,7 +313,7 @@ def run_ours(args):
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "k_spmm_tile_bf16 (mma.sync engine)" if plan.n_tile else "k_spmm_scalar",
+                     "kernel": "k_tile_warp (+ k_tile_warp_fixup)" if plan.n_tile else "k_spmm_scalar",
                      "kernel_ms": tile_ms, "algorithmic_bytes": tile_bytes,
                      "l2_gather_GBps": gather_bytes / (tile_ms * 1e-3) / 1e9 if tile_ms > 0 else None},
         "gpu_launches": plan.launches_per_run(dim) * args.steps,

@@ -106,11 +106,14 @@ int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk
  * epilogue:  out[rows] = (A_w X) M,  and z[rows] = A_w X when z != NULL
  * (forward z_cache).  M is an fp32 [dim x d_out] row-major device matrix: W for the
  * forward, W^T for the backward grad_X = (A^T G) W^T.  dim, d_out <= 128.
- * hcs_gcn_tile takes the tile plan of K2 (bf16); hcs_gcn_scalar a window list. */
+ * hcs_gcn_tile takes the tile plan of K2 (bf16) and the K4 workspace
+ * (hcs_tile_scratch_floats); d_out <= 64 runs on the warp-independent kernel (window
+ * partials cut by warp ranges are summed in warp order), larger d_out on the pipelined
+ * kernel.  hcs_gcn_scalar takes a window list. */
 int hcs_gcn_tile(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
                  const int64_t* ent_ptr, const void* ent, int ent_dtype, int64_t n_rows, int32_t wh, const void* x,
                  int x_dtype, int64_t x_rows, int32_t dim, int64_t ldx, float* z, int64_t ldz, const float* m,
-                 int32_t d_out, float* out, int64_t ldo, void* stream);
+                 int32_t d_out, float* out, int64_t ldo, void* workspace, size_t ws_bytes, void* stream);
 int hcs_gcn_scalar(const int64_t* row_ptr, const int32_t* col_idx, const void* values, int values_dtype,
                    int64_t n_rows, int32_t wh, const int32_t* win_list, int64_t n_list, const void* x, int x_dtype,
                    int64_t x_rows, int32_t dim, int64_t ldx, float* z, int64_t ldz, const float* m, int32_t d_out,

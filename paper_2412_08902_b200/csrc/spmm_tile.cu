@@ -726,6 +726,10 @@ int spmm_tile_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chun
 int spmm_tile_warp_tf32(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
                         const int64_t* ent_ptr, const uint2* ent, int64_t n_rows, int wh, const float* x, int64_t ldx,
                         int dim, float* z, int64_t ldz, float* scratch, int64_t scratch_floats, cudaStream_t st);
+int gcn_tile_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
+                  const int64_t* ent_ptr, const uint32_t* ent, int64_t n_rows, int wh, const __nv_bfloat16* x,
+                  int64_t ldx, int dim, float* z, int64_t ldz, const float* m, int d_out, float* out, int64_t ldo,
+                  float* scratch, int64_t scratch_floats, cudaStream_t st);
 }  // namespace hcs
 
 extern "C" int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
@@ -793,7 +797,8 @@ extern "C" int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int
 extern "C" int hcs_gcn_tile(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
                             const int64_t* ent_ptr, const void* ent, int ent_dtype, int64_t n_rows, int32_t wh,
                             const void* x, int x_dtype, int64_t x_rows, int32_t dim, int64_t ldx, float* z,
-                            int64_t ldz, const float* m, int32_t d_out, float* out, int64_t ldo, void* stream) {
+                            int64_t ldz, const float* m, int32_t d_out, float* out, int64_t ldo, void* workspace,
+                            size_t ws_bytes, void* stream) {
   HCS_REQUIRE(wh > 0 && wh <= 16, HCS_EINVAL, "tile path supports window heights 1..16 (got %d)", wh);
   HCS_REQUIRE(dim > 0 && dim <= kMaxOut, HCS_EINVAL, "fused GCN tile path needs 1 <= d_in <= %d (got %d)", kMaxOut,
               dim);
@@ -808,6 +813,12 @@ extern "C" int hcs_gcn_tile(const int32_t* tile_list, int64_t n_tile, const int6
   cudaStream_t st = as_stream(stream);
   const int grid = (int)std::min<int64_t>(n_tile, num_sms());
   const uint32_t* e = (const uint32_t*)ent;
+  if (d_out <= 64 && (g_tile_engine < 0 || g_tile_engine == 2)) {
+    HCS_REQUIRE(z == nullptr || (((uintptr_t)z & 7) == 0 && ldz % 2 == 0), HCS_EINVAL,
+                "z must be 8-byte aligned with even ldz");
+    return gcn_tile_warp(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, e, n_rows, wh, (const __nv_bfloat16*)x, ldx, dim,
+                         z, ldz, m, d_out, out, ldo, (float*)workspace, (int64_t)(ws_bytes / sizeof(float)), st);
+  }
   const int vec = (dim + 7) / 8;
   const __nv_bfloat16* xs = reinterpret_cast<const __nv_bfloat16*>(x);
   float* zs = z;

@@ -41,7 +41,9 @@ struct WarpCfg {
   static constexpr int kSmem = kWarps * kPerWarp + 128;
   static constexpr int kIssue = 2 * SWV;                 // cp.async instructions per chunk
   static constexpr int kSlot = 16 * kFeat;               // floats of one 16 x kFeat partial
+  static constexpr int kOffW = kWarps * kPerWarp;        // fused GCN: M^T (bf16) after the warp regions
   static_assert(kSmem <= 227 * 1024, "smem");
+  static_assert(SWV != 8 || kSmem + 64 * (128 + 8) * 2 <= 227 * 1024, "fused smem");
   // XOR swizzle of 16-B vector v of row r (conflict-free ldmatrix.trans over 8 consecutive rows)
   __device__ static __forceinline__ int swz(int r, int v) {
     return SWV == 4 ? (v ^ ((r >> 1) & 3)) : (v ^ (r & 7));
@@ -131,12 +133,23 @@ __device__ __forceinline__ void store_slice(float* __restrict__ z, int64_t ldz, 
   }
 }
 
-template <int SWV>
+// Fused GCN epilogue (K6/K7) of the warp kernel: after each (window, slice) unit the
+// warp multiplies its 16 x 64 aggregated slice (bf16 A fragments taken straight from the
+// accumulators) by the matching 64 x d_out block of M (bf16 M^T resident in shared
+// memory) into an out accumulator; a window's out rows are written when its last slice
+// is done, or summed in warp order by k_tile_warp_fixup_out when a warp boundary cuts it.
+constexpr int kFusedOutMax = 64;        // d_out of the warp kernel's fused epilogue
+constexpr int kFusedLdw = 128 + 8;      // bf16 per M^T row (d_in <= 128)
+constexpr int kOutSlot = 16 * kFusedOutMax;
+
+template <int SWV, bool FUSED>
 __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
     k_tile_warp(const int32_t* __restrict__ tile_list, int64_t T, const int64_t* __restrict__ chunk_ptr,
                 const int32_t* __restrict__ gidx, const int64_t* __restrict__ ent_ptr,
                 const uint32_t* __restrict__ ent, int64_t n_rows, int wh, const __nv_bfloat16* __restrict__ x,
-                int64_t ldx, int dim, int FS, float* __restrict__ z, int64_t ldz, float* __restrict__ scratch) {
+                int64_t ldx, int dim, int FS, float* __restrict__ z, int64_t ldz, float* __restrict__ scratch,
+                const float* __restrict__ mw, int d_out, float* __restrict__ out, int64_t ldo,
+                float* __restrict__ oscratch) {
   using C = WarpCfg<SWV>;
   constexpr int kWarpTileWarps = C::kWarps, kWarpStageBytes = C::kStageBytes, kWarpSmemPerWarp = C::kPerWarp;
   constexpr int NI = C::kIssue, RPI = 32 / SWV;
@@ -148,6 +161,14 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
   const int64_t total = (int64_t)FS * chunk_ptr[T];
   int64_t a, b;
   warp_range(total, nwarps, gw, a, b);
+  if (FUSED) {
+    __nv_bfloat16* wt = reinterpret_cast<__nv_bfloat16*>(wsmem + C::kOffW);
+    for (int i = threadIdx.x; i < kFusedOutMax * kFusedLdw; i += blockDim.x) {
+      const int n = i / kFusedLdw, k = i - n * kFusedLdw;
+      wt[i] = __float2bfloat16_rn((n < d_out && k < dim) ? mw[(int64_t)k * d_out + n] : 0.f);
+    }
+    __syncthreads();
+  }
   if (a >= b) return;
 
   const uint32_t stage0 = smem_u32(wsmem + warp * kWarpSmemPerWarp);
@@ -230,6 +251,9 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
   float acc[SWV][4];
 #pragma unroll
   for (int i = 0; i < SWV; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+  float oacc[FUSED ? kFusedOutMax / 8 : 1][4];
+#pragma unroll
+  for (int i = 0; i < (FUSED ? kFusedOutMax / 8 : 1); ++i) oacc[i][0] = oacc[i][1] = oacc[i][2] = oacc[i][3] = 0.f;
 
   int s0 = 0;  // ring slot of p0
   for (; p0.fi < b;) {
@@ -284,16 +308,61 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
     if (unit_done || p0.fi + 1 == b) {
       const int64_t rs = (int64_t)__ldg(tile_list + p0.t) * wh;
       const int rows = (int)(n_rows - rs < wh ? n_rows - rs : wh);
-      if (!in_head && unit_done) {
-        store_slice<SWV>(z, ldz, rs, rows, dim, p0.f, acc, lane);
-      } else {
-        float* slot = scratch + (gw * 2 + (in_head ? 0 : 1)) * C::kSlot;
+      if (z != nullptr) {
+        if (!in_head && unit_done) {
+          store_slice<SWV>(z, ldz, rs, rows, dim, p0.f, acc, lane);
+        } else {
+          float* slot = scratch + (gw * 2 + (in_head ? 0 : 1)) * C::kSlot;
 #pragma unroll
-        for (int nt = 0; nt < SWV; ++nt)
+          for (int nt = 0; nt < SWV; ++nt)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) slot[(nt * 4 + q) * 32 + lane] = acc[nt][q];
+            for (int q = 0; q < 4; ++q) slot[(nt * 4 + q) * 32 + lane] = acc[nt][q];
+        }
       }
       in_head = false;
+      if (FUSED) {
+        // oacc += Z_slice (16 x 8*SWV, bf16 RNE) . M[slice rows, :]
+        const uint32_t* wt = reinterpret_cast<const uint32_t*>(wsmem + C::kOffW);
+        const int g8 = lane >> 2, t4 = lane & 3;
+#pragma unroll
+        for (int j = 0; j < SWV / 2; ++j) {
+          uint32_t af[4];
+          af[0] = pack_bf16(acc[2 * j][0], acc[2 * j][1]);
+          af[1] = pack_bf16(acc[2 * j][2], acc[2 * j][3]);
+          af[2] = pack_bf16(acc[2 * j + 1][0], acc[2 * j + 1][1]);
+          af[3] = pack_bf16(acc[2 * j + 1][2], acc[2 * j + 1][3]);
+          const int kb = p0.f * C::kFeat + 16 * j;
+#pragma unroll
+          for (int n8 = 0; n8 < kFusedOutMax / 8; ++n8) {
+            if (n8 * 8 < d_out) {
+              const uint32_t* wrow = wt + ((n8 * 8 + g8) * kFusedLdw + kb) / 2 + t4;
+              hmma_16816(oacc[n8], af, wrow[0], wrow[4]);
+            }
+          }
+        }
+        const bool win_head = (int64_t)FS * p0.base < a;  // window began in an earlier warp's range
+        const bool win_done = unit_done && p0.f == FS - 1;
+        if (win_done || p0.fi + 1 == b) {
+          if (win_done && !win_head) {
+            const int r0 = lane >> 2, cc = (lane & 3) * 2;
+#pragma unroll
+            for (int n8 = 0; n8 < kFusedOutMax / 8; ++n8)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int r = r0 + 8 * (q >> 1), col = n8 * 8 + cc + (q & 1);
+                if (r < rows && col < d_out) out[(rs + r) * ldo + col] = oacc[n8][q];
+              }
+          } else {
+            float* slot = oscratch + (gw * 2 + (win_head ? 0 : 1)) * kOutSlot;
+#pragma unroll
+            for (int n8 = 0; n8 < kFusedOutMax / 8; ++n8)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) slot[(n8 * 4 + q) * 32 + lane] = oacc[n8][q];
+          }
+#pragma unroll
+          for (int i = 0; i < kFusedOutMax / 8; ++i) oacc[i][0] = oacc[i][1] = oacc[i][2] = oacc[i][3] = 0.f;
+        }
+      }
 #pragma unroll
       for (int i = 0; i < SWV; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
     }
@@ -549,30 +618,95 @@ int spmm_tile_warp_tf32(const int32_t* tile_list, int64_t n_tile, const int64_t*
   return HCS_OK;
 }
 
+// Sums the fused-epilogue out partials of windows cut by warp-range boundaries, in warp order.
+__global__ void k_tile_warp_fixup_out(const int32_t* __restrict__ tile_list, int64_t T,
+                                      const int64_t* __restrict__ chunk_ptr, int64_t n_rows, int wh, int FS,
+                                      int d_out, float* __restrict__ out, int64_t ldo,
+                                      const float* __restrict__ oscratch, int64_t nwarps) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (gw >= nwarps) return;
+  const int64_t total = (int64_t)FS * chunk_ptr[T];
+  int64_t a, b;
+  warp_range(total, nwarps, gw, a, b);
+  if (a >= b) return;
+  const ChunkPos last = locate(chunk_ptr, T, FS, b - 1);
+  const int64_t wstart = (int64_t)FS * last.base, wend = wstart + (int64_t)FS * last.nj;
+  if (!(wend > b && wstart >= a)) return;
+  constexpr int NO = kFusedOutMax / 8;
+  float acc[NO][4];
+  const float* s = oscratch + (gw * 2 + 1) * kOutSlot;
+#pragma unroll
+  for (int n8 = 0; n8 < NO; ++n8)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[n8][q] = s[(n8 * 4 + q) * 32 + lane];
+  for (int64_t k = gw + 1; k < nwarps; ++k) {
+    int64_t ak, bk;
+    warp_range(total, nwarps, k, ak, bk);
+    if (ak >= bk) continue;
+    const float* sk = oscratch + (k * 2 + 0) * kOutSlot;
+#pragma unroll
+    for (int n8 = 0; n8 < NO; ++n8)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[n8][q] += sk[(n8 * 4 + q) * 32 + lane];
+    if (wend <= bk) break;
+  }
+  const int64_t rs = (int64_t)tile_list[last.t] * wh;
+  const int rows = (int)(n_rows - rs < wh ? n_rows - rs : wh);
+  const int r0 = lane >> 2, cc = (lane & 3) * 2;
+#pragma unroll
+  for (int n8 = 0; n8 < NO; ++n8)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = r0 + 8 * (q >> 1), col = n8 * 8 + cc + (q & 1);
+      if (r < rows && col < d_out) out[(rs + r) * ldo + col] = acc[n8][q];
+    }
+}
+
 static int g_warp_swv = 0;  // 0 auto, 4 or 8 (16-B vectors per row slice)
 
-template <int SWV>
+template <int SWV, bool FUSED = false>
 static int launch_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
                        const int64_t* ent_ptr, const uint32_t* ent, int64_t n_rows, int wh, const __nv_bfloat16* x,
                        int64_t ldx, int dim, float* z, int64_t ldz, float* scratch, int64_t scratch_floats,
-                       cudaStream_t st) {
+                       cudaStream_t st, const float* mw = nullptr, int d_out = 0, float* out = nullptr,
+                       int64_t ldo = 0) {
   using C = WarpCfg<SWV>;
   const int FS = (dim + C::kFeat - 1) / C::kFeat;
   const int grid = num_sms();
   const int64_t nwarps = (int64_t)grid * C::kWarps;
-  HCS_REQUIRE(scratch != nullptr && scratch_floats >= nwarps * 2 * C::kSlot, HCS_EINVAL,
-              "tile scratch too small (%lld floats, need %lld)", (long long)scratch_floats,
-              (long long)(nwarps * 2 * C::kSlot));
-  HCS_CUDA(cudaFuncSetAttribute(k_tile_warp<SWV>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
-  k_tile_warp<SWV><<<grid, C::kWarps * 32, C::kSmem, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows,
-                                                            wh, x, ldx, dim, FS, z, ldz, scratch);
+  const int64_t need = nwarps * 2 * C::kSlot + (FUSED ? nwarps * 2 * kOutSlot : 0);
+  HCS_REQUIRE(scratch != nullptr && scratch_floats >= need, HCS_EINVAL, "tile scratch too small (%lld floats, need %lld)",
+              (long long)scratch_floats, (long long)need);
+  float* oscratch = scratch + nwarps * 2 * C::kSlot;
+  const int smem = C::kSmem + (FUSED ? kFusedOutMax * kFusedLdw * 2 : 0);
+  HCS_CUDA(cudaFuncSetAttribute(k_tile_warp<SWV, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  k_tile_warp<SWV, FUSED><<<grid, C::kWarps * 32, smem, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows,
+                                                               wh, x, ldx, dim, FS, z, ldz, scratch, mw, d_out, out,
+                                                               ldo, oscratch);
   HCS_LAUNCH_CHECK("k_tile_warp");
   const int fix_threads = 256;
   const int fix_blocks = (int)((nwarps * 32 + fix_threads - 1) / fix_threads);
-  k_tile_warp_fixup<SWV><<<fix_blocks, fix_threads, 0, st>>>(tile_list, n_tile, chunk_ptr, n_rows, wh, dim, FS, z,
-                                                              ldz, scratch, nwarps);
-  HCS_LAUNCH_CHECK("k_tile_warp_fixup");
+  if (z != nullptr) {
+    k_tile_warp_fixup<SWV><<<fix_blocks, fix_threads, 0, st>>>(tile_list, n_tile, chunk_ptr, n_rows, wh, dim, FS, z,
+                                                                ldz, scratch, nwarps);
+    HCS_LAUNCH_CHECK("k_tile_warp_fixup");
+  }
+  if (FUSED) {
+    k_tile_warp_fixup_out<<<fix_blocks, fix_threads, 0, st>>>(tile_list, n_tile, chunk_ptr, n_rows, wh, FS, d_out,
+                                                               out, ldo, oscratch, nwarps);
+    HCS_LAUNCH_CHECK("k_tile_warp_fixup_out");
+  }
   return HCS_OK;
+}
+
+// K6/K7 on the warp kernel: dim <= 128, d_out <= 64, 64-feature slices.
+int gcn_tile_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
+                  const int64_t* ent_ptr, const uint32_t* ent, int64_t n_rows, int wh, const __nv_bfloat16* x,
+                  int64_t ldx, int dim, float* z, int64_t ldz, const float* m, int d_out, float* out, int64_t ldo,
+                  float* scratch, int64_t scratch_floats, cudaStream_t st) {
+  return launch_warp<8, true>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim, z, ldz,
+                              scratch, scratch_floats, st, m, d_out, out, ldo);
 }
 
 int spmm_tile_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
@@ -590,7 +724,7 @@ int spmm_tile_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chun
 
 int64_t tile_warp_scratch_floats() {
   return std::max<int64_t>((int64_t)num_sms() * WarpCfg<4>::kWarps * 2 * WarpCfg<4>::kSlot,
-                           (int64_t)num_sms() * WarpCfg<8>::kWarps * 2 * WarpCfg<8>::kSlot);
+                           (int64_t)num_sms() * WarpCfg<8>::kWarps * 2 * (WarpCfg<8>::kSlot + kOutSlot));
 }
 
 }  // namespace hcs
