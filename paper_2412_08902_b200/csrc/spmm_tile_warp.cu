@@ -45,8 +45,13 @@ struct WarpCfg {
   static_assert(kSmem <= 227 * 1024, "smem");
   static_assert(SWV != 8 || kSmem + 64 * (128 + 8) * 2 <= 227 * 1024, "fused smem");
   // XOR swizzle of 16-B vector v of row r (conflict-free ldmatrix.trans over 8 consecutive rows)
-  __device__ static __forceinline__ int swz(int r, int v) {
-    return SWV == 4 ? (v ^ ((r >> 1) & 3)) : (v ^ (r & 7));
+  // (SWV = 4: two 64-B rows per 128-B line, bit 2 of the position alternates with r>>3 so the
+  // 8 rows {8q + it} written by one cp.async instruction also spread over all banks)
+  __device__ static __forceinline__ uint32_t off(int r, int v) {
+    if (SWV == 4)
+      return (uint32_t)(r >> 1) * 128u +
+             ((uint32_t)(((r & 1) * 4 + v) ^ (((r >> 1) & 3) | (((r >> 3) & 1) << 2))) << 4);
+    return (uint32_t)r * 128u + ((uint32_t)(v ^ (r & 7)) << 4);
   }
 };
 
@@ -176,49 +181,81 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
   uint8_t* slab_p = wsmem + warp * kWarpSmemPerWarp + kWarpTileStages * kWarpStageBytes;
   const uint64_t keep = policy_evict_last();
   const uint64_t once = policy_evict_first();
+  // gather lane mapping: lane (rg, v) copies 16-B vector v of rows rg*NI + it, it < NI, so its
+  // NI gather indices are contiguous (NI/4 x 128-bit loads)
+  const int gv = lane % SWV, rg = lane / SWV;
+  uint32_t dofs[NI];  // smem destination of each of the lane's copies (constant per lane)
+#pragma unroll
+  for (int it = 0; it < NI; ++it) dofs[it] = C::off(rg * NI + it, gv);
+  const int featv = gv * 8;  // feature offset of the lane's vector inside a slice
+  const uint32_t vb_full = 16u;
   const char* xb = reinterpret_cast<const char*>(x);
-  const int64_t ldxb = ldx * 2;
-  // gather lane mapping: SWV lanes x 16 B per row slice, RPI rows per instruction
-  const int grow = lane / SWV, gv = lane % SWV;
+  const uint32_t ldxb = (uint32_t)(ldx * 2);
   // ldmatrix lane mapping (A: slab rows, B: gathered rows k, 8-feature chunks)
   const int ar = lane & 15, akc = lane >> 4;
   const int bk = (lane & 7) + ((lane >> 3) & 1) * 8, bfc = lane >> 4;
 
-  // pipeline positions: p0 = chunk being computed, p1, p2 (gathers in flight), p3 (indices prefetched)
-  ChunkPos p0 = locate(chunk_ptr, T, FS, a);
-  ChunkPos p1 = p0, p2, p3;
-  advance(p1, chunk_ptr, T, FS);
-  p2 = p1;
-  advance(p2, chunk_ptr, T, FS);
-  p3 = p2;
-  advance(p3, chunk_ptr, T, FS);
-  bool in_head = p0.j != 0;  // our first unit (t, f) began in an earlier warp's range
-
-  auto load_gidx = [&](const ChunkPos& p, int (&g)[NI]) {
-    if (p.fi < b) {
-      const int32_t* gp = gidx + (p.base + p.j) * 64 + grow;
+  struct Pos {
+    int64_t base;   // chunk_ptr[t]
+    int32_t t, f, j, nj, rem;  // rem = b - flattened index (valid while > 0)
+  };
+  auto mk = [&](const ChunkPos& c) {
+    Pos p;
+    p.base = c.base;
+    p.t = (int32_t)c.t;
+    p.f = c.f;
+    p.j = c.j;
+    p.nj = c.nj;
+    p.rem = (int32_t)(b - c.fi);
+    return p;
+  };
+  auto adv = [&](Pos& p) {
+    --p.rem;
+    if (++p.j < p.nj) return;
+    p.j = 0;
+    if (++p.f < FS) return;
+    p.f = 0;
+    ++p.t;
+    p.base += p.nj;
+    p.nj = (p.t < T && p.rem > 0) ? (int32_t)(ldg64(chunk_ptr + p.t + 1) - p.base) : 1;
+  };
+  auto load_gidx = [&](const Pos& p, int (&g)[NI]) {
+    if (p.rem > 0) {
+      const int4* gp = reinterpret_cast<const int4*>(gidx + (p.base + p.j) * 64 + rg * NI);
 #pragma unroll
-      for (int it = 0; it < NI; ++it) g[it] = ld_plan_s32(gp + RPI * it, once);
+      for (int q = 0; q < NI / 4; ++q) {
+        int4 v;
+        asm volatile("ld.global.nc.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "l"(gp + q), "l"(once));
+        g[4 * q] = v.x;
+        g[4 * q + 1] = v.y;
+        g[4 * q + 2] = v.z;
+        g[4 * q + 3] = v.w;
+      }
     }
   };
-  auto issue = [&](const ChunkPos& p, const int (&g)[NI], int slot) {
-    if (p.fi < b) {
-      const int feat = p.f * C::kFeat + gv * 8;
-      const uint32_t vb = feat < dim ? 16u : 0u;
+  auto issue = [&](const Pos& p, const int (&g)[NI], int slot) {
+    if (p.rem > 0) {
+      const int feat = p.f * C::kFeat + featv;
+      const uint32_t vb = feat < dim ? vb_full : 0u;
       const char* src = xb + (int64_t)feat * 2;
       const uint32_t dst = stage0 + slot * kWarpStageBytes;
+      if (p.j + 1 < p.nj) {  // full chunk: every slot holds a column
 #pragma unroll
-      for (int it = 0; it < NI; ++it) {
-        const int row = grow + RPI * it;
-        const int gi = g[it];
-        cp_async16(dst + row * C::kRowBytes + (C::swz(row, gv) << 4), src + (int64_t)max(gi, 0) * ldxb,
-                   gi >= 0 ? vb : 0u, keep);
+        for (int it = 0; it < NI; ++it) cp_async16(dst + dofs[it], src + (uint64_t)(uint32_t)g[it] * ldxb, vb, keep);
+      } else {  // the window's last chunk: pad slots (-1) are zero-filled
+#pragma unroll
+        for (int it = 0; it < NI; ++it) {
+          const int gi = g[it];
+          cp_async16(dst + dofs[it], src + (uint64_t)(uint32_t)max(gi, 0) * ldxb, gi >= 0 ? vb : 0u, keep);
+        }
       }
     }
     cp_async_commit();
   };
-  auto load_ep = [&](const ChunkPos& p, int64_t& e0, int64_t& e1) {
-    if (p.fi < b) {
+  auto load_ep = [&](const Pos& p, int64_t& e0, int64_t& e1) {
+    if (p.rem > 0) {
       const int64_t c = p.base + p.j;
       e0 = ld_plan_s64(ent_ptr + c, once);
       e1 = ld_plan_s64(ent_ptr + c + 1, once);
@@ -234,56 +271,44 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
     }
   };
 
-  int g_a[NI], g_b[NI];
-  // prologue: gathers of p0, p1 in flight; indices of p2; entries of p0; entry pointers of p1
-  load_gidx(p0, g_a);
-  load_gidx(p1, g_b);
-  issue(p0, g_a, 0);
-  issue(p1, g_b, 1);
-  int g2[NI];
-  load_gidx(p2, g2);
-  int64_t ep0a, ep0b, ep1a, ep1b;
-  load_ep(p0, ep0a, ep0b);
-  load_ep(p1, ep1a, ep1b);
-  uint32_t e0r[kWarpEntRegs], e1r[kWarpEntRegs];
-  load_ent(ep0a, ep0b, e0r);
-
   float acc[SWV][4];
 #pragma unroll
   for (int i = 0; i < SWV; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
   float oacc[FUSED ? kFusedOutMax / 8 : 1][4];
 #pragma unroll
   for (int i = 0; i < (FUSED ? kFusedOutMax / 8 : 1); ++i) oacc[i][0] = oacc[i][1] = oacc[i][2] = oacc[i][3] = 0.f;
+  bool in_head;  // our first unit (t, f) began in an earlier warp's range
+  int s0 = 0;    // ring slot of the chunk being computed
 
-  int s0 = 0;  // ring slot of p0
-  for (; p0.fi < b;) {
-    // 1. gathers of p2 (slot s0+2), then indices of p3 for the next iteration
+  // one pipeline step: compute P0 while P1, P2 are in flight; gathers of P2, indices of P3,
+  // entries of P1, entry pointers of P2.  Register sets rotate by renaming (loop unrolled 4x),
+  // so no in-flight load result is copied before it is needed.
+  auto step = [&](Pos& P0, const Pos& P1, const Pos& P2, const Pos& P3, int (&Gcur)[NI], int (&Gnext)[NI],
+                  uint32_t (&Ecur)[kWarpEntRegs], uint32_t (&Enext)[kWarpEntRegs], const int64_t (&EP0)[2],
+                  const int64_t (&EP1)[2], int64_t (&EP2)[2]) -> bool {
+    if (P0.rem <= 0) return true;
     const int s2 = s0 >= 1 ? s0 - 1 : s0 + 2;
-    issue(p2, g2, s2);
-    load_gidx(p3, g2);
-    // 2. entries of p1 (used next iteration), entry pointers of p2
-    load_ent(ep1a, ep1b, e1r);
-    int64_t ep2a, ep2b;
-    load_ep(p2, ep2a, ep2b);
-    // 3. slab of p0: zero, scatter packed entries (bf16 value << 16 | swizzled byte offset)
+    issue(P2, Gcur, s2);
+    load_gidx(P3, Gnext);
+    load_ent(EP1[0], EP1[1], Enext);
+    load_ep(P2, EP2[0], EP2[1]);
+    // slab of P0: zero, scatter packed entries (bf16 value << 16 | swizzled byte offset)
     {
       const int4 zero4 = make_int4(0, 0, 0, 0);
 #pragma unroll
       for (int q = 0; q < 4; ++q) reinterpret_cast<int4*>(slab_p)[lane + 32 * q] = zero4;
       __syncwarp();
-      const int ne = (int)(ep0b - ep0a);
+      const int ne = (int)(EP0[1] - EP0[0]);
 #pragma unroll
       for (int q = 0; q < kWarpEntRegs; ++q)
-        if (lane + 32 * q < ne) *reinterpret_cast<uint16_t*>(slab_p + (e0r[q] & 0x7FFu)) = (uint16_t)(e0r[q] >> 16);
+        if (lane + 32 * q < ne) *reinterpret_cast<uint16_t*>(slab_p + (Ecur[q] & 0x7FFu)) = (uint16_t)(Ecur[q] >> 16);
       for (int i = 32 * kWarpEntRegs + lane; i < ne; i += 32) {  // rare: > 128 entries in a chunk
-        const uint32_t w = ld_plan_u32(ent + ep0a + i, once);
+        const uint32_t w = ld_plan_u32(ent + EP0[0] + i, once);
         *reinterpret_cast<uint16_t*>(slab_p + (w & 0x7FFu)) = (uint16_t)(w >> 16);
       }
     }
-    // 4. p0's gathers landed (the two newest groups may still be in flight)
-    cp_async_wait<2>();
+    cp_async_wait<2>();  // P0's gathers landed (P1, P2 may still be in flight)
     __syncwarp();
-    // 5. 64 x 32 slice: 4 k16 steps x 4 n8 tiles
     {
       const uint32_t st = stage0 + s0 * kWarpStageBytes;
 #pragma unroll
@@ -292,25 +317,24 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
         const int kc = 2 * ks + akc;
         ldsm_x4(af, slab + ar * 128 + (((kc ^ ar) & 7) << 4));
         const int k = ks * 16 + bk;
-        const uint32_t rowa = st + k * C::kRowBytes;
 #pragma unroll
         for (int pr = 0; pr < SWV / 2; ++pr) {
           uint32_t bb[4];
-          ldsm_x4_trans(bb, rowa + (C::swz(k, 2 * pr + bfc) << 4));
+          ldsm_x4_trans(bb, st + C::off(k, 2 * pr + bfc));
           hmma_16816(acc[2 * pr], af, bb[0], bb[1]);
           hmma_16816(acc[2 * pr + 1], af, bb[2], bb[3]);
         }
       }
     }
     __syncwarp();
-    // 6. end of our part of the unit: Z (whole unit) or a scratch slot (split unit)
-    const bool unit_done = p0.j + 1 == p0.nj;
-    if (unit_done || p0.fi + 1 == b) {
-      const int64_t rs = (int64_t)__ldg(tile_list + p0.t) * wh;
+    // end of our part of the unit: Z (whole unit) or a scratch slot (split unit)
+    const bool unit_done = P0.j + 1 == P0.nj;
+    if (unit_done || P0.rem == 1) {
+      const int64_t rs = (int64_t)__ldg(tile_list + P0.t) * wh;
       const int rows = (int)(n_rows - rs < wh ? n_rows - rs : wh);
       if (z != nullptr) {
         if (!in_head && unit_done) {
-          store_slice<SWV>(z, ldz, rs, rows, dim, p0.f, acc, lane);
+          store_slice<SWV>(z, ldz, rs, rows, dim, P0.f, acc, lane);
         } else {
           float* slot = scratch + (gw * 2 + (in_head ? 0 : 1)) * C::kSlot;
 #pragma unroll
@@ -331,7 +355,7 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
           af[1] = pack_bf16(acc[2 * j][2], acc[2 * j][3]);
           af[2] = pack_bf16(acc[2 * j + 1][0], acc[2 * j + 1][1]);
           af[3] = pack_bf16(acc[2 * j + 1][2], acc[2 * j + 1][3]);
-          const int kb = p0.f * C::kFeat + 16 * j;
+          const int kb = P0.f * C::kFeat + 16 * j;
 #pragma unroll
           for (int n8 = 0; n8 < kFusedOutMax / 8; ++n8) {
             if (n8 * 8 < d_out) {
@@ -340,9 +364,9 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
             }
           }
         }
-        const bool win_head = (int64_t)FS * p0.base < a;  // window began in an earlier warp's range
-        const bool win_done = unit_done && p0.f == FS - 1;
-        if (win_done || p0.fi + 1 == b) {
+        const bool win_head = (int64_t)FS * P0.base < a;  // window began in an earlier warp's range
+        const bool win_done = unit_done && P0.f == FS - 1;
+        if (win_done || P0.rem == 1) {
           if (win_done && !win_head) {
             const int r0 = lane >> 2, cc = (lane & 3) * 2;
 #pragma unroll
@@ -366,18 +390,37 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
 #pragma unroll
       for (int i = 0; i < SWV; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
     }
-    // 7. rotate the pipeline
-    p0 = p1;
-    p1 = p2;
-    p2 = p3;
-    advance(p3, chunk_ptr, T, FS);
-#pragma unroll
-    for (int q = 0; q < kWarpEntRegs; ++q) e0r[q] = e1r[q];
-    ep0a = ep1a;
-    ep0b = ep1b;
-    ep1a = ep2a;
-    ep1b = ep2b;
     s0 = s0 == kWarpTileStages - 1 ? 0 : s0 + 1;
+    P0 = P3;  // P0's variable becomes position +4
+    adv(P0);
+    return false;
+  };
+
+  // prologue
+  const ChunkPos c0 = locate(chunk_ptr, T, FS, a);
+  in_head = c0.j != 0;
+  Pos Q0 = mk(c0), Q1 = Q0;
+  adv(Q1);
+  Pos Q2 = Q1;
+  adv(Q2);
+  Pos Q3 = Q2;
+  adv(Q3);
+  int G0[NI], G1[NI];
+  load_gidx(Q0, G0);
+  load_gidx(Q1, G1);
+  issue(Q0, G0, 0);
+  issue(Q1, G1, 1);
+  load_gidx(Q2, G0);
+  int64_t EPa[2], EPb[2], EPc[2], EPd[2];
+  load_ep(Q0, EPa[0], EPa[1]);
+  load_ep(Q1, EPb[0], EPb[1]);
+  uint32_t E0[kWarpEntRegs], E1[kWarpEntRegs];
+  load_ent(EPa[0], EPa[1], E0);
+  for (;;) {
+    if (step(Q0, Q1, Q2, Q3, G0, G1, E0, E1, EPa, EPb, EPc)) break;
+    if (step(Q1, Q2, Q3, Q0, G1, G0, E1, E0, EPb, EPc, EPd)) break;
+    if (step(Q2, Q3, Q0, Q1, G0, G1, E0, E1, EPc, EPd, EPa)) break;
+    if (step(Q3, Q0, Q1, Q2, G1, G0, E1, E0, EPd, EPa, EPb)) break;
   }
   cp_async_wait<0>();
 }
