@@ -36,7 +36,7 @@ struct WarpCfg {
   static constexpr int kFeat = 8 * SWV;                  // features per slice
   static constexpr int kRowBytes = 16 * SWV;             // bytes per gathered row slice
   static constexpr int kStageBytes = 64 * kRowBytes;     // 64 rows (one chunk)
-  static constexpr int kWarps = SWV == 4 ? 16 : 8;       // warps per CTA (smem-limited)
+  static constexpr int kWarps = SWV == 4 ? 12 : 8;       // warps per CTA (smem / register limited)
   static constexpr int kPerWarp = kWarpTileStages * kStageBytes + kWarpSlabBytes;
   static constexpr int kSmem = kWarps * kPerWarp + 128;
   static constexpr int kIssue = 2 * SWV;                 // cp.async instructions per chunk
@@ -178,7 +178,6 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
 
   const uint32_t stage0 = smem_u32(wsmem + warp * kWarpSmemPerWarp);
   const uint32_t slab = stage0 + kWarpTileStages * kWarpStageBytes;
-  uint8_t* slab_p = wsmem + warp * kWarpSmemPerWarp + kWarpTileStages * kWarpStageBytes;
   const uint64_t keep = policy_evict_last();
   const uint64_t once = policy_evict_first();
   // gather lane mapping: lane (rg, v) copies 16-B vector v of rows rg*NI + it, it < NI, so its
@@ -294,17 +293,16 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
     load_ep(P2, EP2[0], EP2[1]);
     // slab of P0: zero, scatter packed entries (bf16 value << 16 | swizzled byte offset)
     {
-      const int4 zero4 = make_int4(0, 0, 0, 0);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) reinterpret_cast<int4*>(slab_p)[lane + 32 * q] = zero4;
+      for (int q = 0; q < 4; ++q) sts128_zero(slab + (lane + 32 * q) * 16);
       __syncwarp();
       const int ne = (int)(EP0[1] - EP0[0]);
 #pragma unroll
       for (int q = 0; q < kWarpEntRegs; ++q)
-        if (lane + 32 * q < ne) *reinterpret_cast<uint16_t*>(slab_p + (Ecur[q] & 0x7FFu)) = (uint16_t)(Ecur[q] >> 16);
+        if (lane + 32 * q < ne) sts16(slab + (Ecur[q] & 0x7FFu), Ecur[q] >> 16);
       for (int i = 32 * kWarpEntRegs + lane; i < ne; i += 32) {  // rare: > 128 entries in a chunk
         const uint32_t w = ld_plan_u32(ent + EP0[0] + i, once);
-        *reinterpret_cast<uint16_t*>(slab_p + (w & 0x7FFu)) = (uint16_t)(w >> 16);
+        sts16(slab + (w & 0x7FFu), w >> 16);
       }
     }
     cp_async_wait<2>();  // P0's gathers landed (P1, P2 may still be in flight)
