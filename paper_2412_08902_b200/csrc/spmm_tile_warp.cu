@@ -82,18 +82,21 @@ struct ChunkPos {
 
 __device__ __forceinline__ int64_t ldg64(const int64_t* p) { return __ldg(p); }
 
-// unit containing flattened chunk index v (0 <= v < FS * chunk_ptr[T])
+// unit containing flattened chunk index v (0 <= v < FS * (chunk_ptr[T] - chunk_ptr[0])).
+// chunk_ptr may be a view into a larger plan (sub-range launches): flattened indices are
+// relative to chunk_ptr[0], plan arrays (gidx, ent_ptr) are addressed with absolute chunks.
 __device__ __forceinline__ ChunkPos locate(const int64_t* __restrict__ chunk_ptr, int64_t T, int FS, int64_t v) {
-  int64_t lo = 0, hi = T;  // largest t with FS*chunk_ptr[t] <= v
+  const int64_t c0 = ldg64(chunk_ptr);
+  int64_t lo = 0, hi = T;  // largest t with FS*(chunk_ptr[t]-c0) <= v
   while (hi - lo > 1) {
     const int64_t mid = (lo + hi) >> 1;
-    if (FS * ldg64(chunk_ptr + mid) <= v) lo = mid; else hi = mid;
+    if (FS * (ldg64(chunk_ptr + mid) - c0) <= v) lo = mid; else hi = mid;
   }
   ChunkPos p;
   p.t = lo;
   p.base = ldg64(chunk_ptr + lo);
   p.nj = (int32_t)(ldg64(chunk_ptr + lo + 1) - p.base);
-  const int64_t rem = v - FS * p.base;
+  const int64_t rem = v - FS * (p.base - c0);
   p.f = (int32_t)(rem / p.nj);
   p.j = (int32_t)(rem - (int64_t)p.f * p.nj);
   p.fi = v;
@@ -163,7 +166,8 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * kWarpTileWarps;
   const int64_t gw = (int64_t)blockIdx.x * kWarpTileWarps + warp;
-  const int64_t total = (int64_t)FS * chunk_ptr[T];
+  const int64_t c0 = chunk_ptr[0];
+  const int64_t total = (int64_t)FS * (chunk_ptr[T] - c0);
   int64_t a, b;
   warp_range(total, nwarps, gw, a, b);
   if (FUSED) {
@@ -362,7 +366,7 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
             }
           }
         }
-        const bool win_head = (int64_t)FS * P0.base < a;  // window began in an earlier warp's range
+        const bool win_head = (int64_t)FS * (P0.base - c0) < a;  // window began in an earlier warp's range
         const bool win_done = unit_done && P0.f == FS - 1;
         if (win_done || P0.rem == 1) {
           if (win_done && !win_head) {
@@ -395,9 +399,9 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
   };
 
   // prologue
-  const ChunkPos c0 = locate(chunk_ptr, T, FS, a);
-  in_head = c0.j != 0;
-  Pos Q0 = mk(c0), Q1 = Q0;
+  const ChunkPos first = locate(chunk_ptr, T, FS, a);
+  in_head = first.j != 0;
+  Pos Q0 = mk(first), Q1 = Q0;
   adv(Q1);
   Pos Q2 = Q1;
   adv(Q2);
@@ -432,12 +436,13 @@ __global__ void k_tile_warp_fixup(const int32_t* __restrict__ tile_list, int64_t
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (gw >= nwarps) return;
-  const int64_t total = (int64_t)FS * chunk_ptr[T];
+  const int64_t c0 = chunk_ptr[0];
+  const int64_t total = (int64_t)FS * (chunk_ptr[T] - c0);
   int64_t a, b;
   warp_range(total, nwarps, gw, a, b);
   if (a >= b) return;
   const ChunkPos last = locate(chunk_ptr, T, FS, b - 1);
-  const int64_t ustart = (int64_t)FS * last.base + (int64_t)last.f * last.nj;
+  const int64_t ustart = (int64_t)FS * (last.base - c0) + (int64_t)last.f * last.nj;
   const int64_t uend = ustart + last.nj;
   if (!(uend > b && ustart >= a)) return;  // not the warp that opens a split unit
   constexpr int kSlot = WarpCfg<SWV>::kSlot;
@@ -487,7 +492,8 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * kTfWarps;
   const int64_t gw = (int64_t)blockIdx.x * kTfWarps + warp;
-  const int64_t total = (int64_t)FS * chunk_ptr[T];
+  const int64_t c0 = chunk_ptr[0];
+  const int64_t total = (int64_t)FS * (chunk_ptr[T] - c0);
   int64_t a, b;
   warp_range(total, nwarps, gw, a, b);
   if (a >= b) return;
@@ -667,12 +673,13 @@ __global__ void k_tile_warp_fixup_out(const int32_t* __restrict__ tile_list, int
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (gw >= nwarps) return;
-  const int64_t total = (int64_t)FS * chunk_ptr[T];
+  const int64_t c0 = chunk_ptr[0];
+  const int64_t total = (int64_t)FS * (chunk_ptr[T] - c0);
   int64_t a, b;
   warp_range(total, nwarps, gw, a, b);
   if (a >= b) return;
   const ChunkPos last = locate(chunk_ptr, T, FS, b - 1);
-  const int64_t wstart = (int64_t)FS * last.base, wend = wstart + (int64_t)FS * last.nj;
+  const int64_t wstart = (int64_t)FS * (last.base - c0), wend = wstart + (int64_t)FS * last.nj;
   if (!(wend > b && wstart >= a)) return;
   constexpr int NO = kFusedOutMax / 8;
   float acc[NO][4];

@@ -226,6 +226,12 @@ class HybridPlan:
         else:
             self.scalar_vals, self.scalar_vals_code = csr.values, _lib.DTYPE_F32
 
+    @property
+    def _cache(self) -> dict:
+        if getattr(self, "_cache_d", None) is None:
+            self._cache_d = {}
+        return self._cache_d
+
     def scratch(self) -> torch.Tensor:
         """Partial-sum slots of the tile kernel (engine 2); one per plan, stream-ordered use."""
         if getattr(self, "_scratch", None) is None:
@@ -238,26 +244,49 @@ class HybridPlan:
         """Kernels of one run(): engine 2 = tile kernel + fix-up, plus the scalar kernel."""
         return (2 if self.n_tile else 0) + (1 if self.scalar_list.numel() else 0)
 
-    def run(self, xop: DeviceOperand, z: torch.Tensor, ldz: int, stream=None, tile_events=None) -> None:
+    def parts(self, k: int) -> list[tuple[int, int, int, int, int, int]]:
+        """k contiguous window ranges of ~equal nnz: (w0, w1, tile t0, t1, scalar s0, s1) each."""
+        key = ("parts", k)
+        if key not in self._cache:
+            ws = self.windows
+            W, wh, n = len(ws), ws.window_height, ws.num_rows
+            rp = ws.csr.row_ptr
+            starts = rp[torch.clamp(torch.arange(W + 1, device=rp.device) * wh, max=n)].cpu().numpy()
+            targets = (np.arange(1, k) * int(starts[-1])) // k
+            bounds = [0] + [int(v) for v in np.searchsorted(starts, targets, side="left")] + [W]
+            tl = self.tile_list.cpu().numpy()
+            sl = self.scalar_list.cpu().numpy()
+            out = []
+            for i in range(k):
+                w0, w1 = bounds[i], max(bounds[i], bounds[i + 1])
+                out.append((w0, w1, int(np.searchsorted(tl, w0)), int(np.searchsorted(tl, w1)),
+                            int(np.searchsorted(sl, w0)), int(np.searchsorted(sl, w1))))
+            self._cache[key] = out
+        return self._cache[key]
+
+    def run(self, xop: DeviceOperand, z: torch.Tensor, ldz: int, stream=None, tile_events=None, part=None) -> None:
         """Launch K4 (tile windows) then K3 (scalar + empty windows) on the current stream.
-        tile_events: optional (start, end) torch.cuda.Event pair recorded around K4."""
+        tile_events: optional (start, end) torch.cuda.Event pair recorded around K4.
+        part: optional (w0, w1, t0, t1, s0, s1) from parts(): only windows [w0, w1)."""
         csr = self.windows.csr
         s = _lib.stream() if stream is None else stream
+        t0, t1 = (0, self.n_tile) if part is None else part[2:4]
+        s0, s1 = (0, int(self.scalar_list.numel())) if part is None else part[4:6]
         if tile_events is not None:
             tile_events[0].record()
-        if self.n_tile:
+        if t1 > t0:
             scratch = self.scratch()
-            _lib.call("hcs_spmm_tile", self.tile_list.data_ptr(), self.n_tile, self.chunk_ptr.data_ptr(),
+            _lib.call("hcs_spmm_tile", self.tile_list.data_ptr() + 4 * t0, t1 - t0, self.chunk_ptr.data_ptr() + 8 * t0,
                       self.gidx.data_ptr(), self.ent_ptr.data_ptr(), self.ent.data_ptr(), self.ent_dtype,
                       csr.num_rows, self.windows.window_height, xop.t.data_ptr(), xop.dtype_code, xop.rows, xop.dim,
                       xop.ld, z.data_ptr(), ldz, scratch.data_ptr(), scratch.numel() * 4, s)
         if tile_events is not None:
             tile_events[1].record()
-        if self.scalar_list.numel():
+        if s1 > s0:
             _lib.call("hcs_spmm_scalar", csr.row_ptr.data_ptr(), csr.col_idx.data_ptr(), self.scalar_vals.data_ptr(),
-                      self.scalar_vals_code, csr.num_rows, self.windows.window_height, self.scalar_list.data_ptr(),
-                      self.scalar_list.numel(), xop.t.data_ptr(), xop.dtype_code, xop.rows, xop.dim, xop.ld,
-                      z.data_ptr(), ldz, s)
+                      self.scalar_vals_code, csr.num_rows, self.windows.window_height,
+                      self.scalar_list.data_ptr() + 4 * s0, s1 - s0, xop.t.data_ptr(), xop.dtype_code, xop.rows,
+                      xop.dim, xop.ld, z.data_ptr(), ldz, s)
 
 
 def get_plan(windows, assignment: Assignment, precision: str) -> HybridPlan:
@@ -324,8 +353,41 @@ def spmm_hybrid(windows, assignment: Assignment, x, precision: str = "bf16", thr
     plan = get_plan(ws, assignment, precision)
     xop, was_host = stage_operand(x, precision, dev, tf32_round=(precision == "tf32" and plan.n_tile > 0))
     z, ldz = _alloc_z(ws.num_rows, xop.dim, dev)
+    if was_host and len(ws) >= HOST_PIPELINE_MIN_WINDOWS:
+        return _run_host_pipelined(plan, xop, z, ldz, _host_kind(x), ExecStats(**plan.stats.as_dict()))
     plan.run(xop, z, ldz)
     return _wrap_result(z, xop.dim, _host_kind(x) if was_host else False, ExecStats(**plan.stats.as_dict()))
+
+
+HOST_PIPELINE_MIN_WINDOWS = 4096
+HOST_PIPELINE_PARTS = 4
+_COPY_STREAMS: dict = {}
+
+
+def _run_host_pipelined(plan, xop, z, ldz, host_kind, stats) -> SpmmResult:
+    """Host-memory result: the windows run in HOST_PIPELINE_PARTS nnz-balanced row ranges,
+    and each range's Z rows are copied to pinned host memory on a copy stream while the
+    next range computes (D2H overlapped with the SpMM)."""
+    dev = z.device
+    dim = xop.dim
+    cs = _COPY_STREAMS.get(dev)
+    if cs is None:
+        cs = _COPY_STREAMS[dev] = torch.cuda.Stream(device=dev)
+    host = torch.empty((z.shape[0], dim), dtype=torch.float32, pin_memory=True)
+    wh, n = plan.windows.window_height, z.shape[0]
+    cur = torch.cuda.current_stream(dev)
+    for part in plan.parts(HOST_PIPELINE_PARTS):
+        plan.run(xop, z, ldz, part=part)
+        r0, r1 = min(part[0] * wh, n), min(part[1] * wh, n)
+        if r1 > r0:
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            cs.wait_event(ev)
+            with torch.cuda.stream(cs):
+                host[r0:r1].copy_(z[r0:r1, :dim], non_blocking=True)
+    cs.synchronize()
+    z.record_stream(cs)
+    return SpmmResult(DenseMatrix(host if host_kind == "torch" else host.numpy()), stats)
 
 
 def spmm_tile(windows, x, precision: str = "bf16", tile_cols: int = 8, dim_tile: int = 16,

@@ -234,3 +234,26 @@ def test_tf32_tile_dims_plaw(cuda_ok, dim):
     r2 = hc.spmm_tile(ws, hc.DenseMatrix(x), precision="tf32")
     assert orc.max_rel_err(r1.z.data, orc.spmm_exact(a, x)) <= TF32_TOL
     assert np.array_equal(r1.z.data, r2.z.data)
+
+
+def test_host_pipelined_path(cuda_ok):
+    """Host inputs with >= 4096 windows: partial launches with D2H overlapped; same result
+    (to fp32 summation order) as the device-resident path and the exact product."""
+    import gen_graphs as gg
+    from paper_2412_08902_b200 import executors as ex
+
+    n, rr, cc = gg.power_law(70000, 24.0, seed=5)
+    adj = orc.from_coo(n, n, rr, cc, np.ones(len(rr)))
+    a = orc.normalize_adj(adj, "gcn")
+    ws = hc.partition(to_hc(a))
+    assert len(ws) >= ex.HOST_PIPELINE_MIN_WINDOWS
+    asg = hc.classify_windows(hc.default_model(), ws)
+    x = orc.random_dense(n, 64, seed=2)
+    host = hc.spmm_hybrid(ws, asg, hc.DenseMatrix(x))            # numpy in -> numpy out (pipelined)
+    xt = torch.from_numpy(x).to(torch.bfloat16).cuda()
+    dev = hc.spmm_hybrid(ws, asg, xt)                            # device in -> device out
+    assert isinstance(host.z.data, np.ndarray)
+    d = dev.z.data.cpu().numpy()
+    assert np.abs(host.z.data - d).max() <= 1e-5 * np.abs(d).max()
+    assert orc.max_rel_err(host.z.data, orc.spmm_exact(a, x)) <= BF16_TOL
+    assert host.stats == dev.stats
