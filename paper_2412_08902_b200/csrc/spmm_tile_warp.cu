@@ -36,7 +36,7 @@ struct WarpCfg {
   static constexpr int kFeat = 8 * SWV;                  // features per slice
   static constexpr int kRowBytes = 16 * SWV;             // bytes per gathered row slice
   static constexpr int kStageBytes = 64 * kRowBytes;     // 64 rows (one chunk)
-  static constexpr int kWarps = SWV == 4 ? 12 : 8;       // warps per CTA (smem / register limited)
+  static constexpr int kWarps = SWV == 4 ? 12 : (SWV == 8 ? 8 : 4);  // warps per CTA (smem / register limited)
   static constexpr int kPerWarp = kWarpTileStages * kStageBytes + kWarpSlabBytes;
   static constexpr int kSmem = kWarps * kPerWarp + 128;
   static constexpr int kIssue = 2 * SWV;                 // cp.async instructions per chunk
@@ -51,6 +51,7 @@ struct WarpCfg {
     if (SWV == 4)
       return (uint32_t)(r >> 1) * 128u +
              ((uint32_t)(((r & 1) * 4 + v) ^ (((r >> 1) & 3) | (((r >> 3) & 1) << 2))) << 4);
+    if (SWV == 16) return (uint32_t)r * 256u + ((uint32_t)((v & 8) | ((v ^ r) & 7)) << 4);
     return (uint32_t)r * 128u + ((uint32_t)(v ^ (r & 7)) << 4);
   }
 };
@@ -763,6 +764,9 @@ int spmm_tile_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chun
                    cudaStream_t st) {
   // 64-feature slices halve the per-feature slab work once a window has >= 2 slices of 32
   const int swv = g_warp_swv ? g_warp_swv : (dim > 32 ? 8 : 4);
+  if (swv == 16)
+    return launch_warp<16>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim, z, ldz, scratch,
+                           scratch_floats, st);
   if (swv == 8)
     return launch_warp<8>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim, z, ldz, scratch,
                           scratch_floats, st);
@@ -771,15 +775,18 @@ int spmm_tile_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chun
 }
 
 int64_t tile_warp_scratch_floats() {
-  return std::max<int64_t>((int64_t)num_sms() * WarpCfg<4>::kWarps * 2 * WarpCfg<4>::kSlot,
-                           (int64_t)num_sms() * WarpCfg<8>::kWarps * 2 * (WarpCfg<8>::kSlot + kOutSlot));
+  return std::max<int64_t>(
+      std::max<int64_t>((int64_t)num_sms() * WarpCfg<4>::kWarps * 2 * WarpCfg<4>::kSlot,
+                        (int64_t)num_sms() * WarpCfg<8>::kWarps * 2 * (WarpCfg<8>::kSlot + kOutSlot)),
+      (int64_t)num_sms() * WarpCfg<16>::kWarps * 2 * WarpCfg<16>::kSlot);
 }
 
 }  // namespace hcs
 
 // Row-slice width of the warp-independent tile kernel: 0 auto, 4 (32 features) or 8 (64).
 extern "C" int hcs_set_tile_slice(int vectors) {
-  HCS_REQUIRE(vectors == 0 || vectors == 4 || vectors == 8, HCS_EINVAL, "slice must be 0, 4 or 8 (got %d)", vectors);
+  HCS_REQUIRE(vectors == 0 || vectors == 4 || vectors == 8 || vectors == 16, HCS_EINVAL,
+              "slice must be 0, 4, 8 or 16 (got %d)", vectors);
   hcs::g_warp_swv = vectors;
   return HCS_OK;
 }

@@ -26,7 +26,7 @@ for dim in dims:
         set_tile_engine(eng)
         for np_ in nps:
             if eng == "warp":
-                _lib.call("hcs_set_tile_slice", np_ if np_ in (4, 8) else 0)
+                _lib.call("hcs_set_tile_slice", np_ if np_ in (4, 8, 16) else 0)
             else:
                 _lib.call("hcs_set_tile_producers", np_)
             for _ in range(3): plan.run(xop, z, dim)
