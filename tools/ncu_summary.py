@@ -45,8 +45,9 @@ def full(rep):
     for name, d in raw(rep):
         print(f"kernel: {name[:160]}")
         for k in KEYS:
-            if k in d:
-                print(f"  {k:95s} {d[k][0]:>20s} {d[k][1]}")
+            hit = k if k in d else next((h for h in d if h.endswith("." + k)), None)
+            if hit is not None:
+                print(f"  {k:95s} {d[hit][0]:>20s} {d[hit][1]}")
 
 
 def traffic(rep):
