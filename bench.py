@@ -214,23 +214,40 @@ def run_ours(args):
         if world > 1:
             import torch.distributed as dist
 
-            # exchange between layers: the next layer consumes bf16 features, so rows travel
-            # as bf16 (padded to the largest shard for all_gather_into_tensor)
-            rows_per = [min(r[1] * 16, n) - r[0] * 16 for r in ranges]
-            maxrows = max(rows_per)
-            send = torch.zeros((maxrows, dim), dtype=torch.bfloat16, device=dev)
-            gathered = torch.empty((world * maxrows, dim), dtype=torch.bfloat16, device=dev)
+            # exchange between layers: the next layer consumes bf16 features, so rows travel as
+            # bf16.  The rank's windows run in `parts` nnz-balanced ranges; each range's rows are
+            # all-gathered (padded to the largest rank's range) while the next range computes.
             gloo = dist.get_backend() != "nccl"
+            nparts = max(1, int(os.environ.get("HCS_EXCHANGE_PARTS", "2")))
+            parts = plan.parts(nparts)
+            nloc = local_a.num_rows
+            spans = [(min(p_[0] * 16, nloc), min(p_[1] * 16, nloc)) for p_ in parts]
+            cnt = torch.tensor([b_ - a_ for a_, b_ in spans], dtype=torch.int64,
+                               device="cpu" if gloo else dev)
+            allc = [torch.empty_like(cnt) for _ in range(world)]
+            dist.all_gather(allc, cnt)
+            maxrows = [max(int(c[i]) for c in allc) for i in range(nparts)]
+            sends = [torch.zeros((max(m, 1), dim), dtype=torch.bfloat16, device=dev) for m in maxrows]
+            recvs = [torch.empty((world * max(m, 1), dim), dtype=torch.bfloat16, device=dev) for m in maxrows]
         tev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
 
         def step(i=None):
-            plan.run(xop, z, ldz, tile_events=tev[i] if i is not None else None)
-            if world > 1:
-                send[: z.shape[0]].copy_(z[:, :dim])
+            if world == 1:
+                plan.run(xop, z, ldz, tile_events=tev[i] if i is not None else None)
+                return
+            works = []
+            for k, part in enumerate(parts):
+                plan.run(xop, z, ldz, part=part,
+                         tile_events=tev[i] if (i is not None and k == 0) else None)
+                r0, r1 = spans[k]
+                if r1 > r0:
+                    sends[k][: r1 - r0].copy_(z[r0:r1, :dim])
                 if gloo:
-                    dist.all_gather(list(gathered.chunk(world)), send)
+                    works.append(dist.all_gather(list(recvs[k].chunk(world)), sends[k], async_op=True))
                 else:
-                    dist.all_gather_into_tensor(gathered, send)
+                    works.append(dist.all_gather_into_tensor(recvs[k], sends[k], async_op=True))
+            for w_ in works:
+                w_.wait()
 
         for _ in range(warmup):
             step()
@@ -248,7 +265,8 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
         ms = s_ev.elapsed_time(e_ev) / steps
-        tile_ms = statistics.mean(a.elapsed_time(b) for a, b in tev) if plan.n_tile else 0.0
+        # per-kernel time only on one GPU (with N ranks the step is split into parts)
+        tile_ms = statistics.mean(a.elapsed_time(b) for a, b in tev) if (plan.n_tile and world == 1) else 0.0
         if world > 1:
             t = torch.tensor([ms, tile_ms], device=dev if not gloo else "cpu", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -288,6 +306,7 @@ def run_ours(args):
     tile_bytes = 8 * (tile_rows + 1) + plan.nnz_tile * (4 + s) + local_a.num_cols * dim * s + tile_rows * dim * 4
     full_bytes = 8 * (n + 1) + nnz * (4 + s) + n * dim * s + n * dim * 4
     achieved = tile_bytes / (tile_ms * 1e-3) / 1e9 if tile_ms > 0 else full_bytes / (ms * 1e-3) / 1e9
+    peak = peak * world  # whole-job HBM peak when N ranks share the step
     gather_bytes = sum_ncols * dim * s  # L2 -> SM X-row gather traffic of the tile path (diagnostic)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
