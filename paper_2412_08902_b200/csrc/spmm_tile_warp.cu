@@ -184,7 +184,9 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
   const uint32_t stage0 = smem_u32(wsmem + warp * kWarpSmemPerWarp);
   const uint32_t slab = stage0 + kWarpTileStages * kWarpStageBytes;
   const uint64_t keep = policy_evict_last();
-  const uint64_t once = policy_evict_first();
+  // plan data (indices, entries) is read once per feature slice: keep it for the window's
+  // other slice-warps (FS > 1), stream it otherwise
+  const uint64_t once = FS > 1 ? policy_evict_normal() : policy_evict_first();
   // gather lane mapping: lane (rg, v) copies 16-B vector v of rows rg*NI + it, it < NI, so its
   // NI gather indices are contiguous (NI/4 x 128-bit loads)
   const int gv = lane % SWV, rg = lane / SWV;
