@@ -343,7 +343,8 @@ def run_ours(args):
                      "kernel": "k_tile_warp (+ k_tile_warp_fixup)" if plan.n_tile else "k_spmm_scalar",
                      "kernel_ms": tile_ms, "algorithmic_bytes": tile_bytes,
                      "l2_gather_GBps": gather_bytes / (tile_ms * 1e-3) / 1e9 if tile_ms > 0 else None},
-        "gpu_launches": plan.launches_per_run(dim) * args.steps,
+        "gpu_launches": plan.launches_per_run(dim) * args.steps * (
+            max(1, int(os.environ.get("HCS_EXCHANGE_PARTS", "2"))) if world > 1 else 1),
         "clocks": clocks,
     }
     if e2e is not None:
