@@ -298,12 +298,10 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
     load_gidx(P3, Gnext);
     load_ent(EP1[0], EP1[1], Enext);
     load_ep(P2, EP2[0], EP2[1]);
-    // slab of P0: zero, scatter packed entries (bf16 value << 16 | swizzled byte offset)
+    // slab of P0 (zero on entry: cleared after the previous chunk's MMAs): scatter the packed
+    // entries (bf16 value << 16 | swizzled byte offset)
+    const int ne = (int)(EP0[1] - EP0[0]);
     {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) sts128_zero(slab + (lane + 32 * q) * 16);
-      __syncwarp();
-      const int ne = (int)(EP0[1] - EP0[0]);
 #pragma unroll
       for (int q = 0; q < kWarpEntRegs; ++q)
         if (lane + 32 * q < ne) sts16(slab + (Ecur[q] & 0x7FFu), Ecur[q] >> 16);
@@ -332,6 +330,16 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
       }
     }
     __syncwarp();
+    // clear the slab for the next chunk: undo this chunk's scatter (all entries in registers),
+    // or zero it fully when the chunk overflowed the register-held entries
+    if (ne <= 32 * kWarpEntRegs) {
+#pragma unroll
+      for (int q = 0; q < kWarpEntRegs; ++q)
+        if (lane + 32 * q < ne) sts16(slab + (Ecur[q] & 0x7FFu), 0u);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) sts128_zero(slab + (lane + 32 * q) * 16);
+    }
     // end of our part of the unit: Z (whole unit) or a scratch slot (split unit)
     const bool unit_done = P0.j + 1 == P0.nj;
     if (unit_done || P0.rem == 1) {
@@ -401,7 +409,10 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
     return false;
   };
 
-  // prologue
+  // prologue: the slab starts zeroed and is kept zero between chunks
+#pragma unroll
+  for (int q = 0; q < 4; ++q) sts128_zero(slab + (lane + 32 * q) * 16);
+  __syncwarp();
   const ChunkPos first = locate(chunk_ptr, T, FS, a);
   in_head = first.j != 0;
   Pos Q0 = mk(first), Q1 = Q0;
