@@ -81,6 +81,11 @@ int hcs_tile_plan(const int64_t* row_ptr, const int32_t* cond_cols, const void* 
 int hcs_spmm_scalar(const int64_t* row_ptr, const int32_t* col_idx, const void* values, int values_dtype,
                     int64_t n_rows, int32_t wh, const int32_t* win_list, int64_t n_list, const void* x, int x_dtype,
                     int64_t x_rows, int32_t dim, int64_t ldx, float* z, int64_t ldz, void* stream);
+/* K3 kernel choice: 0 auto (warp per window, col/val staged in shared memory, 32-byte X
+ * vectors when rows are 32-byte aligned and padded), 1 block per window (8 warps, one row
+ * each, lane groups reduced by a fixed shuffle tree), 2 warp per window with 16-byte vectors.
+ * Window heights > 31 always use variant 1.  Every variant is deterministic. */
+int hcs_set_scalar_variant(int variant);
 
 /* ---------------------------------------------------------------- K4
  * executors.py:111-141 tile_window for every window of a tile plan.  Engines

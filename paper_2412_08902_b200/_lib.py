@@ -16,7 +16,8 @@ import torch
 from .errors import InvariantError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhcspmm.so")
+# HCS_LIB_PATH: load an experimental build of the same library instead (tools/ only)
+LIB_PATH = os.environ.get("HCS_LIB_PATH") or os.path.join(_HERE, "libhcspmm.so")
 
 HCS_OK, HCS_EINVAL, HCS_EDIM, HCS_EINVARIANT, HCS_ECUDA, HCS_ENCCL = range(6)
 DTYPE_F32, DTYPE_BF16 = 0, 1
@@ -46,6 +47,7 @@ _SIGS = {
                                      I64, P, SZ, P]),
     "hcs_tile_scratch_floats": (ctypes.c_int, [ctypes.POINTER(I64)]),
     "hcs_set_tile_slice": (ctypes.c_int, [ctypes.c_int]),
+    "hcs_set_scalar_variant": (ctypes.c_int, [ctypes.c_int]),
     "hcs_gcn_tile": (ctypes.c_int, [P, I64, P, P, P, P, ctypes.c_int, I64, I32, P, ctypes.c_int, I64, I32, I64, P,
                                      I64, P, I32, P, I64, P, SZ, P]),
     "hcs_gcn_scalar": (ctypes.c_int, [P, P, P, ctypes.c_int, I64, I32, P, I64, P, ctypes.c_int, I64, I32, I64, P,

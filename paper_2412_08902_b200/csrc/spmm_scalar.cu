@@ -7,6 +7,9 @@
 // CSR indices/values stream with L2::evict_first; X rows are gathered with
 // L2::evict_last so the feature table stays resident in L2.
 #include "common.cuh"
+#include "mma_helpers.cuh"
+
+#include <algorithm>
 
 namespace hcs {
 
@@ -142,9 +145,258 @@ __global__ void __launch_bounds__(256) k_spmm_scalar(const int64_t* __restrict__
   }
 }
 
+// ---------------------------------------------------------------- warp-per-window kernel
+// K3 as launched for SpMM and the fused GCN layer (the block-per-window kernel above is kept
+// as a selectable variant).  Measured on C5 (R-MAT scale 24: 910 K scalar windows, 7.3 nnz
+// per row; profiles/r01_scalar_c5.txt) the block kernel is latency-bound: every row is a
+// chain row_ptr -> col/val -> X gather, 1.6 TB/s of DRAM.  Here one warp owns a window:
+//   1. lanes 0..nr load the window's row pointers in one coalesced load (rows are read back
+//      with shuffles); windows of <= kScalarCap entries stage all (col, value) pairs in
+//      shared memory with one batch of coalesced loads -- one latency for the whole window;
+//   2. a row of X is covered by L lanes of VB-byte vectors (VB = 32: 256-bit LDG, 16 bf16
+//      per lane, so a 128-feature row is 8 lanes, and the warp's G = 32 / L lane groups work
+//      on G different rows at once: each row is summed by one group in CSR order, U gathers
+//      in flight per group, no cross-lane reduction);
+//   3. windows with more entries (long rows) are walked row by row with the whole warp: the
+//      G groups take entries k = g (mod G) and are combined by a fixed shuffle tree.
+// Both orders are fixed, so results are run-to-run deterministic, and the fused GCN
+// epilogue (FUSED) aggregates with exactly the same code as the plain SpMM.
+constexpr int kScalarCap = 512;
+constexpr int kScalarWarps = 8;
+constexpr int kScalarZsLd = kFusedMaxDim + 4;  // fused: per-warp window rows in shared memory
+#ifndef HCS_SCALAR_U32
+#define HCS_SCALAR_U32 3  // entries in flight per lane group (32-byte vectors)
+#endif
+#ifndef HCS_SCALAR_MINB
+#define HCS_SCALAR_MINB 4  // resident blocks per SM the register budget is sized for
+#endif
+
+#define HCS_TRY(call)                  \
+  do {                                 \
+    const int _rc = (call);            \
+    if (_rc != HCS_OK) return _rc;     \
+  } while (0)
+
+__device__ __forceinline__ int64_t ld_stream_s64(const int64_t* p, uint64_t pol) {
+  int64_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(pol));
+  return r;
+}
+
+template <int VB>
+struct XRaw;
+template <>
+struct XRaw<16> {
+  uint32_t w[4];
+  __device__ __forceinline__ void load(const void* p, uint64_t pol) {
+    asm volatile("ld.global.nc.L2::cache_hint.v4.b32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                 : "l"(p), "l"(pol));
+  }
+  __device__ __forceinline__ void zero() { w[0] = w[1] = w[2] = w[3] = 0u; }
+};
+template <>
+struct XRaw<32> {
+  uint32_t w[8];
+  __device__ __forceinline__ void load(const void* p, uint64_t pol) {
+    asm volatile("ld.global.nc.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+                 : "l"(p), "l"(pol));
+  }
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i] = 0u;
+  }
+};
+
+template <typename XT, int VB>
+__device__ __forceinline__ void fma_raw(float* acc, const uint32_t* w, float a) {
+  if (sizeof(XT) == 2) {
+#pragma unroll
+    for (int i = 0; i < VB / 4; ++i) {
+      acc[2 * i] = fmaf(a, bf16lo(w[i]), acc[2 * i]);
+      acc[2 * i + 1] = fmaf(a, bf16hi(w[i]), acc[2 * i + 1]);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < VB / 4; ++i) acc[i] = fmaf(a, __uint_as_float(w[i]), acc[i]);
+  }
+}
+
+template <typename XT, typename VT, int VB, int U, bool FUSED>
+__global__ void __launch_bounds__(kScalarWarps * 32, FUSED ? 1 : HCS_SCALAR_MINB)
+    k_spmm_scalar_w(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col, const VT* __restrict__ val,
+                    int64_t n_rows, int wh, const int32_t* __restrict__ win_list, int64_t n_list,
+                    const XT* __restrict__ x, int dim, int64_t ldx, float* __restrict__ z, int64_t ldz,
+                    const float* __restrict__ mw, int d_out, float* __restrict__ out, int64_t ldo) {
+  constexpr int E = VB / (int)sizeof(XT);  // features per lane vector
+  extern __shared__ __align__(16) uint8_t wsm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int32_t* scol = reinterpret_cast<int32_t*>(wsm) + warp * kScalarCap;
+  float* sval = reinterpret_cast<float*>(wsm + kScalarWarps * kScalarCap * 4) + warp * kScalarCap;
+  float* zs = reinterpret_cast<float*>(wsm + kScalarWarps * kScalarCap * 8) + warp * (kFusedMaxRows * kScalarZsLd);
+  const int64_t gw = (int64_t)blockIdx.x * kScalarWarps + warp;
+  if (gw >= n_list) return;
+  const uint64_t keep = policy_evict_last();
+  const uint64_t strm = stream_policy();
+  const int64_t rs = (int64_t)win_list[gw] * wh;
+  const int nr = (int)(n_rows - rs < wh ? n_rows - rs : wh);
+  const int64_t rp = lane <= nr ? ld_stream_s64(row_ptr + rs + lane, strm) : 0;
+  const int64_t e0 = __shfl_sync(0xffffffffu, rp, 0), e1 = __shfl_sync(0xffffffffu, rp, nr);
+  const bool staged = e1 - e0 <= kScalarCap;
+  const int32_t* cw = col + e0;  // the window's entries
+  const VT* vw = val + e0;
+  if (staged) {
+    const int n = (int)(e1 - e0);
+#pragma unroll
+    for (int q = 0; q < kScalarCap / 32; ++q) {
+      const int i = lane + 32 * q;
+      if (i < n) {
+        scol[i] = ld_stream_s32(cw + i, strm);
+        sval[i] = load_val(vw + i, strm);
+      }
+    }
+    __syncwarp();
+  }
+  const int nvec_total = (dim + E - 1) / E;
+  const int64_t ldxb = ldx * (int64_t)sizeof(XT);
+  auto store_row = [&](int r, int f0, const float (&acc)[E]) {
+    if (z != nullptr) {
+      float* zr = z + (rs + r) * ldz + f0;
+      if (f0 + E <= dim) {
+#pragma unroll
+        for (int i = 0; i < E; i += 4)
+          reinterpret_cast<float4*>(zr)[i / 4] = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i)
+          if (f0 + i < dim) zr[i] = acc[i];
+      }
+    }
+    if (FUSED) {
+#pragma unroll
+      for (int i = 0; i < E; ++i)
+        if (f0 + i < dim) zs[r * kScalarZsLd + f0 + i] = acc[i];
+    }
+  };
+  for (int fs = 0; fs < nvec_total; fs += 32) {
+    const int L = min(32, nvec_total - fs);
+    const int G = 32 / L;
+    const int g = lane / L, v = lane - g * L;
+    const int f0 = (fs + v) * E;
+    const char* xb = reinterpret_cast<const char*>(x + f0);
+    if (staged) {
+      for (int r0 = 0; r0 < nr; r0 += G) {
+        const int r = r0 + g;
+        // entry offsets relative to e0 (a window holds < 2^31 entries)
+        const int kb = (int)(__shfl_sync(0xffffffffu, rp, min(r, 31)) - e0);
+        const int ke = (int)(__shfl_sync(0xffffffffu, rp, min(r + 1, 31)) - e0);
+        if (g < G && r < nr) {
+          float acc[E];
+#pragma unroll
+          for (int i = 0; i < E; ++i) acc[i] = 0.f;
+          for (int k = kb; k < ke; k += U) {
+            XRaw<VB> xv[U];
+            float a[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int kk = k + u;
+              a[u] = 0.f;
+              xv[u].zero();
+              if (kk < ke) {
+                a[u] = sval[kk];
+                xv[u].load(xb + (int64_t)scol[kk] * ldxb, keep);
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) fma_raw<XT, VB>(acc, xv[u].w, a[u]);
+          }
+          store_row(r, f0, acc);
+        }
+      }
+    } else {
+      for (int r = 0; r < nr; ++r) {
+        const int kb = (int)(__shfl_sync(0xffffffffu, rp, r) - e0);
+        const int ke = (int)(__shfl_sync(0xffffffffu, rp, r + 1) - e0);
+        float acc[E];
+#pragma unroll
+        for (int i = 0; i < E; ++i) acc[i] = 0.f;
+        if (g < G) {
+          for (int k = kb + g; k < ke; k += U * G) {
+            XRaw<VB> xv[U];
+            float a[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int kk = k + u * G;
+              a[u] = 0.f;
+              xv[u].zero();
+              if (kk < ke) {
+                a[u] = load_val(vw + kk, strm);
+                xv[u].load(xb + (int64_t)ld_stream_s32(cw + kk, strm) * ldxb, keep);
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) fma_raw<XT, VB>(acc, xv[u].w, a[u]);
+          }
+        }
+        // fixed-order tree over the G lane groups
+        for (int sft = 1; sft < G; sft <<= 1) {
+#pragma unroll
+          for (int i = 0; i < E; ++i) {
+            const float o = __shfl_down_sync(0xffffffffu, acc[i], sft * L);
+            if ((g % (2 * sft)) == 0 && g + sft < G) acc[i] += o;
+          }
+        }
+        if (g == 0) store_row(r, f0, acc);
+      }
+    }
+  }
+  if (FUSED) {
+    // out[rs + r, j] = sum_k zs[r][k] * M[k][j], k ascending (fp32 FMA)
+    __syncwarp();
+    for (int j = lane; j < d_out; j += 32) {
+      for (int r = 0; r < nr; ++r) {
+        float o = 0.f;
+        for (int k = 0; k < dim; ++k) o = fmaf(zs[r * kScalarZsLd + k], __ldg(mw + (int64_t)k * d_out + j), o);
+        out[(rs + r) * ldo + j] = o;
+      }
+    }
+  }
+}
+
+static int g_scalar_variant = 0;  // 0 auto (warp-per-window), 1 block-per-window kernel, 2 warp kernel with 16-B vectors
+
+template <bool FUSED, typename XT, typename VT>
+static int launch_scalar_w(const int64_t* row_ptr, const int32_t* col, const VT* val, int64_t n_rows, int wh,
+                           const int32_t* win_list, int64_t n_list, const XT* x, int dim, int64_t ldx, float* z,
+                           int64_t ldz, bool v32, cudaStream_t st, const float* mw = nullptr, int d_out = 0,
+                           float* out = nullptr, int64_t ldo = 0) {
+  const unsigned grid = (unsigned)((n_list + kScalarWarps - 1) / kScalarWarps);
+  const int smem = kScalarWarps * (kScalarCap * 8 + (FUSED ? kFusedMaxRows * kScalarZsLd * 4 : 0));
+  auto k = v32 ? k_spmm_scalar_w<XT, VT, 32, HCS_SCALAR_U32, FUSED> : k_spmm_scalar_w<XT, VT, 16, 4, FUSED>;
+  HCS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  k<<<grid, kScalarWarps * 32, smem, st>>>(row_ptr, col, val, n_rows, wh, win_list, n_list, x, dim, ldx, z, ldz, mw,
+                                            d_out, out, ldo);
+  return HCS_OK;
+}
+
+// 32-byte X vectors when every row slice is 32-byte aligned and padded
+static bool scalar_v32(const void* x, int x_dtype, int64_t ldx, int dim) {
+  const int xs = x_dtype == HCS_DTYPE_BF16 ? 2 : 4, e32 = 32 / xs;
+  return g_scalar_variant == 0 && ((uintptr_t)x & 31) == 0 && (ldx * xs) % 32 == 0 &&
+         ldx >= ((dim + e32 - 1) / e32) * e32;
+}
+
 }  // namespace hcs
 
 using namespace hcs;
+
+// Scalar-path kernel choice (experiments): 0 auto, 1 block-per-window, 2 warp-per-window with 16-B vectors.
+extern "C" int hcs_set_scalar_variant(int variant) {
+  HCS_REQUIRE(variant >= 0 && variant <= 2, HCS_EINVAL, "scalar variant must be 0, 1 or 2 (got %d)", variant);
+  g_scalar_variant = variant;
+  return HCS_OK;
+}
 
 extern "C" int hcs_spmm_scalar(const int64_t* row_ptr, const int32_t* col_idx, const void* values, int values_dtype,
                                int64_t n_rows, int32_t wh, const int32_t* win_list, int64_t n_list, const void* x,
@@ -161,6 +413,23 @@ extern "C" int hcs_spmm_scalar(const int64_t* row_ptr, const int32_t* col_idx, c
   HCS_REQUIRE(((uintptr_t)x & 15) == 0 && ((uintptr_t)z & 15) == 0, HCS_EINVAL, "x/z must be 16-byte aligned");
   if (n_list == 0) return HCS_OK;
   cudaStream_t st = as_stream(stream);
+  if (g_scalar_variant != 1 && wh <= 31) {
+    const bool v32 = scalar_v32(x, x_dtype, ldx, dim);
+    if (x_dtype == HCS_DTYPE_BF16 && values_dtype == HCS_DTYPE_BF16)
+      HCS_TRY(launch_scalar_w<false>(row_ptr, col_idx, (const __nv_bfloat16*)values, n_rows, wh, win_list, n_list,
+                                     (const __nv_bfloat16*)x, dim, ldx, z, ldz, v32, st));
+    else if (x_dtype == HCS_DTYPE_BF16 && values_dtype == HCS_DTYPE_F32)
+      HCS_TRY(launch_scalar_w<false>(row_ptr, col_idx, (const float*)values, n_rows, wh, win_list, n_list,
+                                     (const __nv_bfloat16*)x, dim, ldx, z, ldz, v32, st));
+    else if (x_dtype == HCS_DTYPE_F32 && values_dtype == HCS_DTYPE_F32)
+      HCS_TRY(launch_scalar_w<false>(row_ptr, col_idx, (const float*)values, n_rows, wh, win_list, n_list,
+                                     (const float*)x, dim, ldx, z, ldz, v32, st));
+    else
+      return set_error(HCS_EINVAL, "unsupported dtype combination x=%d values=%d", x_dtype, values_dtype);
+    HCS_LAUNCH_CHECK("k_spmm_scalar_w");
+    (void)x_rows;
+    return HCS_OK;
+  }
   dim3 grid((unsigned)n_list);
   if (x_dtype == HCS_DTYPE_BF16 && values_dtype == HCS_DTYPE_BF16)
     k_spmm_scalar<__nv_bfloat16, __nv_bfloat16, false><<<grid, 256, 0, st>>>(
@@ -203,6 +472,20 @@ extern "C" int hcs_gcn_scalar(const int64_t* row_ptr, const int32_t* col_idx, co
   HCS_REQUIRE(((uintptr_t)x & 15) == 0, HCS_EINVAL, "x must be 16-byte aligned");
   if (n_list == 0) return HCS_OK;
   cudaStream_t st = as_stream(stream);
+  if (g_scalar_variant != 1) {  // same aggregation kernel (and order) as hcs_spmm_scalar
+    const bool v32 = scalar_v32(x, x_dtype, ldx, dim);
+    if (x_dtype == HCS_DTYPE_BF16 && values_dtype == HCS_DTYPE_BF16)
+      HCS_TRY(launch_scalar_w<true>(row_ptr, col_idx, (const __nv_bfloat16*)values, n_rows, wh, win_list, n_list,
+                                    (const __nv_bfloat16*)x, dim, ldx, z, ldz, v32, st, m, d_out, out, ldo));
+    else if (x_dtype == HCS_DTYPE_F32 && values_dtype == HCS_DTYPE_F32)
+      HCS_TRY(launch_scalar_w<true>(row_ptr, col_idx, (const float*)values, n_rows, wh, win_list, n_list,
+                                    (const float*)x, dim, ldx, z, ldz, v32, st, m, d_out, out, ldo));
+    else
+      return set_error(HCS_EINVAL, "unsupported dtype combination x=%d values=%d", x_dtype, values_dtype);
+    HCS_LAUNCH_CHECK("k_spmm_scalar_w<fused>");
+    (void)x_rows;
+    return HCS_OK;
+  }
   dim3 grid((unsigned)n_list);
   if (x_dtype == HCS_DTYPE_BF16 && values_dtype == HCS_DTYPE_BF16)
     k_spmm_scalar<__nv_bfloat16, __nv_bfloat16, true><<<grid, 256, 0, st>>>(

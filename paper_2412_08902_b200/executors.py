@@ -442,3 +442,15 @@ def set_tile_engine(engine: str = "auto") -> None:
     if engine not in _ENGINES:
         raise ValueError(f"engine must be one of {sorted(_ENGINES)}, got {engine!r}")
     _lib.call("hcs_set_tile_engine", _ENGINES[engine])
+
+
+_SCALAR_VARIANTS = {"auto": 0, "block": 1, "warp16": 2}
+
+
+def set_scalar_variant(variant: str = "auto") -> None:
+    """Select the CUDA-core (K3) kernel: "auto" (warp per window, col/val staged in shared
+    memory, 32-byte X vectors when the operand allows), "block" (block per window, one warp
+    per row with a fixed shuffle tree), "warp16" (warp per window, 16-byte vectors)."""
+    if variant not in _SCALAR_VARIANTS:
+        raise ValueError(f"variant must be one of {sorted(_SCALAR_VARIANTS)}, got {variant!r}")
+    _lib.call("hcs_set_scalar_variant", _SCALAR_VARIANTS[variant])

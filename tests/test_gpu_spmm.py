@@ -257,3 +257,40 @@ def test_host_pipelined_path(cuda_ok):
     assert np.abs(host.z.data - d).max() <= 1e-5 * np.abs(d).max()
     assert orc.max_rel_err(host.z.data, orc.spmm_exact(a, x)) <= BF16_TOL
     assert host.stats == dev.stats
+
+
+@pytest.mark.parametrize("variant", ["auto", "block", "warp16"])
+@pytest.mark.parametrize("precision", ["bf16", "tf32"])
+def test_scalar_variants(cuda_ok, variant, precision):
+    """Every K3 kernel variant == the exact product within the precision's tolerance, on
+    windows below and above the shared-memory staging cap (256 entries), short last
+    windows, odd window heights and dims that are not multiples of the vector width;
+    run-to-run bitwise identical."""
+    from paper_2412_08902_b200.executors import set_scalar_variant
+
+    tol = BF16_TOL if precision == "bf16" else 1e-3
+    rng = np.random.default_rng(7)
+    # rows 0..159: 1-8 nnz; rows 160..239: 40-90 nnz (windows over the cap); 245 rows total
+    rows, cols = [], []
+    for r in range(245):
+        k = int(rng.integers(1, 9)) if r < 160 else int(rng.integers(40, 90))
+        if r % 37 == 5:
+            k = 0  # empty rows
+        cs = rng.choice(900, size=k, replace=False)
+        rows += [r] * k
+        cols += list(cs)
+    a = orc.from_coo(245, 900, rows, cols, rng.uniform(-1, 1, len(rows)))
+    try:
+        set_scalar_variant(variant)
+        for wh in (16, 7):
+            for dim in (1, 24, 64, 100, 128, 200):
+                x = orc.random_dense(900, dim, seed=dim)
+                ws = hc.partition(to_hc(a), window_height=wh)
+                asg = Assignment.uniform(len(ws), Path.SCALAR)
+                r1 = hc.spmm_hybrid(ws, asg, hc.DenseMatrix(x), precision=precision)
+                exact = orc.spmm_exact(a, x)
+                assert orc.max_rel_err(r1.z.data, exact) <= tol, (wh, dim)
+                r2 = hc.spmm_hybrid(ws, asg, hc.DenseMatrix(x), precision=precision)
+                assert np.array_equal(r1.z.data, r2.z.data)
+    finally:
+        set_scalar_variant("auto")

@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <vector>
 #include <random>
+#include <cstdlib>
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s: %s\n", #x, cudaGetErrorString(e)); exit(1);} } while (0)
 
 template <int MODE>
@@ -128,12 +129,13 @@ void run256(const uint4* tbl, const int* idx, long m, uint32_t* out) {
   }
 }
 
-int main() {
-  const long R = 232965;
+int main(int argc, char** argv) {
+  const long R = argc > 1 ? atol(argv[1]) : 232965;
   const long M = 115374529 / 4;  // rows gathered per launch (a quarter of C2's nnz)
   std::mt19937_64 rng(1);
   std::vector<int> h(M);
   for (long i = 0; i < (1 << 22); ++i) h[i] = (int)(rng() % R);
+  printf("table rows %ld (%.1f MB)\n", R, R * 256 / 1e6);
   int* idx;
   uint4* tbl;
   uint32_t* out;
