@@ -45,6 +45,9 @@ def parse():
     p.add_argument("--dim", type=int, default=128)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", choices=["c2", "c1", "c3", "c4", "c5"], default="c2")
+    p.add_argument("--graph", choices=["powerlaw", "community"], default="powerlaw",
+                   help="Reddit-shaped input for c2/c3/c4: structureless Chung-Lu (default) or 41 planted "
+                        "communities with scrambled ids (secondary data point)")
     p.add_argument("--precision", default="bf16")
     p.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU-baseline sampling")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -138,11 +141,14 @@ def dist_setup(args):
     return world, rank, local
 
 
-def make_graph(cfg: str, seed: int):
+def make_graph(cfg: str, seed: int, graph: str = "powerlaw"):
     from paper_2412_08902_b200 import graphgen
     from paper_2412_08902_b200.gnn import normalize_adj
 
-    if cfg == "c2":
+    if cfg == "c2" and graph == "community":
+        adj = graphgen.reddit_community(seed=seed)
+        name = "C2 reddit-shaped power law with 41 planted communities (80% intra, ids scrambled), gcn-normalised"
+    elif cfg == "c2":
         adj = graphgen.reddit_shaped(seed=seed)
         name = "C2 reddit-shaped power law (Chung-Lu gamma=2.3), gcn-normalised"
     elif cfg == "c1":
@@ -173,7 +179,7 @@ def run_ours(args):
     world, rank, local = dist_setup(args)
     dev = torch.device("cuda", torch.cuda.current_device())
     t0 = time.perf_counter()
-    adj, a, wl_name = make_graph(args.config, args.seed)
+    adj, a, wl_name = make_graph(args.config, args.seed, args.graph)
     torch.cuda.synchronize()
     t_gen = time.perf_counter() - t0
     n, nnz = a.num_rows, a.nnz
@@ -396,7 +402,7 @@ def run_c3(args):
 
     world, rank, local = dist_setup(args)
     dev = torch.device("cuda", torch.cuda.current_device())
-    adj, a, wl_name = make_graph("c2", args.seed)
+    adj, a, wl_name = make_graph("c2", args.seed, args.graph)
     n, nnz = a.num_rows, a.nnz
     shard = None
     if world > 1:
@@ -460,7 +466,7 @@ def run_c4(args):
     from paper_2412_08902_b200.matrices import Graph
 
     world, rank, local = dist_setup(args)
-    adj, a, wl_name = make_graph("c2", args.seed)
+    adj, a, wl_name = make_graph("c2", args.seed, args.graph)
     n = a.num_rows
     g = Graph(n, adj, True)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]

@@ -7,6 +7,8 @@ graphs, so these are vectorised on the device with a seeded torch.Generator
 
   reddit_shaped(): capped Chung-Lu power law, gamma 2.3, n = 232,965, ~114.6M
                    directed nnz before gcn self-loops (C2/C3/C4)
+  reddit_community(): the same shape with 41 planted communities, scrambled ids
+                   (secondary C2/C4 input: the locality LOA is meant to recover)
   cora_shaped():   n = 2,708, ~10.5K directed nnz (C1)
   rmat():          R-MAT (a,b,c,d) = (0.57, 0.19, 0.19, 0.05) (C5)
 All graphs: self-loops dropped, symmetrised, deduplicated, unit values.
@@ -81,6 +83,59 @@ def reddit_shaped(seed: int = 0, device="cuda") -> DeviceCsr:
     ~114.6M directed nnz before self-loops."""
     return chung_lu_device(REDDIT_N, REDDIT_TARGET_NNZ / REDDIT_N, seed=seed, oversample=1.03,
                            device=device)
+
+
+def community_power_law(n: int, avg_deg: float, communities: int, p_in: float = 0.8, seed: int = 0,
+                        gamma: float = 2.3, i0: float | None = None, oversample: float = 1.03,
+                        device="cuda") -> DeviceCsr:
+    """Degree-corrected planted partition: Chung-Lu weights as chung_lu_device, every vertex
+    in one of `communities` groups (uniform), a fraction p_in of the edges drawn with both
+    endpoints inside one community (community chosen by weight mass, endpoints by weight
+    within it), the rest drawn globally.  Vertex ids are a random permutation, so rows carry
+    no locality until a layout pass (LOA, C4) recovers it."""
+    g = _gen(seed, device)
+    if i0 is None:
+        i0 = max(1.0, n * 350.7 / REDDIT_N)
+    i = torch.arange(n, device=device, dtype=torch.float64)
+    w = (1.0 + i / i0) ** (-1.0 / (gamma - 1.0))
+    comm = torch.randint(0, communities, (n,), generator=g, device=device)
+    order = torch.argsort(comm * n + torch.arange(n, device=device))  # vertices grouped by community
+    cw = torch.cumsum(w[order], 0)
+    total = cw[-1]
+    cnt = torch.bincount(comm, minlength=communities)
+    cend = torch.cumsum(cnt, 0)  # community c owns order[cend[c]-cnt[c] : cend[c]]
+    mass_end = cw[cend - 1]
+    mass_start = mass_end - torch.bincount(comm, weights=w, minlength=communities)
+    ccdf = torch.cumsum(mass_end - mass_start, 0) / total
+    gcdf = torch.cumsum(w, 0) / total
+    perm = torch.randperm(n, generator=g, device=device)
+    pairs = int(n * avg_deg / 2 * oversample)
+    out_u, out_v = [], []
+    chunk = 1 << 25
+    for s in range(0, pairs, chunk):
+        m = min(chunk, pairs - s)
+        intra = torch.rand(m, generator=g, device=device) < p_in
+        c = torch.clamp(torch.searchsorted(ccdf, torch.rand(m, generator=g, device=device, dtype=torch.float64)),
+                        max=communities - 1)
+        lo, span = mass_start[c], mass_end[c] - mass_start[c]
+        ru = lo + torch.rand(m, generator=g, device=device, dtype=torch.float64) * span
+        rv = lo + torch.rand(m, generator=g, device=device, dtype=torch.float64) * span
+        ui = order[torch.clamp(torch.searchsorted(cw, ru), max=n - 1)]
+        vi = order[torch.clamp(torch.searchsorted(cw, rv), max=n - 1)]
+        gu = torch.clamp(torch.searchsorted(gcdf, torch.rand(m, generator=g, device=device, dtype=torch.float64)),
+                         max=n - 1)
+        gv = torch.clamp(torch.searchsorted(gcdf, torch.rand(m, generator=g, device=device, dtype=torch.float64)),
+                         max=n - 1)
+        out_u.append(perm[torch.where(intra, ui, gu)])
+        out_v.append(perm[torch.where(intra, vi, gv)])
+    return symmetric_from_pairs(n, torch.cat(out_u), torch.cat(out_v))
+
+
+def reddit_community(seed: int = 0, device="cuda") -> DeviceCsr:
+    """C2/C4 secondary input: Reddit-shaped (n = 232,965, ~114.6M directed nnz) with 41
+    planted communities (Reddit's class count), 80% intra-community edges, scrambled ids."""
+    return community_power_law(REDDIT_N, REDDIT_TARGET_NNZ / REDDIT_N, 41, seed=seed, oversample=1.25,
+                               device=device)
 
 
 def cora_shaped(seed: int = 0, device="cuda") -> DeviceCsr:

@@ -39,6 +39,9 @@ rls = rl[rows_s]
 print(json.dumps({"scalar_win_nnz_max": int(wn.max()), "win_gt256": int((wn > 256).sum()), "win_gt4096": int((wn > 4096).sum()),
                   "nnz_in_gt256": int(wn[wn > 256].sum()), "row_nnz_max": int(rls.max()), "rows_gt1000": int((rls > 1000).sum()),
                   "rows_gt10000": int((rls > 10000).sum())}), flush=True)
+ept = (plan.ent_ptr[1:] - plan.ent_ptr[:-1]).float()
+print(json.dumps({"chunks": plan.nchunks, "ent_per_chunk": float(ept.mean()), "chunks_gt128": int((ept > 128).sum()),
+                  "ent_in_gt128": int(ept[ept > 128].sum()), "ent_max": int(ept.max())}), flush=True)
 if os.environ.get("C5_STATS_ONLY"):
     sys.exit(0)
 x = graphgen.dense_features(a.num_rows, dim, seed=1)
