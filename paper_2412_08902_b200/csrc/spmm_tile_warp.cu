@@ -275,6 +275,9 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
       const int64_t i = e0 + lane + 32 * q;
       e[q] = i < e1 ? ld_plan_u32(ent + i, once) : 0u;
     }
+    // a dense chunk's remaining entries: pull them into L2 one chunk ahead (lane = 128-B line)
+    const int64_t ov = e0 + 32 * kWarpEntRegs + 32 * lane;
+    if (ov < e1) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(ent + ov));
   };
 
   float acc[SWV][4];
@@ -305,9 +308,18 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
 #pragma unroll
       for (int q = 0; q < kWarpEntRegs; ++q)
         if (lane + 32 * q < ne) sts16(slab + (Ecur[q] & 0x7FFu), Ecur[q] >> 16);
-      for (int i = 32 * kWarpEntRegs + lane; i < ne; i += 32) {  // rare: > 128 entries in a chunk
-        const uint32_t w = ld_plan_u32(ent + EP0[0] + i, once);
-        sts16(slab + (w & 0x7FFu), w >> 16);
+      // dense chunks (> 128 entries; e.g. windows after LOA): the remaining entries in
+      // batches of 8 loads per lane, so one memory latency covers 256 entries
+      for (int i0 = 32 * kWarpEntRegs; i0 < ne; i0 += 32 * 8) {
+        uint32_t w[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = i0 + 32 * u + lane;
+          w[u] = i < ne ? ld_plan_u32(ent + EP0[0] + i, once) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (i0 + 32 * u + lane < ne) sts16(slab + (w[u] & 0x7FFu), w[u] >> 16);
       }
     }
     cp_async_wait<2>();  // P0's gathers landed (P1, P2 may still be in flight)
