@@ -49,6 +49,8 @@ def parse():
                    help="Reddit-shaped input for c2/c3/c4: structureless Chung-Lu (default) or 41 planted "
                         "communities with scrambled ids (secondary data point)")
     p.add_argument("--precision", default="bf16")
+    p.add_argument("--selector", default=None,
+                   help="selector model JSON (e.g. from `cli train-selector`); default: the reference's shipped model")
     p.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU-baseline sampling")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
@@ -58,6 +60,11 @@ def parse():
 
 
 # ----------------------------------------------------------------------------- helpers
+# L2 -> SM random-row gather ceiling measured on B200 (profiles/r01_probe_ldg_registers.txt:
+# 256-B rows from a 60 MB L2-resident table, 48 warps/SM, 19.47 TB/s)
+GATHER_PEAK_GBPS = 19470.0
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -192,7 +199,8 @@ def run_ours(args):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
     ws = hc.partition(local_a)
-    asg = hc.classify_windows(hc.default_model(), ws)
+    sel_model = hc.default_model() if args.selector is None else hc.load_model(args.selector)
+    asg = hc.classify_windows(sel_model, ws)
     ev1.record()
     torch.cuda.synchronize()
     t_partition_ms = ev0.elapsed_time(ev1)
@@ -204,6 +212,7 @@ def run_ours(args):
     ncols = ws.ncols()
     plan_bytes = plan.gidx.numel() * 4 + plan.ent.numel() * 4 + local_a.nnz * 6 * int(plan.scalar_list.numel() > 0)
     sum_ncols = int(ncols.sum())
+    tile_ncols = int(ncols[plan.tile_list.long()].sum()) if plan.n_tile else 0
     codes = ws.codes
 
     def measure(dim, steps, warmup, with_e2e):
@@ -316,10 +325,10 @@ def run_ours(args):
     full_bytes = 8 * (n + 1) + nnz * (4 + s) + n * dim * s + n * dim * 4
     achieved = tile_bytes / (tile_ms * 1e-3) / 1e9 if tile_ms > 0 else full_bytes / (ms * 1e-3) / 1e9
     peak = peak * world  # whole-job HBM peak when N ranks share the step
-    gather_bytes = sum_ncols * dim * s  # L2 -> SM X-row gather traffic of the tile path (diagnostic)
+    gather_bytes = tile_ncols * dim * s  # L2 -> SM X-row gather traffic of the tile path
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath) and world == 1:
+    if os.path.exists(tpath) and world == 1 and args.graph == "powerlaw" and args.selector is None:
         with open(tpath) as fh:
             tr = json.load(fh).get(f"{args.config}_dim{dim}")
         traffic = tr
@@ -342,6 +351,7 @@ def run_ours(args):
             "tile_windows": plan.stats.windows_tile, "scalar_windows": plan.stats.windows_scalar,
             "sum_ncols": sum_ncols, "aggregate_ci": local_a.nnz / max(sum_ncols, 1),
             "parallelism": f"row-window shards x{world}" if world > 1 else "single GPU",
+            "selector": "reference default (selector_default.json)" if args.selector is None else args.selector,
             "l2_policy": (f"inputs larger than L2 (tile plan + CSR stream {plan_bytes / 1e9:.2f} GB read once per "
                           f"step, > 126 MB L2); X ({n * dim * 2 / 1e6:.0f} MB) gathered with L2 evict_last hints"),
             "preprocess_ms": {"graph_gen_s": t_gen, "partition_select": t_partition_ms, "tile_plan": t_plan_ms},
@@ -351,7 +361,18 @@ def run_ours(args):
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "kernel": "k_tile_warp (+ k_tile_warp_fixup)" if plan.n_tile else "k_spmm_scalar",
                      "kernel_ms": tile_ms, "algorithmic_bytes": tile_bytes,
-                     "l2_gather_GBps": gather_bytes / (tile_ms * 1e-3) / 1e9 if tile_ms > 0 else None},
+                     "l2_gather_GBps": gather_bytes / (tile_ms * 1e-3) / 1e9 if tile_ms > 0 else None,
+                     # the bound that applies to the tile path: every condensed column
+                     # moves an X row L2 -> SM.  Ceiling measured by tools/probe/ldg_reg.cu (random rows
+                     # from an L2-resident table); LSU floor = 12 SM cycles per 512 B staged through
+                     # shared memory (cp.async 8 + ldmatrix 4) at the measured SM clock
+                     "gather": {"achieved_GBps": gather_bytes / (tile_ms * 1e-3) / 1e9 if tile_ms > 0 else None,
+                                "peak_GBps": GATHER_PEAK_GBPS,
+                                "frac": (gather_bytes / (tile_ms * 1e-3) / 1e9 / GATHER_PEAK_GBPS) if tile_ms > 0
+                                else None,
+                                "lsu_floor_ms": gather_bytes / 512 * 12 / (148 * (clocks or {}).get("sm_mhz", 1965)
+                                                                          * 1e6) * 1e3
+                                if gather_bytes else None}},
         "gpu_launches": plan.launches_per_run(dim) * args.steps * (
             max(1, int(os.environ.get("HCS_EXCHANGE_PARTS", "2"))) if world > 1 else 1),
         "clocks": clocks,
@@ -365,7 +386,7 @@ def run_ours(args):
             fb = 8 * (n + 1) + nnz * (4 + s) + n * d * s + n * d * 4
             sweep[str(d)] = {"ms": m2, "gflops": 2.0 * nnz * d / (m2 * 1e-3) / 1e9,
                              "hbm_frac": fb / (m2 * 1e-3) / 1e9 / peak,
-                             "l2_gather_GBps": sum_ncols * d * s / (t2 * 1e-3) / 1e9 if t2 else None}
+                             "l2_gather_GBps": tile_ncols * d * s / (t2 * 1e-3) / 1e9 if t2 else None}
         out["dims"] = sweep
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(adj, dim, args.cpu_budget)
