@@ -17,4 +17,4 @@ from .windows import (  # noqa: F401
     TILE_COLS, TILE_DIM, WINDOW_HEIGHT, RowWindow, WindowFeatures, WindowSet, features, partition,
     tile_count, total_rows,
 )
-from .selector import SelectorModel, classify, classify_windows, default_model, load_model  # noqa: F401
+from .selector import SelectorModel, b200_model, classify, classify_windows, default_model, load_model  # noqa: F401

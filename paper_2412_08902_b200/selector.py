@@ -3,8 +3,8 @@
 Decisions for a device WindowSet are computed on the GPU in IEEE fp64 with
 round-to-nearest intrinsics (csrc/partition.cu k_features / k_classify), so
 they are bit-identical to the reference's Python-float evaluation of
-((w_ncols*zn) + (w_density*zd)) + bias.  Training (selector.py:67-257) is
-offline tooling and out of scope.
+((w_ncols*zn) + (w_density*zd)) + bias.  Training (selector.py:67-257) lives in
+selector_train.py (B200 timing provider); b200_model() is the opt-in result.
 """
 
 from __future__ import annotations
@@ -22,6 +22,7 @@ from .executors import Assignment, Path
 from .windows import WindowFeatures, WindowSet, _selector_doubles, features
 
 _DATA = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data", "selector_default.json")
+_DATA_B200 = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data", "selector_b200.json")
 
 
 @dataclass(frozen=True)
@@ -91,6 +92,14 @@ def load_model(path: str) -> SelectorModel:
 def default_model() -> SelectorModel:
     """selector.py:284-288: the shipped weights (data/selector_default.json)."""
     return load_model(_DATA)
+
+
+@lru_cache(maxsize=1)
+def b200_model() -> SelectorModel:
+    """Opt-in model trained on measured B200 timings of this repo's kernels (cli
+    train-selector --grid b200 --dim 128; selector_train.py).  Not the default: the
+    reference's shipped model keeps window decisions bit-exact with rowwin."""
+    return load_model(_DATA_B200)
 
 
 def save_model(model: SelectorModel, path: str, provenance: dict | None = None) -> None:

@@ -89,3 +89,13 @@ def test_b200_provider_and_cli(cuda_ok, tmp_path):
     assert rep["metrics"]["n_samples"] == len(T.b200_grid())
     m = load_model(str(out))
     assert np.isfinite([m.w_ncols, m.w_density, m.bias]).all()
+
+
+def test_b200_model_is_opt_in():
+    import paper_2412_08902_b200 as hc
+
+    m, d = hc.b200_model(), hc.default_model()
+    assert m != d
+    # the shipped reference model is still the default; the B200 model prefers TILE for wide windows
+    assert m.decide(512, 0.07).value == "tile"
+    assert m.decide(0, 0.0).value == "scalar"
