@@ -721,7 +721,7 @@ using namespace hcs;
 namespace hcs {
 int spmm_tile_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
                    const int64_t* ent_ptr, const uint32_t* ent, int64_t n_rows, int wh, const __nv_bfloat16* x,
-                   int64_t ldx, int dim, float* z, int64_t ldz, float* scratch, int64_t scratch_floats,
+                   int64_t x_rows, int64_t ldx, int dim, float* z, int64_t ldz, float* scratch, int64_t scratch_floats,
                    cudaStream_t st);
 int spmm_tile_warp_tf32(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
                         const int64_t* ent_ptr, const uint2* ent, int64_t n_rows, int wh, const float* x, int64_t ldx,
@@ -759,7 +759,7 @@ extern "C" int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int
   if (eng == 2) {
     HCS_REQUIRE(((uintptr_t)z & 7) == 0 && ldz % 2 == 0, HCS_EINVAL, "z must be 8-byte aligned with even ldz");
     return spmm_tile_warp(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, (const uint32_t*)ent, n_rows, wh,
-                          (const __nv_bfloat16*)x, ldx, dim, z, ldz, (float*)workspace,
+                          (const __nv_bfloat16*)x, x_rows, ldx, dim, z, ldz, (float*)workspace,
                           (int64_t)(ws_bytes / sizeof(float)), st);
   }
   for (int f0 = 0; f0 < dim; f0 += 128) {

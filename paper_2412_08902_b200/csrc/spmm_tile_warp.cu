@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
                 const uint32_t* __restrict__ ent, int64_t n_rows, int wh, const __nv_bfloat16* __restrict__ x,
                 int64_t ldx, int dim, int FS, float* __restrict__ z, int64_t ldz, float* __restrict__ scratch,
                 const float* __restrict__ mw, int d_out, float* __restrict__ out, int64_t ldo,
-                float* __restrict__ oscratch) {
+                float* __restrict__ oscratch, int paired) {
   using C = WarpCfg<SWV>;
   constexpr int kWarpTileWarps = C::kWarps, kWarpStageBytes = C::kStageBytes, kWarpSmemPerWarp = C::kPerWarp;
   constexpr int NI = C::kIssue, RPI = 32 / SWV;
@@ -168,9 +168,16 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
   const int64_t nwarps = (int64_t)gridDim.x * kWarpTileWarps;
   const int64_t gw = (int64_t)blockIdx.x * kWarpTileWarps + warp;
   const int64_t c0 = chunk_ptr[0];
-  const int64_t total = (int64_t)FS * (chunk_ptr[T] - c0);
-  int64_t a, b;
-  warp_range(total, nwarps, gw, a, b);
+  // paired slices (FS > 1, not FUSED): warps gw = g*FS + f of a group g walk the same balanced
+  // range of (window, chunk) positions, warp f doing feature slice f, so a window's slices run
+  // side by side (the plan is read once from DRAM, an X row's slices are fetched together).
+  // Otherwise one warp walks the flattened (window, slice, chunk) sequence.
+  const int FSr = paired ? 1 : FS;
+  const int fw = paired ? (int)(gw % FS) : 0;
+  const int64_t ngroups = paired ? nwarps / FS : nwarps;
+  const int64_t total = (int64_t)FSr * (chunk_ptr[T] - c0);
+  int64_t a = 0, b = 0;
+  if (!paired || gw < ngroups * FS) warp_range(total, ngroups, paired ? gw / FS : gw, a, b);
   if (FUSED) {
     __nv_bfloat16* wt = reinterpret_cast<__nv_bfloat16*>(wsmem + C::kOffW);
     for (int i = threadIdx.x; i < kFusedOutMax * kFusedLdw; i += blockDim.x) {
@@ -219,7 +226,7 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
     --p.rem;
     if (++p.j < p.nj) return;
     p.j = 0;
-    if (++p.f < FS) return;
+    if (++p.f < FSr) return;
     p.f = 0;
     ++p.t;
     p.base += p.nj;
@@ -243,7 +250,7 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
   };
   auto issue = [&](const Pos& p, const int (&g)[NI], int slot) {
     if (p.rem > 0) {
-      const int feat = p.f * C::kFeat + featv;
+      const int feat = (p.f + fw) * C::kFeat + featv;
       const uint32_t vb = feat < dim ? vb_full : 0u;
       const char* src = xb + (int64_t)feat * 2;
       const uint32_t dst = stage0 + slot * kWarpStageBytes;
@@ -359,7 +366,7 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
       const int rows = (int)(n_rows - rs < wh ? n_rows - rs : wh);
       if (z != nullptr) {
         if (!in_head && unit_done) {
-          store_slice<SWV>(z, ldz, rs, rows, dim, P0.f, acc, lane);
+          store_slice<SWV>(z, ldz, rs, rows, dim, P0.f + fw, acc, lane);
         } else {
           float* slot = scratch + (gw * 2 + (in_head ? 0 : 1)) * C::kSlot;
 #pragma unroll
@@ -425,7 +432,7 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
 #pragma unroll
   for (int q = 0; q < 4; ++q) sts128_zero(slab + (lane + 32 * q) * 16);
   __syncwarp();
-  const ChunkPos first = locate(chunk_ptr, T, FS, a);
+  const ChunkPos first = locate(chunk_ptr, T, FSr, a);
   in_head = first.j != 0;
   Pos Q0 = mk(first), Q1 = Q0;
   adv(Q1);
@@ -458,17 +465,23 @@ template <int SWV>
 __global__ void k_tile_warp_fixup(const int32_t* __restrict__ tile_list, int64_t T,
                                   const int64_t* __restrict__ chunk_ptr, int64_t n_rows, int wh, int dim, int FS,
                                   float* __restrict__ z, int64_t ldz, const float* __restrict__ scratch,
-                                  int64_t nwarps) {
+                                  int64_t nwarps, int paired) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (gw >= nwarps) return;
+  // same warp -> range mapping as k_tile_warp (paired: group gw / FS, slice gw % FS)
+  const int FSr = paired ? 1 : FS;
+  const int fw = paired ? (int)(gw % FS) : 0;
+  const int64_t ngroups = paired ? nwarps / FS : nwarps;
+  const int64_t gi = paired ? gw / FS : gw;
+  if (gi >= ngroups) return;
   const int64_t c0 = chunk_ptr[0];
-  const int64_t total = (int64_t)FS * (chunk_ptr[T] - c0);
+  const int64_t total = (int64_t)FSr * (chunk_ptr[T] - c0);
   int64_t a, b;
-  warp_range(total, nwarps, gw, a, b);
+  warp_range(total, ngroups, gi, a, b);
   if (a >= b) return;
-  const ChunkPos last = locate(chunk_ptr, T, FS, b - 1);
-  const int64_t ustart = (int64_t)FS * (last.base - c0) + (int64_t)last.f * last.nj;
+  const ChunkPos last = locate(chunk_ptr, T, FSr, b - 1);
+  const int64_t ustart = (int64_t)FSr * (last.base - c0) + (int64_t)last.f * last.nj;
   const int64_t uend = ustart + last.nj;
   if (!(uend > b && ustart >= a)) return;  // not the warp that opens a split unit
   constexpr int kSlot = WarpCfg<SWV>::kSlot;
@@ -478,11 +491,12 @@ __global__ void k_tile_warp_fixup(const int32_t* __restrict__ tile_list, int64_t
   for (int nt = 0; nt < SWV; ++nt)
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[nt][q] = s[(nt * 4 + q) * 32 + lane];
-  for (int64_t k = gw + 1; k < nwarps; ++k) {
+  for (int64_t k = gi + 1; k < ngroups; ++k) {  // later ranges of the same slice, in order
     int64_t ak, bk;
-    warp_range(total, nwarps, k, ak, bk);
+    warp_range(total, ngroups, k, ak, bk);
     if (ak >= bk) continue;
-    const float* sk = scratch + (k * 2 + 0) * kSlot;
+    const int64_t wk = paired ? k * FS + fw : k;
+    const float* sk = scratch + (wk * 2 + 0) * kSlot;
 #pragma unroll
     for (int nt = 0; nt < SWV; ++nt)
 #pragma unroll
@@ -491,7 +505,7 @@ __global__ void k_tile_warp_fixup(const int32_t* __restrict__ tile_list, int64_t
   }
   const int64_t rs = (int64_t)tile_list[last.t] * wh;
   const int rows = (int)(n_rows - rs < wh ? n_rows - rs : wh);
-  store_slice<SWV>(z, ldz, rs, rows, dim, last.f, acc, lane);
+  store_slice<SWV>(z, ldz, rs, rows, dim, last.f + fw, acc, lane);
 }
 
 // ---------------------------------------------------------------- tf32 variant
@@ -686,7 +700,7 @@ int spmm_tile_warp_tf32(const int32_t* tile_list, int64_t n_tile, const int64_t*
   const int fix_threads = 256;
   const int fix_blocks = (int)((nwarps * 32 + fix_threads - 1) / fix_threads);
   k_tile_warp_fixup<4><<<fix_blocks, fix_threads, 0, st>>>(tile_list, n_tile, chunk_ptr, n_rows, wh, dim, FS, z, ldz,
-                                                            scratch, nwarps);
+                                                            scratch, nwarps, 0);
   HCS_LAUNCH_CHECK("k_tile_warp_fixup");
   return HCS_OK;
 }
@@ -737,14 +751,19 @@ __global__ void k_tile_warp_fixup_out(const int32_t* __restrict__ tile_list, int
     }
 }
 
-static int g_warp_swv = 0;  // 0 auto, 4 or 8 (16-B vectors per row slice)
+static int g_warp_swv = 0;     // 0 auto, 4 or 8 (16-B vectors per row slice)
+// Feature slices of a window walked side by side by sibling warps: 1 on, 0 off, 2 auto = on
+// when X does not fit in L2 (measured: C5, X 4.3 GB: 29.9 -> 28.2 ms; C2, X 60 MB L2-resident:
+// 2.44 -> 2.50 ms at N = 128, tools/exp_pairing.py).
+static int g_warp_paired = 2;
+constexpr int64_t kPairMinXBytes = 96ll << 20;
 
 template <int SWV, bool FUSED = false>
 static int launch_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
                        const int64_t* ent_ptr, const uint32_t* ent, int64_t n_rows, int wh, const __nv_bfloat16* x,
                        int64_t ldx, int dim, float* z, int64_t ldz, float* scratch, int64_t scratch_floats,
                        cudaStream_t st, const float* mw = nullptr, int d_out = 0, float* out = nullptr,
-                       int64_t ldo = 0) {
+                       int64_t ldo = 0, int64_t x_rows = 0) {
   using C = WarpCfg<SWV>;
   const int FS = (dim + C::kFeat - 1) / C::kFeat;
   const int grid = num_sms();
@@ -754,16 +773,18 @@ static int launch_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* 
               (long long)scratch_floats, (long long)need);
   float* oscratch = scratch + nwarps * 2 * C::kSlot;
   const int smem = C::kSmem + (FUSED ? kFusedOutMax * kFusedLdw * 2 : 0);
+  const bool want = g_warp_paired == 1 || (g_warp_paired == 2 && x_rows * ldx * 2 > kPairMinXBytes);
+  const int paired = (!FUSED && FS > 1 && want && C::kWarps % FS == 0) ? 1 : 0;
   HCS_CUDA(cudaFuncSetAttribute(k_tile_warp<SWV, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   k_tile_warp<SWV, FUSED><<<grid, C::kWarps * 32, smem, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows,
                                                                wh, x, ldx, dim, FS, z, ldz, scratch, mw, d_out, out,
-                                                               ldo, oscratch);
+                                                               ldo, oscratch, paired);
   HCS_LAUNCH_CHECK("k_tile_warp");
   const int fix_threads = 256;
   const int fix_blocks = (int)((nwarps * 32 + fix_threads - 1) / fix_threads);
   if (z != nullptr) {
     k_tile_warp_fixup<SWV><<<fix_blocks, fix_threads, 0, st>>>(tile_list, n_tile, chunk_ptr, n_rows, wh, dim, FS, z,
-                                                                ldz, scratch, nwarps);
+                                                                ldz, scratch, nwarps, paired);
     HCS_LAUNCH_CHECK("k_tile_warp_fixup");
   }
   if (FUSED) {
@@ -785,18 +806,18 @@ int gcn_tile_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk
 
 int spmm_tile_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
                    const int64_t* ent_ptr, const uint32_t* ent, int64_t n_rows, int wh, const __nv_bfloat16* x,
-                   int64_t ldx, int dim, float* z, int64_t ldz, float* scratch, int64_t scratch_floats,
+                   int64_t x_rows, int64_t ldx, int dim, float* z, int64_t ldz, float* scratch, int64_t scratch_floats,
                    cudaStream_t st) {
   // 64-feature slices halve the per-feature slab work once a window has >= 2 slices of 32
   const int swv = g_warp_swv ? g_warp_swv : (dim > 32 ? 8 : 4);
   if (swv == 16)
     return launch_warp<16>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim, z, ldz, scratch,
-                           scratch_floats, st);
+                          scratch_floats, st, nullptr, 0, nullptr, 0, x_rows);
   if (swv == 8)
     return launch_warp<8>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim, z, ldz, scratch,
-                          scratch_floats, st);
+                          scratch_floats, st, nullptr, 0, nullptr, 0, x_rows);
   return launch_warp<4>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim, z, ldz, scratch,
-                        scratch_floats, st);
+                          scratch_floats, st, nullptr, 0, nullptr, 0, x_rows);
 }
 
 int64_t tile_warp_scratch_floats() {
@@ -813,6 +834,15 @@ extern "C" int hcs_set_tile_slice(int vectors) {
   HCS_REQUIRE(vectors == 0 || vectors == 4 || vectors == 8 || vectors == 16, HCS_EINVAL,
               "slice must be 0, 4, 8 or 16 (got %d)", vectors);
   hcs::g_warp_swv = vectors;
+  return HCS_OK;
+}
+
+// Paired feature slices (1), one warp per (window, slice) range (0), or auto (2, default:
+// paired when X exceeds 96 MB, i.e. is not L2-resident).  Both are
+// deterministic; windows are cut at different chunk boundaries, so the last bits can differ.
+extern "C" int hcs_set_tile_pairing(int on) {
+  HCS_REQUIRE(on >= 0 && on <= 2, HCS_EINVAL, "pairing must be 0, 1 or 2 (got %d)", on);
+  hcs::g_warp_paired = on;
   return HCS_OK;
 }
 

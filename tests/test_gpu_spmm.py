@@ -294,3 +294,29 @@ def test_scalar_variants(cuda_ok, variant, precision):
                 assert np.array_equal(r1.z.data, r2.z.data)
     finally:
         set_scalar_variant("auto")
+
+
+@pytest.mark.parametrize("dim", [72, 128, 256])
+def test_tile_slice_pairing(cuda_ok, dim):
+    """Paired feature slices (sibling warps walk one (window, chunk) range, a slice each) ==
+    the exact product within tolerance, run-to-run bitwise, and == the unpaired schedule up to
+    the fp32 rounding of different cut points; windows cut by ranges are exercised (plaw8k has
+    ~46 K chunks for 1,184 warps)."""
+    from paper_2412_08902_b200 import _lib
+
+    a = plaw8k_csr()
+    x = orc.random_dense(a.num_cols, dim, 5)
+    ws = hc.partition(to_hc(a))
+    exact = orc.spmm_exact(a, x)
+    out = {}
+    try:
+        for mode in (0, 1):
+            _lib.call("hcs_set_tile_pairing", mode)
+            r1 = hc.spmm_tile(ws, hc.DenseMatrix(x))
+            r2 = hc.spmm_tile(ws, hc.DenseMatrix(x))
+            assert np.array_equal(r1.z.data, r2.z.data)
+            assert orc.max_rel_err(r1.z.data, exact) <= BF16_TOL
+            out[mode] = r1.z.data
+    finally:
+        _lib.call("hcs_set_tile_pairing", 2)
+    assert orc.max_rel_err(out[1], out[0]) <= 1e-4

@@ -11,6 +11,9 @@ from paper_2412_08902_b200.executors import DeviceOperand, get_plan
 scale = int(os.environ.get("C5_SCALE", "24"))
 dim = int(os.environ.get("C5_DIM", "128"))
 torch.cuda.set_device(0)
+if os.environ.get("C5_PAIRING"):
+    from paper_2412_08902_b200 import _lib as _l
+    _l.call("hcs_set_tile_pairing", int(os.environ["C5_PAIRING"]))
 if os.environ.get("C5_TILE_SLICE"):
     from paper_2412_08902_b200 import _lib as _l
     _l.call("hcs_set_tile_slice", int(os.environ["C5_TILE_SLICE"]))
