@@ -370,7 +370,7 @@ def run_ours(args):
                                 "peak_GBps": GATHER_PEAK_GBPS,
                                 "frac": (gather_bytes / (tile_ms * 1e-3) / 1e9 / GATHER_PEAK_GBPS) if tile_ms > 0
                                 else None,
-                                "lsu_floor_ms": gather_bytes / 512 * 12 / (148 * (clocks or {}).get("sm_mhz", 1965)
+                                "lsu_floor_ms": gather_bytes / 512 * 12 / (148 * ((clocks or {}).get("sm_mhz") or 1965)
                                                                           * 1e6) * 1e3
                                 if gather_bytes else None}},
         "gpu_launches": plan.launches_per_run(dim) * args.steps * (
