@@ -209,6 +209,24 @@ def run_ours(args):
     ev1.record()
     torch.cuda.synchronize()
     t_plan_ms = ev0.elapsed_time(ev1)
+    # the same K1 + K2 work again, warm (the first build includes one-time CUDA module loading)
+    import dataclasses
+
+    from paper_2412_08902_b200.executors import HybridPlan
+
+    a_fresh = dataclasses.replace(local_a, _derived={})  # same arrays, no cached windows
+    ev0.record()
+    ws_w = hc.partition(a_fresh)
+    asg_w = hc.classify_windows(sel_model, ws_w)
+    ev1.record()
+    torch.cuda.synchronize()
+    t_partition_warm = ev0.elapsed_time(ev1)
+    ev0.record()
+    HybridPlan(ws_w, asg_w.device_codes(torch.device("cuda")), args.precision)
+    ev1.record()
+    torch.cuda.synchronize()
+    t_plan_warm = ev0.elapsed_time(ev1)
+    del ws_w, asg_w, a_fresh
     ncols = ws.ncols()
     plan_bytes = plan.gidx.numel() * 4 + plan.ent.numel() * 4 + local_a.nnz * 6 * int(plan.scalar_list.numel() > 0)
     sum_ncols = int(ncols.sum())
@@ -354,7 +372,8 @@ def run_ours(args):
             "selector": "reference default (selector_default.json)" if args.selector is None else args.selector,
             "l2_policy": (f"inputs larger than L2 (tile plan + CSR stream {plan_bytes / 1e9:.2f} GB read once per "
                           f"step, > 126 MB L2); X ({n * dim * 2 / 1e6:.0f} MB) gathered with L2 evict_last hints"),
-            "preprocess_ms": {"graph_gen_s": t_gen, "partition_select": t_partition_ms, "tile_plan": t_plan_ms},
+            "preprocess_ms": {"graph_gen_s": t_gen, "partition_select": t_partition_ms, "tile_plan": t_plan_ms,
+                              "partition_select_warm": t_partition_warm, "tile_plan_warm": t_plan_warm},
             "hbm_roofline_ms": full_bytes / (peak * 1e9) * 1e3,
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -66,6 +66,9 @@ int hcs_classify(const int64_t* win_col_ptr, const double* density, int64_t n_wi
  * ent_ptr[nchunks+1]; ent[nnz_tile] packed (bf16 value << 16 | slab position
  * r*64+c) for HCS_DTYPE_BF16, or {pos, fp32 bits} pairs (uint64) for F32. */
 int hcs_tile_plan_workspace_bytes(int64_t nnz_tile, int64_t nchunks, size_t* bytes);
+/* plan builder: 0 (default) = per-window stable bucketing by chunk, 1 = global radix sort on
+ * (chunk, row, column); both produce identical plans */
+int hcs_set_tile_plan_builder(int builder);
 int hcs_tile_plan(const int64_t* row_ptr, const int32_t* cond_cols, const void* values, int values_dtype,
                   const int64_t* win_col_ptr, const int32_t* nonzero_cols, int64_t n_rows, int64_t n_cols, int32_t wh,
                   const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, int64_t nchunks,

@@ -320,3 +320,38 @@ def test_tile_slice_pairing(cuda_ok, dim):
     finally:
         _lib.call("hcs_set_tile_pairing", 2)
     assert orc.max_rel_err(out[1], out[0]) <= 1e-4
+
+
+@pytest.mark.parametrize("precision", ["bf16", "tf32"])
+def test_plan_builders_identical(cuda_ok, precision):
+    """K2: the per-window bucketing builder (default) and the global radix-sort builder give
+    identical plans (gidx, ent_ptr, packed entries), incl. a window with > 3,072 chunks
+    (several bucketing passes) and a short last window."""
+    from paper_2412_08902_b200 import _lib
+    from paper_2412_08902_b200.executors import HybridPlan
+
+    rng = np.random.default_rng(11)
+    rows, cols = [], []
+    for r in range(16):  # one very wide window: ~222 K condensed columns
+        cs = rng.choice(250_000, size=32_000, replace=False)
+        rows += [r] * len(cs)
+        cols += list(cs)
+    for r in range(16, 16 + 37):  # narrower windows, the last one short
+        cs = rng.choice(250_000, size=int(rng.integers(1, 3000)), replace=False)
+        rows += [r] * len(cs)
+        cols += list(cs)
+    a = orc.from_coo(53, 250_000, rows, cols, rng.uniform(-1, 1, len(rows)))
+    ws = hc.partition(to_hc(a))
+    codes = torch.ones(len(ws), dtype=torch.uint8, device="cuda")
+    plans = []
+    try:
+        for builder in (0, 1):
+            _lib.call("hcs_set_tile_plan_builder", builder)
+            plans.append(HybridPlan(ws, codes, precision))
+    finally:
+        _lib.call("hcs_set_tile_plan_builder", 0)
+    p0, p1 = plans
+    assert int(p0.chunk_ptr[1] - p0.chunk_ptr[0]) > 3072
+    assert torch.equal(p0.gidx, p1.gidx)
+    assert torch.equal(p0.ent_ptr, p1.ent_ptr)
+    assert torch.equal(p0.ent, p1.ent)
