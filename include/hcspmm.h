@@ -103,9 +103,10 @@ int hcs_set_scalar_variant(int variant);
 int hcs_tile_scratch_floats(int64_t* floats);
 /* engine 2 row-slice width in 16-B vectors: 0 auto (8 for dim > 32, else 4), 4 or 8 */
 int hcs_set_tile_slice(int vectors);
-/* engine 2 with > 1 feature slice: 2 (default) = auto (1 when X exceeds 96 MB), 1 = the FS warps of a group walk the same
+/* engine 2 with > 1 feature slice: 1 (default) = the FS warps of a group walk the same
  * (window, chunk) range, one slice each (plan read once, an X row's slices fetched together);
- * 0 = one warp per contiguous range of (window, slice, chunk).  Both deterministic. */
+ * 0 = one warp per contiguous range of (window, slice, chunk); 2 = 1 only when X exceeds 96 MB.
+ * All deterministic. */
 int hcs_set_tile_pairing(int on);
 int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
                   const int64_t* ent_ptr, const void* ent, int ent_dtype, int64_t n_rows, int32_t wh, const void* x,

@@ -193,7 +193,8 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
   const uint64_t keep = policy_evict_last();
   // plan data (indices, entries) is read once per feature slice: keep it for the window's
   // other slice-warps (FS > 1), stream it otherwise
-  const uint64_t once = FS > 1 ? policy_evict_normal() : policy_evict_first();
+  // (paired slice-warps read each chunk's plan together: stream it)
+  const uint64_t once = (FS > 1 && !paired) ? policy_evict_normal() : policy_evict_first();
   // gather lane mapping: lane (rg, v) copies 16-B vector v of rows rg*NI + it, it < NI, so its
   // NI gather indices are contiguous (NI/4 x 128-bit loads)
   const int gv = lane % SWV, rg = lane / SWV;
@@ -752,10 +753,12 @@ __global__ void k_tile_warp_fixup_out(const int32_t* __restrict__ tile_list, int
 }
 
 static int g_warp_swv = 0;     // 0 auto, 4 or 8 (16-B vectors per row slice)
-// Feature slices of a window walked side by side by sibling warps: 1 on, 0 off, 2 auto = on
-// when X does not fit in L2 (measured: C5, X 4.3 GB: 29.9 -> 28.2 ms; C2, X 60 MB L2-resident:
-// 2.44 -> 2.50 ms at N = 128, tools/exp_pairing.py).
-static int g_warp_paired = 2;
+// Feature slices of a window walked side by side by sibling warps: 1 on (default), 0 off,
+// 2 auto = on when X does not fit in L2.  Paired warps read each chunk's plan together (the
+// second read hits L1), so the plan streams with evict_first and X stays L2-resident:
+// C2/N=128 DRAM reads 3.25 -> 1.16 GB per launch, L2 hit 82.7 -> 93.5 %, same time (2.46 ms);
+// C5 tile windows 29.9 -> 27.7 ms (tools/exp_pairing.py, exp_pair_ncu.py, exp_c5.py).
+static int g_warp_paired = 1;
 constexpr int64_t kPairMinXBytes = 96ll << 20;
 
 template <int SWV, bool FUSED = false>
@@ -837,7 +840,7 @@ extern "C" int hcs_set_tile_slice(int vectors) {
   return HCS_OK;
 }
 
-// Paired feature slices (1), one warp per (window, slice) range (0), or auto (2, default:
+// Paired feature slices (1, default), one warp per (window, slice) range (0), or auto (2:
 // paired when X exceeds 96 MB, i.e. is not L2-resident).  Both are
 // deterministic; windows are cut at different chunk boundaries, so the last bits can differ.
 extern "C" int hcs_set_tile_pairing(int on) {

@@ -318,7 +318,7 @@ def test_tile_slice_pairing(cuda_ok, dim):
             assert orc.max_rel_err(r1.z.data, exact) <= BF16_TOL
             out[mode] = r1.z.data
     finally:
-        _lib.call("hcs_set_tile_pairing", 2)
+        _lib.call("hcs_set_tile_pairing", 1)
     assert orc.max_rel_err(out[1], out[0]) <= 1e-4
 
 
