@@ -355,3 +355,34 @@ def test_plan_builders_identical(cuda_ok, precision):
     assert torch.equal(p0.gidx, p1.gidx)
     assert torch.equal(p0.ent_ptr, p1.ent_ptr)
     assert torch.equal(p0.ent, p1.ent)
+
+
+@pytest.mark.parametrize("shape", ["no_rows", "no_entries", "one_row", "ragged_17", "one_col"])
+def test_degenerate_shapes(cuda_ok, shape):
+    """Empty and ragged inputs on every path (reference executors.py:216-272 semantics: Z has
+    total_rows(windows) rows, untouched rows are zero, stats count only non-empty windows)."""
+    n, m = {"no_rows": (0, 5), "no_entries": (40, 7), "one_row": (1, 9), "ragged_17": (17, 30),
+            "one_col": (33, 1)}[shape]
+    rng = np.random.default_rng(3)
+    if shape in ("no_rows", "no_entries"):
+        rows, cols = [], []
+    else:
+        rows = list(rng.integers(0, n, size=3 * n))
+        cols = list(rng.integers(0, m, size=3 * n))
+    a = orc.from_coo(n, m, rows, cols, rng.uniform(-1, 1, len(rows)))
+    x = orc.random_dense(m, 6, 4)
+    exact = orc.spmm_exact(a, x)
+    ws = hc.partition(to_hc(a))
+    assert len(ws) == -(-n // 16)
+    asg = hc.classify_windows(hc.default_model(), ws)
+    for res in (hc.spmm_hybrid(ws, asg, hc.DenseMatrix(x)), hc.spmm_tile(ws, hc.DenseMatrix(x)),
+                hc.spmm_scalar(to_hc(a), hc.DenseMatrix(x)),
+                hc.spmm_hybrid(ws, asg, hc.DenseMatrix(x), precision="tf32")):
+        z = np.asarray(res.z.data)
+        assert z.shape == (n, 6)
+        if n:
+            assert orc.max_rel_err(z, exact) <= BF16_TOL if np.abs(exact).max() > 0 else not z.any()
+        live = int((ws.nnz_per_window() > 0).sum()) if n else 0
+        s = res.stats
+        assert s.windows_scalar + s.windows_tile == live
+        assert s.entries_scalar + s.entries_tile == a.nnz

@@ -8,7 +8,7 @@ from paper_2412_08902_b200.gnn import normalize_adj
 from paper_2412_08902_b200.executors import DeviceOperand, get_plan
 
 torch.cuda.set_device(0)
-_lib.call("hcs_set_tile_pairing", int(os.environ.get("PAIR", "2")))
+_lib.call("hcs_set_tile_pairing", int(os.environ.get("PAIR", "1")))
 adj = graphgen.reddit_shaped(seed=0); adj.symmetric = True
 a = normalize_adj(adj, "gcn")
 ws = hc.partition(a)
