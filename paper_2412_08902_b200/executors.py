@@ -314,9 +314,12 @@ def _check_window_bounds(windows, x_rows: int) -> None:
     on the same windows add no device round trip."""
     max_col = getattr(windows, "_max_col", None)
     if max_col is None:
-        live = windows.ncols() > 0
-        last = windows.nonzero_cols[(windows.win_col_ptr[1:] - 1).clamp(min=0)].to(torch.int64)
-        max_col = int(torch.where(live, last, torch.full_like(last, -1)).max().item()) if len(live) else -1
+        if windows.nonzero_cols.numel() == 0:  # no entries at all
+            max_col = -1
+        else:
+            live = windows.ncols() > 0
+            last = windows.nonzero_cols[(windows.win_col_ptr[1:] - 1).clamp(min=0)].to(torch.int64)
+            max_col = int(torch.where(live, last, torch.full_like(last, -1)).max().item())
         windows._max_col = max_col
     if max_col < x_rows:
         return
