@@ -49,6 +49,8 @@ def parse():
                    help="Reddit-shaped input for c2/c3/c4: structureless Chung-Lu (default) or 41 planted "
                         "communities with scrambled ids (secondary data point)")
     p.add_argument("--precision", default="bf16")
+    p.add_argument("--cuda-graph", choices=["auto", "on", "off"], default="auto",
+                   help="replay each step's kernels as one CUDA graph (auto: on for the launch-bound C1)")
     p.add_argument("--selector", default=None,
                    help="selector model JSON (e.g. from `cli train-selector`); default: the reference's shipped model")
     p.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU-baseline sampling")
@@ -233,6 +235,8 @@ def run_ours(args):
     tile_ncols = int(ncols[plan.tile_list.long()].sum()) if plan.n_tile else 0
     codes = ws.codes
 
+    use_graph = args.cuda_graph == "on" or (args.cuda_graph == "auto" and args.config == "c1")
+
     def measure(dim, steps, warmup, with_e2e):
         if args.precision == "tf32":  # fp32 X, RNA-rounded to tf32 once (inputs of the tf32 tensor-core path)
             from paper_2412_08902_b200.executors import stage_operand
@@ -263,9 +267,25 @@ def run_ours(args):
             sends = [torch.zeros((max(m, 1), dim), dtype=torch.bfloat16, device=dev) for m in maxrows]
             recvs = [torch.empty((world * max(m, 1), dim), dtype=torch.bfloat16, device=dev) for m in maxrows]
         tev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        graph = None
+        if world == 1 and use_graph:  # one graph launch per step (SpmmGraph's capture of plan.run)
+            if plan.n_tile:
+                plan.scratch()
+            plan.run(xop, z, ldz)
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                plan.run(xop, z, ldz)
 
         def step(i=None):
             if world == 1:
+                if graph is not None:
+                    if i is not None:
+                        tev[i][0].record()
+                    graph.replay()
+                    if i is not None:
+                        tev[i][1].record()
+                    return
                 plan.run(xop, z, ldz, tile_events=tev[i] if i is not None else None)
                 return
             works = []
@@ -370,6 +390,7 @@ def run_ours(args):
             "sum_ncols": sum_ncols, "aggregate_ci": local_a.nnz / max(sum_ncols, 1),
             "parallelism": f"row-window shards x{world}" if world > 1 else "single GPU",
             "selector": "reference default (selector_default.json)" if args.selector is None else args.selector,
+            "launch": "one CUDA graph per step" if (use_graph and world == 1) else "stream launches",
             "l2_policy": (f"inputs larger than L2 (tile plan + CSR stream {plan_bytes / 1e9:.2f} GB read once per "
                           f"step, > 126 MB L2); X ({n * dim * 2 / 1e6:.0f} MB) gathered with L2 evict_last hints"),
             "preprocess_ms": {"graph_gen_s": t_gen, "partition_select": t_partition_ms, "tile_plan": t_plan_ms,
@@ -378,7 +399,8 @@ def run_ours(args):
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "k_tile_warp (+ k_tile_warp_fixup)" if plan.n_tile else "k_spmm_scalar",
+                     "kernel": ("whole step (CUDA graph: k_tile_warp + fix-up + K3)" if use_graph else
+                                "k_tile_warp (+ k_tile_warp_fixup)") if plan.n_tile else "k_spmm_scalar_w",
                      "kernel_ms": tile_ms, "algorithmic_bytes": tile_bytes,
                      "l2_gather_GBps": gather_bytes / (tile_ms * 1e-3) / 1e9 if tile_ms > 0 else None,
                      # the bound that applies to the tile path: every condensed column

@@ -404,6 +404,46 @@ def _run_host_pipelined(plan, xop, z, ldz, host_kind, stats) -> SpmmResult:
     return SpmmResult(DenseMatrix(host if host_kind == "torch" else host.numpy()), stats)
 
 
+class SpmmGraph:
+    """A hybrid SpMM captured once as a CUDA graph and replayed: for repeated products with
+    the same windows, assignment and X buffer (small graphs, where the 2-3 kernel launches of
+    one product cost more than the kernels).  `x` must be a CUDA tensor; when it already is
+    in the compute dtype with 16-byte rows it is used in place, so updating it in place and
+    calling replay() recomputes Z.  Results are those of spmm_hybrid (same kernels)."""
+
+    def __init__(self, windows, assignment: Assignment, x: torch.Tensor, precision: str = "bf16"):
+        from .windows import as_windowset
+
+        if len(assignment) != len(windows):
+            raise ValueError(f"assignment covers {len(assignment)} windows, expected {len(windows)}")
+        if not isinstance(x, torch.Tensor) or x.device.type != "cuda":
+            raise ValueError("SpmmGraph needs a CUDA tensor operand")
+        precision = _resolve_precision(precision)
+        ws = as_windowset(windows)
+        _check_window_bounds(ws, int(x.shape[0]))
+        dev = ws.csr.device
+        self.plan = get_plan(ws, assignment, precision)
+        self.xop, _ = stage_operand(x, precision, dev, tf32_round=(precision == "tf32" and self.plan.n_tile > 0))
+        self.z, self.ldz = _alloc_z(ws.num_rows, self.xop.dim, dev)
+        self.stats = ExecStats(**self.plan.stats.as_dict())
+        if self.plan.n_tile:
+            self.plan.scratch()  # allocated before capture
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):  # warm-up outside the capture (module loading, attributes)
+            self.plan.run(self.xop, self.z, self.ldz)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.plan.run(self.xop, self.z, self.ldz)
+        self.launches = self.plan.launches_per_run(self.xop.dim)
+
+    def replay(self) -> torch.Tensor:
+        """Recompute Z = A X on the current stream; returns the [rows, dim] view of Z."""
+        self.graph.replay()
+        return self.z[:, : self.xop.dim]
+
+
 def spmm_tile(windows, x, precision: str = "bf16", tile_cols: int = 8, dim_tile: int = 16,
               threads: int = 1) -> SpmmResult:
     """executors.py:216-231: every non-empty window on the tensor-core path."""

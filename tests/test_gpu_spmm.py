@@ -386,3 +386,23 @@ def test_degenerate_shapes(cuda_ok, shape):
         s = res.stats
         assert s.windows_scalar + s.windows_tile == live
         assert s.entries_scalar + s.entries_tile == a.nnz
+
+
+@pytest.mark.parametrize("precision", ["bf16", "tf32"])
+def test_spmm_graph_replay(cuda_ok, precision):
+    """SpmmGraph (one CUDA-graph launch per product) == spmm_hybrid bit for bit, and replays
+    pick up in-place updates of X."""
+    a = plaw8k_csr()
+    ws = hc.partition(to_hc(a))
+    asg = hc.classify_windows(hc.default_model(), ws)
+    dt = torch.bfloat16 if precision == "bf16" else torch.float32
+    x = torch.from_numpy(orc.random_dense(a.num_cols, 64, 2)).to("cuda", dt)
+    g = hc.SpmmGraph(ws, asg, x, precision=precision)
+    z1 = g.replay().clone()
+    ref = hc.spmm_hybrid(ws, asg, x, precision=precision).z.data
+    assert torch.equal(z1, ref)
+    if precision == "bf16":  # operand used in place: replay sees the new X
+        x.mul_(2)
+        assert torch.equal(g.replay(), 2 * z1)
+    with pytest.raises(ValueError, match="CUDA tensor"):
+        hc.SpmmGraph(ws, asg, x.cpu())
