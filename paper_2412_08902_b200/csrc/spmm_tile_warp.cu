@@ -527,7 +527,7 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
                      const int32_t* __restrict__ gidx, const int64_t* __restrict__ ent_ptr,
                      const uint2* __restrict__ ent, int64_t n_rows, int wh, const float* __restrict__ x, int64_t ldx,
                      int dim, int FS, float* __restrict__ z, int64_t ldz, float* __restrict__ scratch) {
-  constexpr int NI = 16, RPI = 4;
+  constexpr int NI = 16;
   extern __shared__ uint8_t tsmem_raw[];
   uint8_t* tsmem = (uint8_t*)(((uintptr_t)tsmem_raw + 127) & ~(uintptr_t)127);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -545,6 +545,8 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
   const uint64_t once = policy_evict_first();
   const char* xb = reinterpret_cast<const char*>(x);
   const int64_t ldxb = ldx * 4;
+  // gather lane mapping: lane (grow, gv) copies 16-B vector gv of rows grow*16 + it, so its 16
+  // gather indices are contiguous (4 x 128-bit loads); 8 lanes fill one 128-B row per copy
   const int grow = lane >> 3, gv = lane & 7;
   const int g8 = lane >> 2, t4 = lane & 3;
   const int arow = (lane & 7) + ((lane >> 3) & 1) * 8, ach = lane >> 4;
@@ -560,9 +562,18 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
 
   auto load_gidx = [&](const ChunkPos& p, int (&g)[NI]) {
     if (p.fi < b) {
-      const int32_t* gp = gidx + (p.base + p.j) * 64 + grow;
+      const int4* gp = reinterpret_cast<const int4*>(gidx + (p.base + p.j) * 64 + grow * NI);
 #pragma unroll
-      for (int it = 0; it < NI; ++it) g[it] = ld_plan_s32(gp + RPI * it, once);
+      for (int q = 0; q < NI / 4; ++q) {
+        int4 v;
+        asm volatile("ld.global.nc.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "l"(gp + q), "l"(once));
+        g[4 * q] = v.x;
+        g[4 * q + 1] = v.y;
+        g[4 * q + 2] = v.z;
+        g[4 * q + 3] = v.w;
+      }
     }
   };
   auto issue = [&](const ChunkPos& p, const int (&g)[NI], int slot) {
@@ -573,7 +584,7 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
       const uint32_t dst = stage0 + slot * kTfStage;
 #pragma unroll
       for (int it = 0; it < NI; ++it) {
-        const int row = grow + RPI * it;
+        const int row = grow * NI + it;
         const int gi = g[it];
         cp_async16(dst + row * kTfRow + (swz_tf(row, gv) << 4), src + (int64_t)max(gi, 0) * ldxb, gi >= 0 ? vb : 0u,
                    keep);
@@ -613,6 +624,12 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
 #pragma unroll
   for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
   int s0 = 0;
+  {  // the slab starts zeroed and is kept zero between chunks (entries are undone after use)
+    const int4 zero4 = make_int4(0, 0, 0, 0);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) reinterpret_cast<int4*>(slab_p)[lane + 32 * q] = zero4;
+    __syncwarp();
+  }
   for (; p0.fi < b;) {
     const int s2 = s0 >= 1 ? s0 - 1 : s0 + 2;
     issue(p2, g2, s2);
@@ -620,12 +637,8 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
     load_ent(ep1a, ep1b, e1r);
     int64_t ep2a, ep2b;
     load_ep(p2, ep2a, ep2b);
+    const int ne = (int)(ep0b - ep0a);
     {
-      const int4 zero4 = make_int4(0, 0, 0, 0);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) reinterpret_cast<int4*>(slab_p)[lane + 32 * q] = zero4;
-      __syncwarp();
-      const int ne = (int)(ep0b - ep0a);
 #pragma unroll
       for (int q = 0; q < kWarpEntRegs; ++q)
         if (lane + 32 * q < ne) *reinterpret_cast<uint32_t*>(slab_p + e0r[q].x) = e0r[q].y;
@@ -652,6 +665,16 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
           mma_tf32_1688(acc[nt], af, b0, b1);
         }
       }
+    }
+    __syncwarp();
+    if (ne <= 32 * kWarpEntRegs) {  // undo this chunk's scatter
+#pragma unroll
+      for (int q = 0; q < kWarpEntRegs; ++q)
+        if (lane + 32 * q < ne) *reinterpret_cast<uint32_t*>(slab_p + e0r[q].x) = 0u;
+    } else {
+      const int4 zero4 = make_int4(0, 0, 0, 0);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) reinterpret_cast<int4*>(slab_p)[lane + 32 * q] = zero4;
     }
     __syncwarp();
     const bool unit_done = p0.j + 1 == p0.nj;
