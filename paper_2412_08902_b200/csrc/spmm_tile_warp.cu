@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
                 float* __restrict__ oscratch, int paired) {
   using C = WarpCfg<SWV>;
   constexpr int kWarpTileWarps = C::kWarps, kWarpStageBytes = C::kStageBytes, kWarpSmemPerWarp = C::kPerWarp;
-  constexpr int NI = C::kIssue, RPI = 32 / SWV;
+  constexpr int NI = C::kIssue;
   extern __shared__ uint8_t wsmem_raw[];
   uint8_t* wsmem = (uint8_t*)(((uintptr_t)wsmem_raw + 127) & ~(uintptr_t)127);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
