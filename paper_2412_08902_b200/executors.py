@@ -170,6 +170,10 @@ def stage_operand(x, precision: str, device, tf32_round: bool = False) -> tuple[
         buf = torch.empty((rows, ld), dtype=want, device=device)
         buf.copy_(t, non_blocking=True)
         return DeviceOperand(buf, dim, ld, code), was_host
+    if ld == dim and not tf32_round:  # no padding: one conversion copy, no zero fill
+        buf = torch.empty((rows, ld), dtype=want, device=device)
+        buf.copy_(t, non_blocking=True)
+        return DeviceOperand(buf, dim, ld, code), was_host
     buf = torch.zeros((rows, ld), dtype=want, device=device)
     if rows and dim:
         src = t.to(device=device, non_blocking=True)

@@ -24,11 +24,28 @@ from .executors import _alloc_z, get_plan, stage_operand
 FUSED_MAX_DIM = 128
 
 
+GRAD_W_SPLIT = 2048  # rows per K-slice of the split-K grad_W GEMM
+
+
 def grad_weight(z: torch.Tensor, g: torch.Tensor) -> torch.Tensor:
+    """Z^T G as a deterministic split-K GEMM: K = n rows in slices of GRAD_W_SPLIT, one batched
+    TF32 tensor-core GEMM over the slices (a CTA per slice instead of one per 64 x 64 output
+    tile: the plain GEMM took 125 us at C3), then the slice partials summed in slice order."""
+    z, g = z.float(), g.float()
+    n = int(z.shape[0])
+    s = n // GRAD_W_SPLIT
     prev = torch.backends.cuda.matmul.allow_tf32
     torch.backends.cuda.matmul.allow_tf32 = True
     try:
-        return z.t().float() @ g.float()
+        if s < 2:
+            return z.t() @ g
+        head = s * GRAD_W_SPLIT
+        zb = z[:head].reshape(s, GRAD_W_SPLIT, z.shape[1])
+        gb = g[:head].reshape(s, GRAD_W_SPLIT, g.shape[1])
+        out = torch.bmm(zb.transpose(1, 2), gb).sum(0)
+        if head < n:
+            out = out + z[head:].t() @ g[head:]
+        return out
     finally:
         torch.backends.cuda.matmul.allow_tf32 = prev
 

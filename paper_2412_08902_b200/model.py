@@ -93,10 +93,9 @@ class Gcn2:
     def epoch(self, x, labels, windows: WindowSet, windows_t=None, precision="bf16", shard=None):
         """One training epoch; returns the loss tensor (on the device)."""
         logits = self.forward(x, windows, windows_t, precision, shard)
-        # mean softmax cross-entropy; written as logsumexp - picked logit (row-parallel
-        # kernels: F.cross_entropy's nll_loss reduction took 250 + 143 us at C3)
-        picked = logits.gather(1, labels.view(-1, 1).long()).squeeze(1)
-        loss = (torch.logsumexp(logits, dim=1) - picked).mean()
+        # mean softmax cross-entropy as -mean(log_softmax[label]): warp-per-row softmax kernels
+        # (F.cross_entropy's nll_loss reduction took 250 + 143 us at C3, logsumexp 110 us)
+        loss = -torch.log_softmax(logits, dim=1).gather(1, labels.view(-1, 1).long()).mean()
         for p in self.parameters():
             p.grad = None
         loss.backward()
