@@ -235,13 +235,31 @@ __global__ void __launch_bounds__(kScalarWarps * 32, FUSED ? 1 : HCS_SCALAR_MINB
   int32_t* scol = reinterpret_cast<int32_t*>(wsm) + warp * kScalarCap;
   float* sval = reinterpret_cast<float*>(wsm + kScalarWarps * kScalarCap * 4) + warp * kScalarCap;
   float* zs = reinterpret_cast<float*>(wsm + kScalarWarps * kScalarCap * 8) + warp * (kFusedMaxRows * kScalarZsLd);
-  const int64_t gw = (int64_t)blockIdx.x * kScalarWarps + warp;
-  if (gw >= n_list) return;
+  const int64_t nwarps = (int64_t)gridDim.x * kScalarWarps;
+  const int64_t gw0 = (int64_t)blockIdx.x * kScalarWarps + warp;
+  if (gw0 >= n_list) return;
   const uint64_t keep = policy_evict_last();
   const uint64_t strm = stream_policy();
-  const int64_t rs = (int64_t)win_list[gw] * wh;
-  const int nr = (int)(n_rows - rs < wh ? n_rows - rs : wh);
-  const int64_t rp = lane <= nr ? ld_stream_s64(row_ptr + rs + lane, strm) : 0;
+  // persistent warps, windows dealt round-robin (a block's warps never idle on a slow
+  // sibling's window); the next window's row pointers are loaded one window ahead
+  auto load_rp = [&](int64_t wi, int64_t& rs_, int& nr_) -> int64_t {
+    if (wi >= n_list) {
+      rs_ = 0;
+      nr_ = 0;
+      return 0;
+    }
+    rs_ = (int64_t)__ldg(win_list + wi) * wh;
+    nr_ = (int)(n_rows - rs_ < wh ? n_rows - rs_ : wh);
+    return lane <= nr_ ? ld_stream_s64(row_ptr + rs_ + lane, strm) : 0;
+  };
+  int64_t rs_n;
+  int nr_n;
+  int64_t rp_n = load_rp(gw0, rs_n, nr_n);
+  for (int64_t gw = gw0; gw < n_list; gw += nwarps) {
+  const int64_t rs = rs_n;
+  const int nr = nr_n;
+  const int64_t rp = rp_n;
+  rp_n = load_rp(gw + nwarps, rs_n, nr_n);
   const int64_t e0 = __shfl_sync(0xffffffffu, rp, 0), e1 = __shfl_sync(0xffffffffu, rp, nr);
   const bool staged = e1 - e0 <= kScalarCap;
   const int32_t* cw = col + e0;  // the window's entries
@@ -362,6 +380,8 @@ __global__ void __launch_bounds__(kScalarWarps * 32, FUSED ? 1 : HCS_SCALAR_MINB
       }
     }
   }
+  __syncwarp();  // staging / zs buffers are reused by the warp's next window
+  }
 }
 
 static int g_scalar_variant = 0;  // 0 auto (warp-per-window), 1 block-per-window kernel, 2 warp kernel with 16-B vectors
@@ -371,7 +391,9 @@ static int launch_scalar_w(const int64_t* row_ptr, const int32_t* col, const VT*
                            const int32_t* win_list, int64_t n_list, const XT* x, int dim, int64_t ldx, float* z,
                            int64_t ldz, bool v32, cudaStream_t st, const float* mw = nullptr, int d_out = 0,
                            float* out = nullptr, int64_t ldo = 0) {
-  const unsigned grid = (unsigned)((n_list + kScalarWarps - 1) / kScalarWarps);
+  // resident blocks only (persistent warps): 4 per SM for the SpMM, 1 for the fused kernel
+  const int64_t want = (n_list + kScalarWarps - 1) / kScalarWarps;
+  const unsigned grid = (unsigned)std::min<int64_t>(want, (int64_t)num_sms() * (FUSED ? 1 : HCS_SCALAR_MINB));
   const int smem = kScalarWarps * (kScalarCap * 8 + (FUSED ? kFusedMaxRows * kScalarZsLd * 4 : 0));
   auto k = v32 ? k_spmm_scalar_w<XT, VT, 32, HCS_SCALAR_U32, FUSED> : k_spmm_scalar_w<XT, VT, 16, 4, FUSED>;
   HCS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
