@@ -168,7 +168,7 @@ constexpr int kScalarZsLd = kFusedMaxDim + 4;  // fused: per-warp window rows in
 #define HCS_SCALAR_U32 3  // entries in flight per lane group (32-byte vectors)
 #endif
 #ifndef HCS_SCALAR_MINB
-#define HCS_SCALAR_MINB 4  // resident blocks per SM the register budget is sized for
+#define HCS_SCALAR_MINB 3  // resident blocks per SM the register budget is sized for
 #endif
 
 #define HCS_TRY(call)                  \
