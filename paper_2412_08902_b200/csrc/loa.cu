@@ -206,11 +206,35 @@ __global__ void __launch_bounds__(kLoaThreads, 1)
           }
           k = lo;
         }
-        for (int64_t i = s0 + lane; i < s1; i += 32) {
-          while (sh.prefix[k + 1] <= i) ++k;
-          const int c = ci[sh.cand_row[k] + (i - sh.prefix[k])];
-          if (bit_test(allcols, c)) atomicAdd(&sh.cnt[k], 1);
+        // kLoaProbe neighbour loads in flight per lane; hits summed lane-locally and flushed
+        // once per candidate (integer sums: the counts are exact in any order)
+        constexpr int kLoaProbe = 8;
+        int local = 0, kcur = k;
+        for (int64_t ib = s0 + lane; ib < s1; ib += 32 * kLoaProbe) {
+          int cc[kLoaProbe], kk[kLoaProbe];
+#pragma unroll
+          for (int u = 0; u < kLoaProbe; ++u) {
+            const int64_t i = ib + 32 * u;
+            kk[u] = -1;
+            cc[u] = 0;
+            if (i < s1) {
+              while (sh.prefix[k + 1] <= i) ++k;
+              kk[u] = k;
+              cc[u] = __ldg(ci + sh.cand_row[k] + (i - sh.prefix[k]));
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kLoaProbe; ++u) {
+            if (kk[u] < 0) continue;
+            if (kk[u] != kcur) {
+              if (local) atomicAdd(&sh.cnt[kcur], local);
+              local = 0;
+              kcur = kk[u];
+            }
+            local += bit_test(allcols, cc[u]) ? 1 : 0;
+          }
         }
+        if (local) atomicAdd(&sh.cnt[kcur], local);
       }
       __syncthreads();
       // ---- argmax over the candidates (exact key, CTA reduction)
