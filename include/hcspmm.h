@@ -66,6 +66,16 @@ int hcs_classify(const int64_t* win_col_ptr, const double* density, int64_t n_wi
  * ent_ptr[nchunks+1]; ent[nnz_tile] packed (bf16 value << 16 | slab position
  * r*64+c) for HCS_DTYPE_BF16, or {pos, fp32 bits} pairs (uint64) for F32. */
 int hcs_tile_plan_workspace_bytes(int64_t nnz_tile, int64_t nchunks, size_t* bytes);
+/* ---------------------------------------------------------------- host ingestion
+ * matrices.py:175-307 (load_matrix_market / parse_edge_list): multi-threaded parse of the
+ * entry lines from byte `offset` (kind 0: Matrix Market entries, `expected` = 2 pattern or 3
+ * fields; kind 1: 'u v' edge list).  A strict subset of the reference grammar; *irregular = 1
+ * means "re-parse with the reference rules" (exact FormatError messages and line numbers).
+ * nthreads <= 0: all hardware threads.  a/b: row,col (1-based as written) or u,v; v: values. */
+int hcs_io_count(const char* path, int64_t offset, int kind, int nthreads, int64_t* count, int* irregular);
+int hcs_io_parse(const char* path, int64_t offset, int kind, int expected, int64_t count, int nthreads, int64_t* a,
+                 int64_t* b, double* v, int* irregular);
+
 /* plan builder: 0 (default) = per-window stable bucketing by chunk, 1 = global radix sort on
  * (chunk, row, column); both produce identical plans */
 int hcs_set_tile_plan_builder(int builder);

@@ -60,6 +60,10 @@ _SIGS = {
     "hcs_normalize_values": (ctypes.c_int, [ctypes.c_int, P, P, P, I64, P, P, P, P]),
     "hcs_debug_tile_profile": (ctypes.c_int, [ctypes.c_int, P, ctypes.c_int]),
     "hcs_set_tile_engine": (ctypes.c_int, [ctypes.c_int]),
+    "hcs_io_count": (ctypes.c_int, [ctypes.c_char_p, I64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(I64),
+                                    ctypes.POINTER(ctypes.c_int)]),
+    "hcs_io_parse": (ctypes.c_int, [ctypes.c_char_p, I64, ctypes.c_int, ctypes.c_int, I64, ctypes.c_int, P, P, P,
+                                    ctypes.POINTER(ctypes.c_int)]),
     "hcs_set_tile_producers": (ctypes.c_int, [ctypes.c_int]),
     "hcs_debug_tile_switches": (ctypes.c_int, [ctypes.c_int]),
 }

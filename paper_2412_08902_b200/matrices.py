@@ -71,16 +71,23 @@ class SparseCsr:
                 raise ValueError("row index out of range")
             if cols.min() < 0 or cols.max() >= num_cols:
                 raise ValueError("column index out of range")
-        order = np.lexsort((cols, rows))
+        if num_rows * max(num_cols, 1) < (1 << 62):
+            # one stable key sort == lexsort((cols, rows)) (equal keys keep input order)
+            order = np.argsort(rows * max(num_cols, 1) + cols, kind="stable")
+        else:
+            order = np.lexsort((cols, rows))
         rows, cols, vals = rows[order], cols[order], vals[order]
         if rows.size:
             head = np.empty(rows.size, dtype=bool)
             head[0] = True
             head[1:] = (rows[1:] != rows[:-1]) | (cols[1:] != cols[:-1])
-            group = np.cumsum(head) - 1
-            summed = np.zeros(int(group[-1]) + 1, dtype=np.float64)
-            np.add.at(summed, group, vals)
-            rows, cols, vals = rows[head], cols[head], summed
+            if head.all():  # no duplicates: np.add.at into zeros is 0.0 + v (maps -0.0 to +0.0)
+                vals = vals + 0.0
+            else:
+                group = np.cumsum(head) - 1
+                summed = np.zeros(int(group[-1]) + 1, dtype=np.float64)
+                np.add.at(summed, group, vals)
+                rows, cols, vals = rows[head], cols[head], summed
         counts = np.bincount(rows, minlength=num_rows) if num_rows else np.zeros(0, np.int64)
         row_ptr = np.zeros(num_rows + 1, dtype=np.int64)
         np.cumsum(counts, out=row_ptr[1:])
