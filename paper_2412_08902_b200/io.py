@@ -280,3 +280,26 @@ def load_edge_list(path: str, undirected: bool = True) -> Graph:
     np.cumsum(np.bincount(rows, minlength=num_vertices), out=row_ptr[1:])
     adj = SparseCsr(num_vertices, num_vertices, row_ptr, cols, np.ones(rows.size))
     return Graph(num_vertices, adj, undirected)
+
+
+def load_edge_list_device(path: str, undirected: bool = True, device=None):
+    """load_edge_list straight into HBM: the parsed (u, v) arrays go to the GPU once and are
+    symmetrised, deduplicated and sorted there (one radix sort of 64-bit keys), giving the
+    DeviceCsr the kernels consume -- the same CSR as load_edge_list(...).adjacency."""
+    import torch
+
+    from . import _lib
+    from .graphgen import csr_from_keys
+
+    dev = device if device is not None else _lib.require_cuda()
+    u, v, _ = parse_edge_arrays(path)
+    num_vertices = int(max(u.max(), v.max())) + 1
+    tu = torch.from_numpy(u).to(dev, non_blocking=True)
+    tv = torch.from_numpy(v).to(dev, non_blocking=True)
+    keys = tu * num_vertices + tv
+    if undirected:
+        keys = torch.cat([keys, tv * num_vertices + tu])
+    keys = torch.unique(keys, sorted=True)
+    csr = csr_from_keys(num_vertices, keys)
+    csr.symmetric = bool(undirected)
+    return csr
