@@ -1,26 +1,29 @@
 // K4 (default engine): warp-independent tensor-core tile path (executors.py:111-141
 // tile_window) on sm_100a.
 //
-// Measured on B200 (profiles/r01_tile_switches_c2.txt): the warp-specialised
-// producer/builder/MMA pipeline of spmm_tile.cu spends ~3.8 ms of its 5.0 ms
-// (C2, N = 128) in per-chunk cross-warp hand-offs alone.  Here every warp is an
-// independent worker with its own cp.async ring, so no barrier is shared between
-// warps on the per-chunk path:
+// Measured on B200 (profiles/r01_tile_switches_pipeline_engine_c2.txt): the warp-specialised
+// producer/builder/MMA pipeline of spmm_tile.cu spends ~3.8 ms of its 5.0 ms (C2, N = 128)
+// in per-chunk cross-warp hand-offs alone.  Here every warp is an independent worker with
+// its own cp.async ring, so no barrier is shared between warps on the per-chunk path:
 //
-//   unit  = (TILE window t, 32-feature slice f); a window's condensed columns are
-//           processed in the K2 plan's 64-column chunks (tile_plan.cu);
-//   warp  = a contiguous, exactly balanced range [a, b) of the flattened
-//           (unit, chunk) sequence; ranges may cut a unit, whose partial sums then
-//           go to two scratch slots per warp and are added in warp order by
-//           k_tile_warp_fixup (deterministic, no float atomics);
-//   chunk = gather 64 X-row slices of 64 B (cp.async 16 B, L2 evict_last, 3-stage
-//           ring per warp, XOR-swizzled for conflict-free ldmatrix.trans), build the
-//           16 x 64 bf16 slab from the packed entries (prefetched into registers one
-//           chunk ahead), then 4 k16 steps x 4 n8 tiles of mma.sync m16n8k16 with
-//           fp32 accumulators in registers;
-//   store = the window's 16 x 32 fp32 slice straight to Z.
-// The slab of a chunk is rebuilt by each of the window's FS slice-warps (cheap:
-// ~70 entries); the X traffic is the same Σncols·N·2 bytes as before.
+//   unit  = (TILE window t, feature slice f) with 32- or 64-feature slices (SWV = 4 / 8
+//           16-B vectors per row slice); a window's condensed columns are processed in the
+//           K2 plan's 64-column chunks (tile_plan.cu);
+//   warp  = a contiguous, exactly balanced range [a, b) of the flattened (unit, chunk)
+//           sequence -- or, with paired slices (default for FS > 1), the FS warps of a
+//           group walk one balanced range of (window, chunk) positions, one slice each, so
+//           a chunk's plan is read once and an X row's slices are fetched together;
+//           ranges may cut a unit, whose partial sums then go to two scratch slots per
+//           warp and are added in range order by k_tile_warp_fixup (deterministic, no
+//           float atomics);
+//   chunk = gather 64 X-row slices (cp.async 16 B, L2 evict_last, 3-stage ring per warp,
+//           XOR-swizzled for conflict-free ldmatrix.trans), build the 16 x 64 bf16 slab
+//           from the packed entries (prefetched into registers one chunk ahead; the slab is
+//           kept zero by undoing each chunk's scatter), then 4 k16 steps x (2 SWV) n8 tiles
+//           of mma.sync m16n8k16 with fp32 accumulators in registers;
+//   store = the window's 16 x (8 SWV) fp32 slice straight to Z.
+// The bound is the LSU: 8 + 4 SM cycles per 512 B gathered (cp.async + ldmatrix), see
+// DESIGN.md section 4 and profiles/r01_probe_*.
 #include "common.cuh"
 #include "mma_helpers.cuh"
 
