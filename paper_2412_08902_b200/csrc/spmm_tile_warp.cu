@@ -154,7 +154,10 @@ constexpr int kFusedOutMax = 64;        // d_out of the warp kernel's fused epil
 constexpr int kFusedLdw = 128 + 8;      // bf16 per M^T row (d_in <= 128)
 constexpr int kOutSlot = 16 * kFusedOutMax;
 
-template <int SWV, bool FUSED>
+// NPR = 16-feature groups of a slice that hold features (compile time, so the unrolled
+// ldmatrix/mma schedule is kept): SWV/2, or 3 for a single 33..48-feature slice (the 41-wide
+// GCN gradient), whose last group is neither gathered nor multiplied.
+template <int SWV, bool FUSED, int NPR = SWV / 2>
 __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
     k_tile_warp(const int32_t* __restrict__ tile_list, int64_t T, const int64_t* __restrict__ chunk_ptr,
                 const int32_t* __restrict__ gidx, const int64_t* __restrict__ ent_ptr,
@@ -253,7 +256,7 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
     }
   };
   auto issue = [&](const Pos& p, const int (&g)[NI], int slot) {
-    if (p.rem > 0) {
+    if (p.rem > 0 && (NPR == SWV / 2 || gv < 2 * NPR)) {
       const int feat = (p.f + fw) * C::kFeat + featv;
       const uint32_t vb = feat < dim ? vb_full : 0u;
       const char* src = xb + (int64_t)feat * 2;
@@ -344,7 +347,7 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
         ldsm_x4(af, slab + ar * 128 + (((kc ^ ar) & 7) << 4));
         const int k = ks * 16 + bk;
 #pragma unroll
-        for (int pr = 0; pr < SWV / 2; ++pr) {
+        for (int pr = 0; pr < NPR; ++pr) {
           uint32_t bb[4];
           ldsm_x4_trans(bb, st + C::off(k, 2 * pr + bfc));
           hmma_16816(acc[2 * pr], af, bb[0], bb[1]);
@@ -385,7 +388,7 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
         const uint32_t* wt = reinterpret_cast<const uint32_t*>(wsmem + C::kOffW);
         const int g8 = lane >> 2, t4 = lane & 3;
 #pragma unroll
-        for (int j = 0; j < SWV / 2; ++j) {
+        for (int j = 0; j < NPR; ++j) {
           uint32_t af[4];
           af[0] = pack_bf16(acc[2 * j][0], acc[2 * j][1]);
           af[1] = pack_bf16(acc[2 * j][2], acc[2 * j][3]);
@@ -804,10 +807,12 @@ static int launch_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* 
   const int smem = C::kSmem + (FUSED ? kFusedOutMax * kFusedLdw * 2 : 0);
   const bool want = g_warp_paired == 1 || (g_warp_paired == 2 && x_rows * ldx * 2 > kPairMinXBytes);
   const int paired = (!FUSED && FS > 1 && want && C::kWarps % FS == 0) ? 1 : 0;
-  HCS_CUDA(cudaFuncSetAttribute(k_tile_warp<SWV, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  k_tile_warp<SWV, FUSED><<<grid, C::kWarps * 32, smem, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows,
-                                                               wh, x, ldx, dim, FS, z, ldz, scratch, mw, d_out, out,
-                                                               ldo, oscratch, paired);
+  // one slice of 33..48 features: the last 16-feature group is all zero
+  auto kern = (SWV == 8 && FS == 1 && dim <= 48 && dim > 32) ? k_tile_warp<SWV, FUSED, (SWV == 8 ? 3 : SWV / 2)>
+                                                            : k_tile_warp<SWV, FUSED>;
+  HCS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  kern<<<grid, C::kWarps * 32, smem, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim,
+                                            FS, z, ldz, scratch, mw, d_out, out, ldo, oscratch, paired);
   HCS_LAUNCH_CHECK("k_tile_warp");
   const int fix_threads = 256;
   const int fix_blocks = (int)((nwarps * 32 + fix_threads - 1) / fix_threads);
