@@ -838,31 +838,12 @@ int gcn_tile_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk
                               scratch, scratch_floats, st, m, d_out, out, ldo);
 }
 
-int spmm_tile_reg32(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
-                    const int64_t* ent_ptr, const uint32_t* ent, int64_t n_rows, int wh, const __nv_bfloat16* x,
-                    int64_t ldx, int dim, float* z, int64_t ldz, float* scratch, int64_t scratch_floats,
-                    cudaStream_t st, int64_t* nwarps_out);
-// Experimental register-direct gather kernel for dim <= 32 (spmm_tile_reg.cu): 0 off (default), 1 on.
-static int g_tile_reg = 0;
-
 int spmm_tile_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
                    const int64_t* ent_ptr, const uint32_t* ent, int64_t n_rows, int wh, const __nv_bfloat16* x,
                    int64_t x_rows, int64_t ldx, int dim, float* z, int64_t ldz, float* scratch, int64_t scratch_floats,
                    cudaStream_t st) {
   // 64-feature slices halve the per-feature slab work once a window has >= 2 slices of 32
   const int swv = g_warp_swv ? g_warp_swv : (dim > 32 ? 8 : 4);
-  if (g_tile_reg && dim <= 32 && ldx % 8 == 0) {
-    int64_t nwarps = 0;
-    const int rc = spmm_tile_reg32(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim, z, ldz,
-                                   scratch, scratch_floats, st, &nwarps);
-    if (rc != HCS_OK) return rc;
-    const int fix_threads = 256;
-    const int fix_blocks = (int)((nwarps * 32 + fix_threads - 1) / fix_threads);
-    k_tile_warp_fixup<4><<<fix_blocks, fix_threads, 0, st>>>(tile_list, n_tile, chunk_ptr, n_rows, wh, dim, 1, z, ldz,
-                                                             scratch, nwarps, 0);
-    HCS_LAUNCH_CHECK("k_tile_warp_fixup");
-    return HCS_OK;
-  }
   if (swv == 16)
     return launch_warp<16>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim, z, ldz, scratch,
                           scratch_floats, st, nullptr, 0, nullptr, 0, x_rows);
@@ -881,12 +862,6 @@ int64_t tile_warp_scratch_floats() {
 }
 
 }  // namespace hcs
-
-extern "C" int hcs_set_tile_reg(int on) {
-  HCS_REQUIRE(on == 0 || on == 1, HCS_EINVAL, "tile_reg must be 0 or 1 (got %d)", on);
-  hcs::g_tile_reg = on;
-  return HCS_OK;
-}
 
 // Row-slice width of the warp-independent tile kernel: 0 auto, 4 (32 features) or 8 (64).
 extern "C" int hcs_set_tile_slice(int vectors) {

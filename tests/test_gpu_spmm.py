@@ -205,25 +205,6 @@ def test_warp_kernel_slice_widths(cuda_ok, vectors, dim):
     assert np.array_equal(r1.z.data, r2.z.data)
 
 
-@pytest.mark.parametrize("dim", [8, 16, 24, 32])
-def test_register_gather_kernel_matches(cuda_ok, dim):
-    """hcs_set_tile_reg(1) (dim <= 32: X rows loaded straight into mma B fragments) gives the
-    cp.async kernel's result bit for bit (same k16 order, same fix-up order)."""
-    from paper_2412_08902_b200 import _lib
-
-    a = plaw8k_csr()
-    x = orc.random_dense(a.num_cols, dim, seed=dim + 5)
-    ws = hc.partition(to_hc(a))
-    base = hc.spmm_tile(ws, hc.DenseMatrix(x)).z.data
-    try:
-        _lib.call("hcs_set_tile_reg", 1)
-        r1 = hc.spmm_tile(ws, hc.DenseMatrix(x)).z.data
-    finally:
-        _lib.call("hcs_set_tile_reg", 0)
-    assert orc.max_rel_err(r1, orc.spmm_exact(a, x)) <= BF16_TOL
-    assert np.array_equal(r1, base)
-
-
 TF32_TOL = 1e-3
 
 
