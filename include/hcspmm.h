@@ -113,9 +113,6 @@ int hcs_set_scalar_variant(int variant);
 int hcs_tile_scratch_floats(int64_t* floats);
 /* engine 2 row-slice width in 16-B vectors: 0 auto (8 for dim > 32, else 4), 4 or 8 */
 int hcs_set_tile_slice(int vectors);
-/* engine 2, 64-feature slices: X rows per 16-row group fetched by TMA tile::gather4 instead
- * of cp.async (experimental; 0 = default, 4 or 8) */
-int hcs_set_tile_tma_rows(int rows);
 /* engine 2 with > 1 feature slice: 1 (default) = the FS warps of a group walk the same
  * (window, chunk) range, one slice each (plan read once, an X row's slices fetched together);
  * 0 = one warp per contiguous range of (window, slice, chunk); 2 = 1 only when X exceeds 96 MB.

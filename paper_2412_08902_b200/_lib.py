@@ -47,7 +47,6 @@ _SIGS = {
                                      I64, P, SZ, P]),
     "hcs_tile_scratch_floats": (ctypes.c_int, [ctypes.POINTER(I64)]),
     "hcs_set_tile_slice": (ctypes.c_int, [ctypes.c_int]),
-    "hcs_set_tile_tma_rows": (ctypes.c_int, [ctypes.c_int]),
     "hcs_set_scalar_variant": (ctypes.c_int, [ctypes.c_int]),
     "hcs_set_tile_pairing": (ctypes.c_int, [ctypes.c_int]),
     "hcs_set_tile_plan_builder": (ctypes.c_int, [ctypes.c_int]),

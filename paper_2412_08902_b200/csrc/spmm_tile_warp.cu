@@ -157,12 +157,9 @@ constexpr int kOutSlot = 16 * kFusedOutMax;
 // NPR = 16-feature groups of a slice that hold features (compile time, so the unrolled
 // ldmatrix/mma schedule is kept): SWV/2, or 3 for a single 33..48-feature slice (the 41-wide
 // GCN gradient), whose last group is neither gathered nor multiplied.
-// KT (SWV = 8, experimental): rows rg*16 + [0, KT) of each full chunk are fetched by TMA
-// tile::gather4 (SWIZZLE_128B tensor map over X; the hardware swizzle equals off() on a
-// 1024-B aligned stage) instead of cp.async, moving that share of the gather off the LSU.
-template <int SWV, bool FUSED, int NPR = SWV / 2, int KT = 0>
+template <int SWV, bool FUSED, int NPR = SWV / 2>
 __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
-    k_tile_warp(const __grid_constant__ CUtensorMap tmx, const int32_t* __restrict__ tile_list, int64_t T, const int64_t* __restrict__ chunk_ptr,
+    k_tile_warp(const int32_t* __restrict__ tile_list, int64_t T, const int64_t* __restrict__ chunk_ptr,
                 const int32_t* __restrict__ gidx, const int64_t* __restrict__ ent_ptr,
                 const uint32_t* __restrict__ ent, int64_t n_rows, int wh, const __nv_bfloat16* __restrict__ x,
                 int64_t ldx, int dim, int FS, float* __restrict__ z, int64_t ldz, float* __restrict__ scratch,
@@ -171,19 +168,10 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
   using C = WarpCfg<SWV>;
   constexpr int kWarpTileWarps = C::kWarps, kWarpStageBytes = C::kStageBytes, kWarpSmemPerWarp = C::kPerWarp;
   constexpr int NI = C::kIssue;
-  static_assert(KT == 0 || (SWV == 8 && !FUSED && KT % 4 == 0 && KT <= 16), "TMA rows: SWV 8 only");
   extern __shared__ uint8_t wsmem_raw[];
-  uint8_t* wsmem = (uint8_t*)(((uintptr_t)wsmem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* wsmem = (uint8_t*)(((uintptr_t)wsmem_raw + 127) & ~(uintptr_t)127);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * kWarpTileWarps;
-  // TMA completion: one mbarrier per ring slot per warp (after the warp regions)
-  uint64_t* tbar = reinterpret_cast<uint64_t*>(wsmem + kWarpTileWarps * kWarpSmemPerWarp) + warp * kWarpTileStages;
-  if (KT > 0) {
-    if (lane < kWarpTileStages) mbar_init(tbar + lane, 1);
-    fence_barrier_init();
-    __syncwarp();
-  }
-  uint32_t tph = 0;  // parity of the next completion of each slot's barrier
   const int64_t gw = (int64_t)blockIdx.x * kWarpTileWarps + warp;
   const int64_t c0 = chunk_ptr[0];
   // paired slices (FS > 1, not FUSED): warps gw = g*FS + f of a group g walk the same balanced
@@ -268,24 +256,6 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
     }
   };
   auto issue = [&](const Pos& p, const int (&g)[NI], int slot) {
-    if (KT > 0 && p.rem > 0) {
-      // full chunks: KT rows per row group by TMA (lane gv = q issues rows rg*16 + 4q .. 4q+3)
-      const bool full = p.j + 1 < p.nj;
-      if (lane == 0) mbar_expect_tx(tbar + slot, full ? 4u * KT * 128u : 0u);
-      if (full && gv < KT / 4) {
-        const int q = gv;
-        int r[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) r[u] = g[0];
-#pragma unroll
-        for (int qq = 0; qq < KT / 4; ++qq)
-          if (qq == q) {
-            r[0] = g[4 * qq]; r[1] = g[4 * qq + 1]; r[2] = g[4 * qq + 2]; r[3] = g[4 * qq + 3];
-          }
-        tma_gather4(&tmx, tbar + slot, wsmem + warp * kWarpSmemPerWarp + slot * kWarpStageBytes + (rg * NI + 4 * q) * 128,
-                    (p.f + fw) * C::kFeat, r[0], r[1], r[2], r[3], keep);
-      }
-    }
     if (p.rem > 0 && (NPR == SWV / 2 || gv < 2 * NPR)) {
       const int feat = (p.f + fw) * C::kFeat + featv;
       const uint32_t vb = feat < dim ? vb_full : 0u;
@@ -293,7 +263,7 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
       const uint32_t dst = stage0 + slot * kWarpStageBytes;
       if (p.j + 1 < p.nj) {  // full chunk: every slot holds a column
 #pragma unroll
-        for (int it = KT; it < NI; ++it) cp_async16(dst + dofs[it], src + (uint64_t)(uint32_t)g[it] * ldxb, vb, keep);
+        for (int it = 0; it < NI; ++it) cp_async16(dst + dofs[it], src + (uint64_t)(uint32_t)g[it] * ldxb, vb, keep);
       } else {  // the window's last chunk: pad slots (-1) are zero-filled
 #pragma unroll
         for (int it = 0; it < NI; ++it) {
@@ -367,10 +337,6 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
       }
     }
     cp_async_wait<2>();  // P0's gathers landed (P1, P2 may still be in flight)
-    if (KT > 0) {
-      mbar_wait(tbar + s0, (tph >> s0) & 1u);
-      tph ^= 1u << s0;
-    }
     __syncwarp();
     {
       const uint32_t st = stage0 + s0 * kWarpStageBytes;
@@ -823,9 +789,6 @@ static int g_warp_swv = 0;     // 0 auto, 4 or 8 (16-B vectors per row slice)
 // C5 tile windows 29.9 -> 27.7 ms (tools/exp_pairing.py, exp_pair_ncu.py, exp_c5.py).
 static int g_warp_paired = 1;
 constexpr int64_t kPairMinXBytes = 96ll << 20;
-// Experimental: rows per 16-row group fetched by TMA gather4 on the 64-feature slice kernel
-// (0 = all rows by cp.async, the default; 4 or 8).
-static int g_warp_tma_rows = 0;
 
 template <int SWV, bool FUSED = false>
 static int launch_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
@@ -841,26 +804,15 @@ static int launch_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* 
   HCS_REQUIRE(scratch != nullptr && scratch_floats >= need, HCS_EINVAL, "tile scratch too small (%lld floats, need %lld)",
               (long long)scratch_floats, (long long)need);
   float* oscratch = scratch + nwarps * 2 * C::kSlot;
-  // + 1024-B alignment of the warp regions (TMA swizzle) + per-warp TMA barriers
-  const int smem = C::kSmem + 1024 + C::kWarps * kWarpTileStages * 8 + (FUSED ? kFusedOutMax * kFusedLdw * 2 : 0);
+  const int smem = C::kSmem + (FUSED ? kFusedOutMax * kFusedLdw * 2 : 0);
   const bool want = g_warp_paired == 1 || (g_warp_paired == 2 && x_rows * ldx * 2 > kPairMinXBytes);
   const int paired = (!FUSED && FS > 1 && want && C::kWarps % FS == 0) ? 1 : 0;
   // one slice of 33..48 features: the last 16-feature group is all zero
   auto kern = (SWV == 8 && FS == 1 && dim <= 48 && dim > 32) ? k_tile_warp<SWV, FUSED, (SWV == 8 ? 3 : SWV / 2)>
                                                             : k_tile_warp<SWV, FUSED>;
-  CUtensorMap tmx;
-  memset(&tmx, 0, sizeof(tmx));
-  if (SWV == 8 && !FUSED && g_warp_tma_rows > 0 && kern == k_tile_warp<SWV, FUSED> && x_rows > 0 &&
-      x_rows < (1ll << 31)) {
-    int rc = encode_tiled_2d(&tmx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, const_cast<__nv_bfloat16*>(x), (uint64_t)dim,
-                             (uint64_t)x_rows, (uint64_t)ldx * 2, 64, 1, CU_TENSOR_MAP_SWIZZLE_128B);
-    if (rc != HCS_OK) return rc;
-    if constexpr (SWV == 8 && !FUSED)
-      kern = g_warp_tma_rows == 4 ? k_tile_warp<8, false, 4, 4> : k_tile_warp<8, false, 4, 8>;
-  }
   HCS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  kern<<<grid, C::kWarps * 32, smem, st>>>(tmx, tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx,
-                                            dim, FS, z, ldz, scratch, mw, d_out, out, ldo, oscratch, paired);
+  kern<<<grid, C::kWarps * 32, smem, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim,
+                                            FS, z, ldz, scratch, mw, d_out, out, ldo, oscratch, paired);
   HCS_LAUNCH_CHECK("k_tile_warp");
   const int fix_threads = 256;
   const int fix_blocks = (int)((nwarps * 32 + fix_threads - 1) / fix_threads);
@@ -910,13 +862,6 @@ int64_t tile_warp_scratch_floats() {
 }
 
 }  // namespace hcs
-
-// Experimental: X rows per 16-row group gathered by TMA on the 64-feature-slice kernel (0, 4, 8).
-extern "C" int hcs_set_tile_tma_rows(int rows) {
-  HCS_REQUIRE(rows == 0 || rows == 4 || rows == 8, HCS_EINVAL, "tma rows must be 0, 4 or 8 (got %d)", rows);
-  hcs::g_warp_tma_rows = rows;
-  return HCS_OK;
-}
 
 // Row-slice width of the warp-independent tile kernel: 0 auto, 4 (32 features) or 8 (64).
 extern "C" int hcs_set_tile_slice(int vectors) {

@@ -205,26 +205,6 @@ def test_warp_kernel_slice_widths(cuda_ok, vectors, dim):
     assert np.array_equal(r1.z.data, r2.z.data)
 
 
-@pytest.mark.parametrize("rows", [4, 8])
-@pytest.mark.parametrize("dim", [41, 64, 100, 128])
-def test_tma_rows_match_cp_async(cuda_ok, rows, dim):
-    """hcs_set_tile_tma_rows (part of each chunk's X rows by TMA gather4 into the same
-    swizzled stage) gives the all-cp.async result bit for bit."""
-    from paper_2412_08902_b200 import _lib
-
-    a = plaw8k_csr()
-    x = orc.random_dense(a.num_cols, dim, seed=dim + 9)
-    ws = hc.partition(to_hc(a))
-    base = hc.spmm_tile(ws, hc.DenseMatrix(x)).z.data
-    try:
-        _lib.call("hcs_set_tile_tma_rows", rows)
-        r1 = hc.spmm_tile(ws, hc.DenseMatrix(x)).z.data
-    finally:
-        _lib.call("hcs_set_tile_tma_rows", 0)
-    assert orc.max_rel_err(r1, orc.spmm_exact(a, x)) <= BF16_TOL
-    assert np.array_equal(r1, base)
-
-
 TF32_TOL = 1e-3
 
 
