@@ -8,8 +8,9 @@
 //  * bitmap (n_cols <= kBitmapMaxCols): one CTA per window (grid-strided), the
 //    window's distinct columns marked in a shared-memory bitmap; ncols counted from
 //    atomicOr return values; ranks (cond_cols) from per-8-word popcount prefixes.
-//  * sort (larger n_cols): CUB radix sort of (window, col) keys, run heads give the
-//    ascending unique columns and the inverse index.
+//  * sort (larger n_cols): windows of <= 1024 entries sort their (col, entry) pairs inside one
+//    CTA, larger ones go through one CUB segmented radix sort (the windows are contiguous
+//    segments of the CSR); run heads -> ascending unique columns, scan of the flags -> ranks.
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -165,49 +166,171 @@ __global__ void __launch_bounds__(kPartThreads) k_fill_bitmap(const int64_t* __r
   }
 }
 
-// ---- sort path
-__global__ void k_make_keys(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col, int64_t n_rows,
-                            int wh, uint64_t* __restrict__ keys, int32_t* __restrict__ vals) {
-  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  int lane = threadIdx.x & 31;
-  for (int64_t r = warp; r < n_rows; r += nwarps) {
-    uint64_t win = (uint64_t)(r / wh);
-    for (int64_t e = row_ptr[r] + lane; e < row_ptr[r + 1]; e += 32) {
-      keys[e] = (win << 32) | (uint32_t)col[e];
-      vals[e] = (int32_t)e;
+// ---- sort path.  Windows are contiguous in the CSR, so each is one segment of col_idx.
+//  * windows of <= kCtaSortMax entries: one CTA sorts the (col, local entry) pairs in shared
+//    memory (cub::BlockRadixSort, size classes 128 / 512 / 1024), then the run heads give the
+//    ascending unique columns and a block scan of the head flags the inverse index;
+//  * larger windows: one segmented radix sort (their segments only, column bits only), then a
+//    CTA per window walks its sorted segment the same way.
+// Both stage ranks (per entry) and unique columns (at the window's first entry offset), so
+// hcs_partition_fill only copies them once win_col_ptr is known.
+constexpr int kCtaSortMax = 1024;
+
+__global__ void k_win_offsets(const int64_t* __restrict__ row_ptr, int64_t n_rows, int wh, int64_t W,
+                              int32_t* __restrict__ woff, int32_t* __restrict__ iota, int64_t nnz) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t w = i; w <= W; w += stride) woff[w] = (int32_t)row_ptr[min(w * wh, n_rows)];
+  for (int64_t e = i; e < nnz; e += stride) iota[e] = (int32_t)e;
+}
+
+template <int TH, int IT>
+__global__ void __launch_bounds__(TH) k_win_sort(int64_t W, const int32_t* __restrict__ woff,
+                                                 const int32_t* __restrict__ col, int lo, int end_bit,
+                                                 int64_t* __restrict__ ncols_out, int32_t* __restrict__ stage_rank,
+                                                 int32_t* __restrict__ stage_uniq) {
+  using Sort = cub::BlockRadixSort<uint32_t, TH, IT, int32_t>;
+  using Scan = cub::BlockScan<int, TH>;
+  __shared__ union {
+    typename Sort::TempStorage sort;
+    typename Scan::TempStorage scan;
+  } ts;
+  __shared__ uint32_t last[TH];
+  const int tid = threadIdx.x;
+  for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
+    const int32_t e0 = woff[w];
+    const int n = woff[w + 1] - e0;
+    if (n <= lo || n > TH * IT) continue;  // uniform across the block
+    uint32_t k[IT];
+    int32_t v[IT];
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {  // striped load (the input order does not matter to the sort)
+      const int idx = i * TH + tid;
+      k[i] = idx < n ? (uint32_t)col[e0 + idx] : 0xFFFFFFFFu;  // pads sort after every column
+      v[i] = idx;
     }
+    Sort(ts.sort).Sort(k, v, 0, end_bit);  // blocked: thread tid holds sorted [tid*IT, tid*IT+IT)
+    last[tid] = k[IT - 1];
+    __syncthreads();
+    int f[IT], r[IT];
+    uint32_t prev = tid ? last[tid - 1] : 0u;
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+      const int p = tid * IT + i;
+      f[i] = (p < n && (p == 0 || k[i] != prev)) ? 1 : 0;
+      prev = k[i];
+    }
+    int total;
+    Scan(ts.scan).ExclusiveSum(f, r, total);
+#pragma unroll
+    for (int i = 0; i < IT; ++i) {
+      if (tid * IT + i < n) {
+        const int rk = r[i] + f[i] - 1;
+        if (f[i]) stage_uniq[e0 + rk] = (int32_t)k[i];
+        stage_rank[e0 + v[i]] = rk;
+      }
+    }
+    if (tid == 0) ncols_out[w] = total;
+    __syncthreads();  // shared memory is reused by the next window
   }
 }
 
-__global__ void k_count_heads(const uint64_t* __restrict__ keys, int64_t nnz, int64_t* __restrict__ ncols) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (; i < nnz; i += stride) {
-    uint64_t k = keys[i];
-    if (i == 0 || keys[i - 1] != k) atomicAdd(reinterpret_cast<unsigned long long*>(&ncols[k >> 32]), 1ull);
+template <int TH, int IT>
+static int launch_win_sort(int64_t W, const int32_t* woff, const int32_t* col, int lo, int end_bit, int64_t* ncols,
+                           int32_t* rank, int32_t* uniq, cudaStream_t st) {
+  auto kern = k_win_sort<TH, IT>;
+  int per_sm = 0;
+  HCS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TH, 0));
+  const int64_t grid = std::min<int64_t>(W, (int64_t)num_sms() * std::max(per_sm, 1));
+  kern<<<(int)grid, TH, 0, st>>>(W, woff, col, lo, end_bit, ncols, rank, uniq);
+  HCS_LAUNCH_CHECK("k_win_sort");
+  return HCS_OK;
+}
+
+// windows above kCtaSortMax entries: list + segment bounds for the segmented sort
+__global__ void k_big_flags(int64_t W, const int32_t* __restrict__ woff, int64_t* __restrict__ bidx) {
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (w >= W) return;
+  bidx[w + 1] = (woff[w + 1] - woff[w]) > kCtaSortMax ? 1 : 0;
+  if (w == 0) bidx[0] = 0;
+}
+
+// after the inclusive scan bidx[w] = number of big windows before w
+__global__ void k_big_list(int64_t W, const int32_t* __restrict__ woff, const int64_t* __restrict__ bidx,
+                           int32_t* __restrict__ big_w, int32_t* __restrict__ seg_b, int32_t* __restrict__ seg_e) {
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (w >= W || bidx[w + 1] == bidx[w]) return;
+  const int64_t j = bidx[w];
+  big_w[j] = (int32_t)w;
+  seg_b[j] = woff[w];
+  seg_e[j] = woff[w + 1];
+}
+
+constexpr int kWalkThreads = 256, kWalkItems = 4;
+__global__ void __launch_bounds__(kWalkThreads) k_big_walk(int64_t nbig, const int32_t* __restrict__ big_w,
+                                                           const int32_t* __restrict__ woff,
+                                                           const uint32_t* __restrict__ keys,
+                                                           const int32_t* __restrict__ vals,
+                                                           int64_t* __restrict__ ncols_out,
+                                                           int32_t* __restrict__ stage_rank,
+                                                           int32_t* __restrict__ stage_uniq) {
+  using Scan = cub::BlockScan<int, kWalkThreads>;
+  __shared__ typename Scan::TempStorage ts;
+  for (int64_t j = blockIdx.x; j < nbig; j += gridDim.x) {
+    const int64_t w = big_w[j];
+    const int32_t s0 = woff[w], s1 = woff[w + 1];
+    int running = 0;
+    for (int32_t c = s0; c < s1; c += kWalkThreads * kWalkItems) {
+      uint32_t k[kWalkItems];
+      int f[kWalkItems], r[kWalkItems];
+      const int32_t p0 = c + threadIdx.x * kWalkItems;
+      uint32_t prev = (p0 > s0 && p0 < s1) ? keys[p0 - 1] : 0u;
+#pragma unroll
+      for (int i = 0; i < kWalkItems; ++i) {
+        const int32_t p = p0 + i;
+        k[i] = p < s1 ? keys[p] : 0u;
+        f[i] = (p < s1 && (p == s0 || k[i] != prev)) ? 1 : 0;
+        prev = k[i];
+      }
+      int agg;
+      Scan(ts).ExclusiveSum(f, r, agg);
+#pragma unroll
+      for (int i = 0; i < kWalkItems; ++i) {
+        const int32_t p = p0 + i;
+        if (p < s1) {
+          const int rk = running + r[i] + f[i] - 1;
+          if (f[i]) stage_uniq[s0 + rk] = (int32_t)k[i];
+          stage_rank[vals[p]] = rk;
+        }
+      }
+      running += agg;
+      __syncthreads();  // scan storage reuse
+    }
+    if (threadIdx.x == 0) ncols_out[w] = running;
   }
 }
 
-__global__ void k_flags(const uint64_t* __restrict__ keys, int64_t nnz, int32_t* __restrict__ flags) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (; i < nnz; i += stride) flags[i] = (i == 0 || keys[i - 1] != keys[i]) ? 1 : 0;
-}
-
-__global__ void k_fill_sorted(const uint64_t* __restrict__ keys, const int32_t* __restrict__ pos,
-                              const int32_t* __restrict__ uid_incl, int64_t nnz,
-                              const int64_t* __restrict__ win_col_ptr, int32_t* __restrict__ nonzero_cols,
-                              int32_t* __restrict__ cond) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (; i < nnz; i += stride) {
-    uint64_t k = keys[i];
-    int64_t g = (int64_t)uid_incl[i] - 1;  // global unique index
-    int64_t win = (int64_t)(k >> 32);
-    int64_t r = g - win_col_ptr[win];
-    if (i == 0 || keys[i - 1] != k) nonzero_cols[g] = (int32_t)(uint32_t)(k & 0xffffffffu);
-    cond[pos[i]] = (int32_t)r;
+// nonzero_cols of window w = its staged unique columns (one CTA per window, 4 loads in flight)
+__global__ void __launch_bounds__(256) k_win_emit(int64_t W, const int32_t* __restrict__ woff,
+                                                  const int64_t* __restrict__ wcp,
+                                                  const int32_t* __restrict__ stage_uniq,
+                                                  int32_t* __restrict__ nonzero_cols) {
+  for (int64_t w = blockIdx.x; w < W; w += gridDim.x) {
+    const int64_t b = wcp[w], n = wcp[w + 1] - b;
+    const int32_t* src = stage_uniq + woff[w];
+    for (int64_t i0 = 0; i0 < n; i0 += 4 * 256) {
+      int32_t t[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = i0 + u * 256 + threadIdx.x;
+        t[u] = i < n ? src[i] : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = i0 + u * 256 + threadIdx.x;
+        if (i < n) nonzero_cols[b + i] = t[u];
+      }
+    }
   }
 }
 
@@ -266,41 +389,46 @@ static Selector make_selector(const double* s) {
   return sel;
 }
 
+// sort-path workspace (after the scan temp storage): key/value double buffers of the
+// segmented sort, the staged ranks / unique columns, window offsets, big-window list,
+// CUB temp storage
 struct SortWs {
-  uint64_t* keys_a; uint64_t* keys_b; int32_t* vals_a; int32_t* vals_b; void* cub_tmp; size_t cub_bytes;
+  uint32_t* keys_a; uint32_t* keys_b; int32_t* vals_a; int32_t* vals_b; int32_t* rank; int32_t* uniq;
+  int32_t* woff; int64_t* bidx; int32_t* big_w; int32_t* seg_b; int32_t* seg_e; void* cub_tmp; size_t cub_bytes;
 };
-
-static int key_bits(int64_t W) {
-  int b = 1;
-  while ((1LL << b) < W) ++b;
-  return 32 + b;
-}
-
-static size_t cub_sort_bytes(int64_t nnz, int64_t W) {
-  size_t sort_bytes = 0, scan_bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, (uint64_t*)nullptr, (uint64_t*)nullptr, (int32_t*)nullptr,
-                                  (int32_t*)nullptr, (int)nnz, 0, key_bits(W));
-  cub::DeviceScan::InclusiveSum(nullptr, scan_bytes, (int32_t*)nullptr, (int32_t*)nullptr, (int)nnz);
-  size_t s2 = 0;
-  cub::DeviceScan::InclusiveSum(nullptr, s2, (int64_t*)nullptr, (int64_t*)nullptr, (int)(W + 1));
-  return std::max(std::max(sort_bytes, scan_bytes), s2);
-}
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
+static size_t cub_seg_bytes(int64_t nnz, int64_t W) {
+  size_t b = 0, c = 0;
+  cub::DoubleBuffer<uint32_t> k(nullptr, nullptr);
+  cub::DoubleBuffer<int32_t> v(nullptr, nullptr);
+  cub::DeviceSegmentedRadixSort::SortPairs(nullptr, b, k, v, (int)nnz, (int)W, (const int32_t*)nullptr,
+                                           (const int32_t*)nullptr, 0, 32);
+  cub::DeviceScan::InclusiveSum(nullptr, c, (int64_t*)nullptr, (int64_t*)nullptr, (int)(W + 1));
+  return std::max(b, c);
+}
+
 static size_t sort_ws_bytes(int64_t nnz, int64_t W) {
-  return align_up(nnz * 8) * 2 + align_up(nnz * 4) * 2 + align_up(cub_sort_bytes(nnz, W));
+  return align_up(nnz * 4) * 6 + align_up((W + 1) * 4) * 4 + align_up((W + 1) * 8) + align_up(cub_seg_bytes(nnz, W));
 }
 
 static SortWs carve(void* ws, int64_t nnz, int64_t W) {
   SortWs s{};
   char* p = (char*)ws;
-  s.keys_a = (uint64_t*)p; p += align_up(nnz * 8);
-  s.keys_b = (uint64_t*)p; p += align_up(nnz * 8);
+  s.keys_a = (uint32_t*)p; p += align_up(nnz * 4);
+  s.keys_b = (uint32_t*)p; p += align_up(nnz * 4);
   s.vals_a = (int32_t*)p; p += align_up(nnz * 4);
   s.vals_b = (int32_t*)p; p += align_up(nnz * 4);
+  s.rank = (int32_t*)p; p += align_up(nnz * 4);
+  s.uniq = (int32_t*)p; p += align_up(nnz * 4);
+  s.woff = (int32_t*)p; p += align_up((W + 1) * 4);
+  s.big_w = (int32_t*)p; p += align_up((W + 1) * 4);
+  s.seg_b = (int32_t*)p; p += align_up((W + 1) * 4);
+  s.seg_e = (int32_t*)p; p += align_up((W + 1) * 4);
+  s.bidx = (int64_t*)p; p += align_up((W + 1) * 8);
   s.cub_tmp = p;
-  s.cub_bytes = cub_sort_bytes(nnz, W);
+  s.cub_bytes = cub_seg_bytes(nnz, W);
   return s;
 }
 
@@ -362,15 +490,38 @@ int hcs_partition_count(const int64_t* row_ptr, const int32_t* col_idx, int64_t 
       HCS_LAUNCH_CHECK("k_count_bitmap");
     } else {
       SortWs s = carve((char*)workspace + scan_bytes, nnz, W);
-      int grid = std::min<int64_t>((n_rows + 7) / 8, (int64_t)num_sms() * 16);
-      k_make_keys<<<grid, 256, 0, st>>>(row_ptr, col_idx, n_rows, wh, s.keys_a, s.vals_a);
-      HCS_LAUNCH_CHECK("k_make_keys");
+      const int g = (int)std::min<int64_t>((std::max(nnz, W + 1) + 255) / 256, (int64_t)num_sms() * 16);
+      k_win_offsets<<<g, 256, 0, st>>>(row_ptr, n_rows, wh, W, s.woff, s.vals_a, nnz);
+      HCS_LAUNCH_CHECK("k_win_offsets");
+      int end_bit = 1;
+      while ((1LL << end_bit) <= n_cols) ++end_bit;  // every column < 2^end_bit - 1 = the pad key's bits
+      int64_t* ncols = win_col_ptr + 1;
+      rc = launch_win_sort<32, 4>(W, s.woff, col_idx, 0, end_bit, ncols, s.rank, s.uniq, st);
+      if (rc == HCS_OK) rc = launch_win_sort<64, 8>(W, s.woff, col_idx, 128, end_bit, ncols, s.rank, s.uniq, st);
+      if (rc == HCS_OK) rc = launch_win_sort<128, 8>(W, s.woff, col_idx, 512, end_bit, ncols, s.rank, s.uniq, st);
+      if (rc != HCS_OK) return rc;
+      const int g1 = (int)((W + 255) / 256);
+      k_big_flags<<<g1, 256, 0, st>>>(W, s.woff, s.bidx);
+      HCS_LAUNCH_CHECK("k_big_flags");
       size_t tb = s.cub_bytes;
-      HCS_CUDA(cub::DeviceRadixSort::SortPairs(s.cub_tmp, tb, s.keys_a, s.keys_b, s.vals_a, s.vals_b, (int)nnz, 0,
-                                               key_bits(W), st));
-      int g2 = std::min<int64_t>((nnz + 255) / 256, (int64_t)num_sms() * 16);
-      k_count_heads<<<g2, 256, 0, st>>>(s.keys_b, nnz, win_col_ptr + 1);
-      HCS_LAUNCH_CHECK("k_count_heads");
+      HCS_CUDA(cub::DeviceScan::InclusiveSum(s.cub_tmp, tb, s.bidx, s.bidx, (int)(W + 1), st));
+      k_big_list<<<g1, 256, 0, st>>>(W, s.woff, s.bidx, s.big_w, s.seg_b, s.seg_e);
+      HCS_LAUNCH_CHECK("k_big_list");
+      int64_t nbig = 0;
+      HCS_CUDA(cudaMemcpyAsync(&nbig, s.bidx + W, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      HCS_CUDA(cudaStreamSynchronize(st));  // CUB's segment count is a host argument
+      if (nbig > 0) {
+        HCS_CUDA(cudaMemcpyAsync(s.keys_a, col_idx, nnz * 4, cudaMemcpyDeviceToDevice, st));
+        cub::DoubleBuffer<uint32_t> keys(s.keys_a, s.keys_b);
+        cub::DoubleBuffer<int32_t> vals(s.vals_a, s.vals_b);
+        tb = s.cub_bytes;
+        HCS_CUDA(cub::DeviceSegmentedRadixSort::SortPairs(s.cub_tmp, tb, keys, vals, (int)nnz, (int)nbig, s.seg_b,
+                                                          s.seg_e, 0, end_bit, st));
+        const int gw = (int)std::min<int64_t>(nbig, (int64_t)num_sms() * 8);
+        k_big_walk<<<gw, kWalkThreads, 0, st>>>(nbig, s.big_w, s.woff, keys.Current(), vals.Current(), ncols, s.rank,
+                                                s.uniq);
+        HCS_LAUNCH_CHECK("k_big_walk");
+      }
     }
   }
   size_t sb = scan_bytes;
@@ -401,16 +552,11 @@ int hcs_partition_fill(const int64_t* row_ptr, const int32_t* col_idx, int64_t n
                                                           nonzero_cols, cond_cols);
     HCS_LAUNCH_CHECK("k_fill_bitmap");
   } else {
-    size_t scan_bytes = scan_ws_bytes(W);
-    SortWs s = carve((char*)workspace + scan_bytes, nnz, W);
-    int g2 = std::min<int64_t>((nnz + 255) / 256, (int64_t)num_sms() * 16);
-    int32_t* flags = s.vals_a;  // vals_a is free after the sort (sorted positions live in vals_b)
-    k_flags<<<g2, 256, 0, st>>>(s.keys_b, nnz, flags);
-    HCS_LAUNCH_CHECK("k_flags");
-    size_t tb = s.cub_bytes;
-    HCS_CUDA(cub::DeviceScan::InclusiveSum(s.cub_tmp, tb, flags, flags, (int)nnz, st));
-    k_fill_sorted<<<g2, 256, 0, st>>>(s.keys_b, s.vals_b, flags, nnz, win_col_ptr, nonzero_cols, cond_cols);
-    HCS_LAUNCH_CHECK("k_fill_sorted");
+    SortWs s = carve((char*)workspace + scan_ws_bytes(W), nnz, W);  // staged by hcs_partition_count
+    HCS_CUDA(cudaMemcpyAsync(cond_cols, s.rank, nnz * 4, cudaMemcpyDeviceToDevice, st));
+    const int g = (int)std::min<int64_t>(W, (int64_t)num_sms() * 8);
+    k_win_emit<<<g, 256, 0, st>>>(W, s.woff, win_col_ptr, s.uniq, nonzero_cols);
+    HCS_LAUNCH_CHECK("k_win_emit");
   }
   return HCS_OK;
 }
