@@ -11,7 +11,8 @@ __version__ = "0.1.0"
 from .errors import FormatError, InvariantError  # noqa: F401
 from .matrices import DenseMatrix, DeviceCsr, Graph, SparseCsr, graph_from_edges, to_device_csr  # noqa: F401
 from .executors import (  # noqa: F401
-    Assignment, ExecStats, Path, SpmmGraph, SpmmResult, spmm_auto, spmm_hybrid, spmm_scalar, spmm_tile,
+    Assignment, ExecStats, Path, SpmmGraph, SpmmRequest, SpmmResult, spmm_auto, spmm_hybrid, spmm_hybrid_async,
+    spmm_scalar, spmm_tile,
 )
 from .windows import (  # noqa: F401
     TILE_COLS, TILE_DIM, WINDOW_HEIGHT, RowWindow, WindowFeatures, WindowSet, features, partition,

@@ -408,6 +408,85 @@ def _run_host_pipelined(plan, xop, z, ldz, host_kind, stats) -> SpmmResult:
     return SpmmResult(DenseMatrix(host if host_kind == "torch" else host.numpy()), stats)
 
 
+_H2D_STREAMS: dict = {}
+
+
+class SpmmRequest:
+    """A host-memory hybrid SpMM in flight (spmm_hybrid_async).  result() waits for the
+    request's last D2H copy and returns what spmm_hybrid would have returned."""
+
+    def __init__(self, host: torch.Tensor, done: torch.cuda.Event, host_kind, stats: ExecStats):
+        self._host, self._done, self._kind, self._stats = host, done, host_kind, stats
+
+    def done(self) -> bool:
+        return self._done.query()
+
+    def result(self) -> SpmmResult:
+        self._done.synchronize()
+        h = self._host
+        return SpmmResult(DenseMatrix(h if self._kind == "torch" else h.numpy()), self._stats)
+
+
+def spmm_hybrid_async(windows, assignment: Assignment, x, precision: str = "bf16",
+                      out: torch.Tensor | None = None) -> SpmmRequest:
+    """spmm_hybrid for a HOST operand, returning before the product is done, so consecutive
+    requests overlap: request i+1's X upload (H2D stream) runs under request i's kernels, and
+    each request's Z rows stream back (copy stream) while its later row ranges compute.  The
+    kernels, the row ranges and therefore the results are those of spmm_hybrid.  Pinned host
+    memory makes the copies asynchronous; a request's X must not be modified before result().
+    `out`: optional pinned fp32 host tensor of at least (rows, dim) for Z (a caller-owned ring of
+    result buffers avoids a pinned allocation per request)."""
+    from .windows import as_windowset
+
+    if len(assignment) != len(windows):
+        raise ValueError(f"assignment covers {len(assignment)} windows, expected {len(windows)}")
+    precision = _resolve_precision(precision)
+    ws = as_windowset(windows)
+    xrows = x.rows if isinstance(x, DenseMatrix) else int(x.shape[0])
+    _check_window_bounds(ws, xrows)
+    dev = ws.csr.device
+    plan = get_plan(ws, assignment, precision)
+    data = x.data if isinstance(x, DenseMatrix) else x
+    if isinstance(data, torch.Tensor) and data.is_cuda:
+        raise ValueError("spmm_hybrid_async takes a host operand; use spmm_hybrid for device tensors")
+    h2d = _H2D_STREAMS.get(dev)
+    if h2d is None:
+        h2d = _H2D_STREAMS[dev] = torch.cuda.Stream(device=dev)
+    cs = _COPY_STREAMS.get(dev)
+    if cs is None:
+        cs = _COPY_STREAMS[dev] = torch.cuda.Stream(device=dev)
+    cur = torch.cuda.current_stream(dev)
+    with torch.cuda.stream(h2d):  # the upload does not wait for earlier requests' kernels
+        xop, _ = stage_operand(x, precision, dev, tf32_round=(precision == "tf32" and plan.n_tile > 0))
+        up = torch.cuda.Event()
+        up.record(h2d)
+    cur.wait_event(up)
+    xop.t.record_stream(cur)
+    z, ldz = _alloc_z(ws.num_rows, xop.dim, dev)
+    dim, wh, n = xop.dim, plan.windows.window_height, z.shape[0]
+    if out is None:
+        host = torch.empty((n, dim), dtype=torch.float32, pin_memory=True)
+    else:
+        if out.is_cuda or out.dtype != torch.float32 or out.shape[0] < n or out.shape[1] < dim:
+            raise ValueError(f"out must be a host float32 tensor of at least ({n}, {dim})")
+        host = out[:n, :dim]
+    W = len(ws)
+    parts = plan.parts(HOST_PIPELINE_PARTS) if W >= HOST_PIPELINE_MIN_WINDOWS else [None]
+    for part in parts:
+        plan.run(xop, z, ldz, part=part)
+        r0, r1 = (min(part[0] * wh, n), min(part[1] * wh, n)) if part is not None else (0, n)
+        if r1 > r0:
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            cs.wait_event(ev)
+            with torch.cuda.stream(cs):
+                host[r0:r1].copy_(z[r0:r1, :dim], non_blocking=True)
+    done = torch.cuda.Event()
+    done.record(cs)
+    z.record_stream(cs)
+    return SpmmRequest(host, done, _host_kind(x), ExecStats(**plan.stats.as_dict()))
+
+
 class SpmmGraph:
     """A hybrid SpMM captured once as a CUDA graph and replayed: for repeated products with
     the same windows, assignment and X buffer (small graphs, where the 2-3 kernel launches of

@@ -259,6 +259,45 @@ def test_host_pipelined_path(cuda_ok):
     assert host.stats == dev.stats
 
 
+@pytest.mark.parametrize("big", [False, True])
+def test_async_requests_match_sync(cuda_ok, big):
+    """spmm_hybrid_async with three requests in flight (different X each, pinned torch and
+    numpy inputs) returns exactly what spmm_hybrid returns for each of them."""
+    import gen_graphs as gg
+
+    n, rr, cc = gg.power_law(70000 if big else 3000, 24.0, seed=5)
+    adj = orc.from_coo(n, n, rr, cc, np.ones(len(rr)))
+    a = orc.normalize_adj(adj, "gcn")
+    ws = hc.partition(to_hc(a))
+    asg = hc.classify_windows(hc.default_model(), ws)
+    xs = [orc.random_dense(n, d, seed=10 + i) for i, d in enumerate((64, 128, 40))]
+    ins = [hc.DenseMatrix(xs[0]), torch.from_numpy(xs[1]).to(torch.bfloat16).pin_memory(),
+           torch.from_numpy(xs[2]).float()]
+    reqs = [hc.spmm_hybrid_async(ws, asg, x) for x in ins]
+    got = [r.result() for r in reqs]
+    for x, g in zip(ins, got):
+        want = hc.spmm_hybrid(ws, asg, x)
+        assert type(g.z.data) is type(want.z.data)
+        gz = g.z.data if isinstance(g.z.data, np.ndarray) else g.z.data.numpy()
+        wz = want.z.data if isinstance(want.z.data, np.ndarray) else want.z.data.numpy()
+        assert np.array_equal(gz, wz)
+        assert g.stats == want.stats
+    assert orc.max_rel_err(got[0].z.data, orc.spmm_exact(a, xs[0])) <= BF16_TOL
+    # caller-owned pinned result buffers (a ring of two, three requests)
+    ring = [torch.full((n + 3, 130), float("nan")).pin_memory() for _ in range(2)]
+    reqs = [hc.spmm_hybrid_async(ws, asg, ins[1], out=ring[0]), hc.spmm_hybrid_async(ws, asg, ins[2], out=ring[1])]
+    z1 = reqs[0].result().z.data.clone()
+    reqs.append(hc.spmm_hybrid_async(ws, asg, ins[0], out=ring[0]))
+    z2, z0 = reqs[1].result().z.data, reqs[2].result().z.data
+    as_np = lambda v: v if isinstance(v, np.ndarray) else v.numpy()  # noqa: E731
+    for gz, x in ((z1, ins[1]), (z2, ins[2]), (z0, ins[0])):
+        assert np.array_equal(as_np(gz), as_np(hc.spmm_hybrid(ws, asg, x).z.data))
+    with pytest.raises(ValueError, match="out must be"):
+        hc.spmm_hybrid_async(ws, asg, ins[1], out=torch.empty(n, 8))
+    with pytest.raises(ValueError, match="host operand"):
+        hc.spmm_hybrid_async(ws, asg, torch.zeros(n, 8, device="cuda"))
+
+
 @pytest.mark.parametrize("variant", ["auto", "block", "warp16"])
 @pytest.mark.parametrize("precision", ["bf16", "tf32"])
 def test_scalar_variants(cuda_ok, variant, precision):
