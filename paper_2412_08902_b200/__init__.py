@@ -19,3 +19,4 @@ from .windows import (  # noqa: F401
     tile_count, total_rows,
 )
 from .selector import SelectorModel, b200_model, classify, classify_windows, default_model, load_model  # noqa: F401
+from . import ops  # noqa: F401,E402  (registers torch.ops.hcspmm.spmm / gcn_layer)

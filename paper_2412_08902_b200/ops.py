@@ -1,0 +1,144 @@
+"""PyTorch custom operators over the C ABI (BASELINE north_star: the reference's SpMM and
+GCN-layer entry points "exposed as a PyTorch custom op over a thin C-ABI").
+
+    torch.ops.hcspmm.spmm(row_ptr, col_idx, values, num_cols, x, precision) -> Z
+        Z = A X (executors.py:234-251 spmm_hybrid: windows, default selector, hybrid kernels);
+        differentiable in X: dX = A^T dZ (the values are constants, as in the reference GCN).
+    torch.ops.hcspmm.gcn_layer(row_ptr, col_idx, values, num_cols, x, w, precision) -> (out, z)
+        out = (A X) W with z = A X (gnn.py:121-159 forward, fused SpMM+GEMM kernels);
+        differentiable in X and W: dW = z^T dout, dX = A^T (dout W^T) (gnn.py:162-205 backward).
+
+The CSR is passed as plain tensors (row_ptr int64 [n+1], col_idx int32/int64 [nnz], values
+[nnz]) so the ops compose with torch code; the windows, selector decisions, K2 plan and A^T are
+derived once per operator and cached (keyed by the tensors' storage and version counters).
+There is no CPU kernel: on a tensor that is not on a CUDA device the ops raise.
+"""
+
+from __future__ import annotations
+
+from collections import OrderedDict
+
+import torch
+
+from . import _lib
+from .executors import spmm_hybrid
+from .fused import fused_aggregate_update, grad_weight
+from .gnn import transpose_csr
+from .matrices import DeviceCsr
+from .selector import classify_windows, default_model
+from .windows import partition
+
+_CACHE_SIZE = 8
+_OPERATORS: "OrderedDict[tuple, DeviceCsr]" = OrderedDict()
+
+
+def _operator(row_ptr: torch.Tensor, col_idx: torch.Tensor, values: torch.Tensor, num_cols: int) -> DeviceCsr:
+    if not (row_ptr.is_cuda and col_idx.is_cuda and values.is_cuda):
+        raise ValueError("hcspmm ops take CUDA tensors (there is no CPU kernel)")
+    if row_ptr.dim() != 1 or col_idx.dim() != 1 or values.shape != col_idx.shape:
+        raise ValueError("row_ptr, col_idx, values must be 1-D with len(values) == len(col_idx)")
+    key = (row_ptr.data_ptr(), col_idx.data_ptr(), values.data_ptr(), int(row_ptr.numel()), int(col_idx.numel()),
+           int(num_cols), row_ptr._version, col_idx._version, values._version, str(row_ptr.device))
+    a = _OPERATORS.get(key)
+    if a is None:
+        a = DeviceCsr(int(row_ptr.numel()) - 1, int(num_cols), row_ptr.to(torch.int64).contiguous(),
+                      col_idx.to(torch.int32).contiguous(), values.to(torch.float32).contiguous())
+        _OPERATORS[key] = a
+        while len(_OPERATORS) > _CACHE_SIZE:
+            _OPERATORS.popitem(last=False)
+    else:
+        _OPERATORS.move_to_end(key)
+    return a
+
+
+def _windows(a: DeviceCsr):
+    ws = partition(a)
+    return ws, classify_windows(default_model(), ws)
+
+
+def _check_x(a: DeviceCsr, x: torch.Tensor) -> None:
+    if not x.is_cuda:
+        raise ValueError("hcspmm ops take CUDA tensors (there is no CPU kernel)")
+    if x.dim() != 2 or int(x.shape[0]) != a.num_cols:
+        raise ValueError(f"X has {tuple(x.shape)} but the matrix has {a.num_cols} columns")
+
+
+# ----------------------------------------------------------------------------- spmm
+@torch.library.custom_op("hcspmm::spmm", mutates_args=())
+def spmm(row_ptr: torch.Tensor, col_idx: torch.Tensor, values: torch.Tensor, num_cols: int, x: torch.Tensor,
+         precision: str = "bf16") -> torch.Tensor:
+    _lib.lib()  # the extension must be loaded: no fallback
+    a = _operator(row_ptr, col_idx, values, num_cols)
+    _check_x(a, x)
+    ws, asg = _windows(a)
+    return spmm_hybrid(ws, asg, x.detach(), precision=precision).z.data.contiguous()
+
+
+@spmm.register_fake
+def _spmm_fake(row_ptr, col_idx, values, num_cols, x, precision="bf16"):
+    return x.new_empty((row_ptr.shape[0] - 1, x.shape[1]), dtype=torch.float32)
+
+
+def _spmm_setup(ctx, inputs, output):
+    row_ptr, col_idx, values, num_cols, x, precision = inputs
+    ctx.save_for_backward(row_ptr, col_idx, values)
+    ctx.num_cols, ctx.precision, ctx.x_dtype = num_cols, precision, x.dtype
+
+
+def _spmm_backward(ctx, grad):
+    row_ptr, col_idx, values = ctx.saved_tensors
+    gx = None
+    if ctx.needs_input_grad[4]:
+        at = transpose_csr(_operator(row_ptr, col_idx, values, ctx.num_cols))
+        ws, asg = _windows(at)
+        gx = spmm_hybrid(ws, asg, grad.contiguous(), precision=ctx.precision).z.data.to(ctx.x_dtype).contiguous()
+    return None, None, None, None, gx, None
+
+
+spmm.register_autograd(_spmm_backward, setup_context=_spmm_setup)
+
+
+# ----------------------------------------------------------------------------- gcn layer
+@torch.library.custom_op("hcspmm::gcn_layer", mutates_args=())
+def gcn_layer(row_ptr: torch.Tensor, col_idx: torch.Tensor, values: torch.Tensor, num_cols: int, x: torch.Tensor,
+              w: torch.Tensor, precision: str = "bf16") -> tuple[torch.Tensor, torch.Tensor]:
+    _lib.lib()
+    a = _operator(row_ptr, col_idx, values, num_cols)
+    _check_x(a, x)
+    if w.dim() != 2 or int(w.shape[0]) != int(x.shape[1]):
+        raise ValueError(f"W has {tuple(w.shape)}, X has {int(x.shape[1])} features")
+    ws, asg = _windows(a)
+    out, z = fused_aggregate_update(ws, asg, x.detach(), w.detach(), precision, want_z=True)
+    return out.contiguous(), z.contiguous()
+
+
+@gcn_layer.register_fake
+def _gcn_fake(row_ptr, col_idx, values, num_cols, x, w, precision="bf16"):
+    n = row_ptr.shape[0] - 1
+    return (x.new_empty((n, w.shape[1]), dtype=torch.float32), x.new_empty((n, x.shape[1]), dtype=torch.float32))
+
+
+def _gcn_setup(ctx, inputs, output):
+    row_ptr, col_idx, values, num_cols, x, w, precision = inputs
+    ctx.save_for_backward(row_ptr, col_idx, values, w, output[1])
+    ctx.num_cols, ctx.precision, ctx.x_dtype = num_cols, precision, x.dtype
+
+
+def _gcn_backward(ctx, g_out, g_z):
+    row_ptr, col_idx, values, w, z = ctx.saved_tensors
+    gx = gw = None
+    g = g_out.contiguous() if g_out is not None else torch.zeros(z.shape[0], w.shape[1], device=z.device)
+    if ctx.needs_input_grad[5]:
+        gw = grad_weight(z, g).to(w.dtype)  # dW = z^T dout (gnn.py:188-189), deterministic split-K
+    if ctx.needs_input_grad[4]:
+        at = transpose_csr(_operator(row_ptr, col_idx, values, ctx.num_cols))
+        ws, asg = _windows(at)
+        # dX = A^T (dout W^T): aggregate dout, then the on-chip product with W^T (K7)
+        gx, _ = fused_aggregate_update(ws, asg, g, w.detach().t(), ctx.precision, want_z=False)
+        if g_z is not None:  # z = A X is an output too: its gradient adds A^T dz
+            gx = gx + spmm_hybrid(ws, asg, g_z.contiguous(), precision=ctx.precision).z.data
+        gx = gx.to(ctx.x_dtype).contiguous()
+    return None, None, None, None, gx, gw, None
+
+
+gcn_layer.register_autograd(_gcn_backward, setup_context=_gcn_setup)

@@ -122,3 +122,4 @@ def test_large_random_files_match(tmp_path):
     epath = write(tmp_path, "big.txt", "".join(f"{a} {b}\n" for a, b in zip(i, j)))
     u, v, _ = io.parse_edge_arrays(epath)
     assert np.array_equal(u, i - 1) and np.array_equal(v, j - 1)
+
