@@ -29,7 +29,7 @@ from .selector import classify_windows, default_model
 from .windows import partition
 
 _CACHE_SIZE = 8
-_OPERATORS: "OrderedDict[tuple, DeviceCsr]" = OrderedDict()
+_OPERATORS: "OrderedDict[tuple, tuple]" = OrderedDict()
 
 
 def _operator(row_ptr: torch.Tensor, col_idx: torch.Tensor, values: torch.Tensor, num_cols: int) -> DeviceCsr:
@@ -39,16 +39,18 @@ def _operator(row_ptr: torch.Tensor, col_idx: torch.Tensor, values: torch.Tensor
         raise ValueError("row_ptr, col_idx, values must be 1-D with len(values) == len(col_idx)")
     key = (row_ptr.data_ptr(), col_idx.data_ptr(), values.data_ptr(), int(row_ptr.numel()), int(col_idx.numel()),
            int(num_cols), row_ptr._version, col_idx._version, values._version, str(row_ptr.device))
-    a = _OPERATORS.get(key)
-    if a is None:
+    hit = _OPERATORS.get(key)
+    if hit is None:
         a = DeviceCsr(int(row_ptr.numel()) - 1, int(num_cols), row_ptr.to(torch.int64).contiguous(),
                       col_idx.to(torch.int32).contiguous(), values.to(torch.float32).contiguous())
-        _OPERATORS[key] = a
+        # the entry keeps the caller's tensors alive, so their addresses cannot be reused by other
+        # tensors while the entry exists (a key match is the same storage; versions catch writes)
+        _OPERATORS[key] = (a, (row_ptr, col_idx, values))
         while len(_OPERATORS) > _CACHE_SIZE:
             _OPERATORS.popitem(last=False)
-    else:
-        _OPERATORS.move_to_end(key)
-    return a
+        return a
+    _OPERATORS.move_to_end(key)
+    return hit[0]
 
 
 def _windows(a: DeviceCsr):

@@ -99,3 +99,16 @@ def test_opcheck(cuda_ok):
     tests = ("test_schema", "test_faketensor", "test_autograd_registration")
     torch.library.opcheck(torch.ops.hcspmm.spmm.default, (*csr, x, "bf16"), test_utils=tests)
     torch.library.opcheck(torch.ops.hcspmm.gcn_layer.default, (*csr, x, w, "bf16"), test_utils=tests)
+
+
+def test_operator_cache_follows_in_place_writes(cuda_ok):
+    """Windows/plans are cached per operator; an in-place write to the values (version
+    counter) gives a fresh operator: doubling every value doubles Z exactly."""
+    a = plaw8k_csr()
+    d, (rp, ci, v, nc) = _tensors(a)
+    v = v.clone()
+    x = torch.from_numpy(orc.random_dense(a.num_cols, 16, seed=11)).float().cuda()
+    z1 = torch.ops.hcspmm.spmm(rp, ci, v, nc, x, "bf16")
+    v.mul_(2)
+    z2 = torch.ops.hcspmm.spmm(rp, ci, v, nc, x, "bf16")
+    assert torch.equal(z2, 2 * z1)
