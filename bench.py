@@ -66,6 +66,7 @@ def parse():
 # 256-B rows from a 60 MB L2-resident table, 48 warps/SM, 19.47 TB/s)
 GATHER_PEAK_GBPS = 19470.0
 E2E_IN_FLIGHT = 2  # outstanding spmm_hybrid_async requests in the e2e measurement
+EXTRA: dict = {}  # multi-GPU timings added to the JSON line
 
 
 def peaks():
@@ -322,9 +323,23 @@ def run_ours(args):
         # per-kernel time only on one GPU (with N ranks the step is split into parts)
         tile_ms = statistics.mean(a.elapsed_time(b) for a, b in tev) if (plan.n_tile and world == 1) else 0.0
         if world > 1:
-            t = torch.tensor([ms, tile_ms], device=dev if not gloo else "cpu", dtype=torch.float64)
+            # the same shard's SpMM alone (no exchange), so the line reports both "SpMM only" and
+            # "SpMM + all-gather", max over ranks
+            dist.barrier()
+            torch.cuda.synchronize()
+            a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a_ev.record()
+            for _ in range(steps):
+                plan.run(xop, z, ldz)
+            b_ev.record()
+            torch.cuda.synchronize()
+            spmm_only = a_ev.elapsed_time(b_ev) / steps
+            t = torch.tensor([ms, tile_ms, spmm_only], device=dev if not gloo else "cpu", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms, tile_ms = float(t[0]), float(t[1])
+            EXTRA["spmm_only_ms"] = float(t[2])
+            EXTRA["exchange"] = f"NCCL all-gather of bf16 rows in {nparts} parts, overlapped" if not gloo else \
+                f"gloo all-gather of bf16 rows in {nparts} parts (shared-GPU test mode)"
         e2e = None
         if with_e2e and world == 1:
             xh = x.cpu().pin_memory()
@@ -449,6 +464,8 @@ def run_ours(args):
     }
     if e2e is not None:
         out["e2e"] = e2e
+    if EXTRA:
+        out["multi_gpu"] = dict(EXTRA, spmm_plus_allgather_ms=ms)
     if args.sweep_dims and world == 1:
         sweep = {}
         for d in (32, 64, 128):
