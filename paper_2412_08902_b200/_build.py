@@ -23,6 +23,8 @@ INCLUDE = os.path.join(ROOT, "include")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
               "-Xptxas", "-warn-spills", "-I", INCLUDE]
+# experiments only (tools/exp_scalar_tune.sh): extra -D flags for kernel tuning constants
+NVCC_FLAGS += os.environ.get("HCS_NVCC_EXTRA", "").split()
 
 
 def nvcc() -> str:
