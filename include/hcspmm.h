@@ -113,6 +113,9 @@ int hcs_set_scalar_variant(int variant);
 int hcs_tile_scratch_floats(int64_t* floats);
 /* engine 2 row-slice width in 16-B vectors: 0 auto (8 for dim > 32, else 4), 4 or 8 */
 int hcs_set_tile_slice(int vectors);
+/* engine 2 fused GCN epilogue, one 33..48-feature slice: 1 (default) = kernel that skips the
+ * empty 16-feature group, 0 = the full 64-feature kernel (experiment switch) */
+int hcs_set_tile_npr3(int on);
 /* engine 2 with > 1 feature slice: 1 (default) = the FS warps of a group walk the same
  * (window, chunk) range, one slice each (plan read once, an X row's slices fetched together);
  * 0 = one warp per contiguous range of (window, slice, chunk); 2 = 1 only when X exceeds 96 MB.

@@ -47,6 +47,7 @@ _SIGS = {
                                      I64, P, SZ, P]),
     "hcs_tile_scratch_floats": (ctypes.c_int, [ctypes.POINTER(I64)]),
     "hcs_set_tile_slice": (ctypes.c_int, [ctypes.c_int]),
+    "hcs_set_tile_npr3": (ctypes.c_int, [ctypes.c_int]),
     "hcs_set_scalar_variant": (ctypes.c_int, [ctypes.c_int]),
     "hcs_set_tile_pairing": (ctypes.c_int, [ctypes.c_int]),
     "hcs_set_tile_plan_builder": (ctypes.c_int, [ctypes.c_int]),

@@ -29,6 +29,14 @@
 
 namespace hcs {
 
+// warps per CTA of the 32- / 64-feature-slice kernels (overridable for tuning sweeps:
+// tools/exp_tile_warps.sh); the 3-stage ring below is structural (P0..P3 rotation)
+#ifndef HCS_TILE_WARPS4
+#define HCS_TILE_WARPS4 12
+#endif
+#ifndef HCS_TILE_WARPS8
+#define HCS_TILE_WARPS8 8
+#endif
 constexpr int kWarpTileStages = 3;   // cp.async ring depth per warp
 constexpr int kWarpSlabBytes = 16 * 64 * 2;
 constexpr int kWarpEntRegs = 4;      // packed entries per lane held in registers (128 per chunk)
@@ -39,7 +47,7 @@ struct WarpCfg {
   static constexpr int kFeat = 8 * SWV;                  // features per slice
   static constexpr int kRowBytes = 16 * SWV;             // bytes per gathered row slice
   static constexpr int kStageBytes = 64 * kRowBytes;     // 64 rows (one chunk)
-  static constexpr int kWarps = SWV == 4 ? 12 : (SWV == 8 ? 8 : 4);  // warps per CTA (smem / register limited)
+  static constexpr int kWarps = SWV == 4 ? HCS_TILE_WARPS4 : (SWV == 8 ? HCS_TILE_WARPS8 : 4);  // warps per CTA (smem / register limited)
   static constexpr int kPerWarp = kWarpTileStages * kStageBytes + kWarpSlabBytes;
   static constexpr int kSmem = kWarps * kPerWarp + 128;
   static constexpr int kIssue = 2 * SWV;                 // cp.async instructions per chunk
@@ -258,7 +266,10 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
   auto issue = [&](const Pos& p, const int (&g)[NI], int slot) {
     if (p.rem > 0 && (NPR == SWV / 2 || gv < 2 * NPR)) {
       const int feat = (p.f + fw) * C::kFeat + featv;
-      const uint32_t vb = feat < dim ? vb_full : 0u;
+      // X rows are padded with zeros to whole slices (executors.stage_operand), so every lane of
+      // a slice inside the row copies 16 B: zero-fill lanes (src-size 0) mixed into a cp.async
+      // instruction cost more than the bytes they save (N = 24: 1.13 vs 0.79 ms at N = 32)
+      const uint32_t vb = feat < ldx ? vb_full : 0u;
       const char* src = xb + (int64_t)feat * 2;
       const uint32_t dst = stage0 + slot * kWarpStageBytes;
       if (p.j + 1 < p.nj) {  // full chunk: every slot holds a column
@@ -585,7 +596,7 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
   auto issue = [&](const ChunkPos& p, const int (&g)[NI], int slot) {
     if (p.fi < b) {
       const int feat = p.f * 32 + gv * 4;
-      const uint32_t vb = feat < dim ? 16u : 0u;
+      const uint32_t vb = feat < ldx ? 16u : 0u;  // zero padding read as data (see k_tile_warp)
       const char* src = xb + (int64_t)feat * 4;
       const uint32_t dst = stage0 + slot * kTfStage;
 #pragma unroll
@@ -788,6 +799,8 @@ static int g_warp_swv = 0;     // 0 auto, 4 or 8 (16-B vectors per row slice)
 // C2/N=128 DRAM reads 3.25 -> 1.16 GB per launch, L2 hit 82.7 -> 93.5 %, same time (2.46 ms);
 // C5 tile windows 29.9 -> 27.7 ms (tools/exp_pairing.py, exp_pair_ncu.py, exp_c5.py).
 static int g_warp_paired = 1;
+// 33..48-feature single slice: 1 = skip the empty 16-feature group at compile time (NPR = 3)
+static int g_warp_npr3 = 1;
 constexpr int64_t kPairMinXBytes = 96ll << 20;
 
 template <int SWV, bool FUSED = false>
@@ -807,9 +820,12 @@ static int launch_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* 
   const int smem = C::kSmem + (FUSED ? kFusedOutMax * kFusedLdw * 2 : 0);
   const bool want = g_warp_paired == 1 || (g_warp_paired == 2 && x_rows * ldx * 2 > kPairMinXBytes);
   const int paired = (!FUSED && FS > 1 && want && C::kWarps % FS == 0) ? 1 : 0;
-  // one slice of 33..48 features: the last 16-feature group is all zero
-  auto kern = (SWV == 8 && FS == 1 && dim <= 48 && dim > 32) ? k_tile_warp<SWV, FUSED, (SWV == 8 ? 3 : SWV / 2)>
-                                                            : k_tile_warp<SWV, FUSED>;
+  // one slice of 33..48 features: the fused (GCN) kernel skips the empty 16-feature group
+  // (C3 5.92 -> 5.71 ms); the plain SpMM is faster with the full unrolled schedule now that
+  // every lane copies whole padded rows (N = 40/41/48: 1.29 -> 1.21 ms; tools/exp_c3_npr3.sh)
+  auto kern = (FUSED && g_warp_npr3 && SWV == 8 && FS == 1 && dim <= 48 && dim > 32)
+                  ? k_tile_warp<SWV, FUSED, (SWV == 8 ? 3 : SWV / 2)>
+                  : k_tile_warp<SWV, FUSED>;
   HCS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   kern<<<grid, C::kWarps * 32, smem, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim,
                                             FS, z, ldz, scratch, mw, d_out, out, ldo, oscratch, paired);
@@ -862,6 +878,13 @@ int64_t tile_warp_scratch_floats() {
 }
 
 }  // namespace hcs
+
+// Experiment switch: the fused kernel's NPR = 3 variant for a single 33..48-feature slice (1, default) or the full one (0).
+extern "C" int hcs_set_tile_npr3(int on) {
+  HCS_REQUIRE(on == 0 || on == 1, HCS_EINVAL, "npr3 must be 0 or 1 (got %d)", on);
+  hcs::g_warp_npr3 = on;
+  return HCS_OK;
+}
 
 // Row-slice width of the warp-independent tile kernel: 0 auto, 4 (32 features) or 8 (64).
 extern "C" int hcs_set_tile_slice(int vectors) {

@@ -142,6 +142,13 @@ class DeviceOperand:
         return int(self.t.shape[0])
 
 
+# Pad X rows to whole gather slices (32 / 64 bf16 features, 32 fp32) whenever the feature width is
+# not a multiple of the slice, even when no padding would otherwise be needed: unpadded 48-B rows
+# (N = 24) straddle sectors and lines and took the tile kernel from 0.79 to 1.22 ms
+# (tools/exp_tile_dims.py).
+PAD_TO_SLICE = True
+
+
 def stage_operand(x, precision: str, device, tf32_round: bool = False) -> tuple[DeviceOperand, bool]:
     """Returns (operand, was_host).  Host numpy / DenseMatrix inputs are copied to HBM."""
     data = x.data if isinstance(x, DenseMatrix) else x
@@ -155,6 +162,9 @@ def stage_operand(x, precision: str, device, tf32_round: bool = False) -> tuple[
     else:
         want, elems, code = torch.float32, 4, _lib.DTYPE_F32
     ld = max(_round_up(dim, elems), elems)
+    slice_elems = (32 if dim <= 32 else 64) if want == torch.bfloat16 else 32
+    if PAD_TO_SLICE and dim % slice_elems:
+        ld = _round_up(dim, slice_elems)  # whole gather slices per row (see below)
     direct = (not was_host and t.device == device and t.dtype == want and t.is_contiguous() and ld == dim
               and t.data_ptr() % 16 == 0 and not tf32_round)
     if direct:
@@ -163,7 +173,6 @@ def stage_operand(x, precision: str, device, tf32_round: bool = False) -> tuple[
         # a padded copy is made anyway: pad rows to whole gather slices (64 or 128 B for bf16,
         # 128 B for fp32) so every gathered row slice starts on a cache-line boundary (C3's
         # 41-wide gradient: 96-B rows straddle lines; the fused backward took 1.52 ms)
-        slice_elems = (32 if dim <= 32 else 64) if want == torch.bfloat16 else 32
         ld = _round_up(dim, slice_elems)
     if was_host and t.dtype == want and ld == dim and t.is_contiguous() and not tf32_round:
         # host operand already in the compute dtype: one (async when pinned) H2D copy
