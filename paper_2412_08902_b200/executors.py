@@ -389,6 +389,9 @@ def spmm_hybrid(windows, assignment: Assignment, x, precision: str = "bf16", thr
 HOST_PIPELINE_MIN_WINDOWS = 4096
 HOST_PIPELINE_PARTS = 8  # measured on C2 (tools/exp_e2e_parts.py): 4 -> 4.36 ms, 8 -> 4.18, 16 -> 4.18, 32 -> 4.48
 _COPY_STREAMS: dict = {}
+# spmm_hybrid_async: requests overlap each other, so fewer, larger launches win (C2 N=128, two in
+# flight, tools/exp_e2e_async.py PARTS_SWEEP: 1 -> 3.11-3.20 ms, 2 -> 2.61, 4 -> 2.64, 8 -> 2.72)
+ASYNC_PIPELINE_PARTS = 2
 
 
 def _run_host_pipelined(plan, xop, z, ldz, host_kind, stats) -> SpmmResult:
@@ -441,7 +444,8 @@ def spmm_hybrid_async(windows, assignment: Assignment, x, precision: str = "bf16
     """spmm_hybrid for a HOST operand, returning before the product is done, so consecutive
     requests overlap: request i+1's X upload (H2D stream) runs under request i's kernels, and
     each request's Z rows stream back (copy stream) while its later row ranges compute.  The
-    kernels, the row ranges and therefore the results are those of spmm_hybrid.  Pinned host
+    kernels are those of spmm_hybrid; the product runs in ASYNC_PIPELINE_PARTS row ranges, so
+    results equal spmm_hybrid's to fp32 summation order (bit for bit when unsplit).  Pinned host
     memory makes the copies asynchronous; a request's X must not be modified before result().
     `out`: optional pinned fp32 host tensor of at least (rows, dim) for Z (a caller-owned ring of
     result buffers avoids a pinned allocation per request)."""
@@ -480,7 +484,7 @@ def spmm_hybrid_async(windows, assignment: Assignment, x, precision: str = "bf16
             raise ValueError(f"out must be a host float32 tensor of at least ({n}, {dim})")
         host = out[:n, :dim]
     W = len(ws)
-    parts = plan.parts(HOST_PIPELINE_PARTS) if W >= HOST_PIPELINE_MIN_WINDOWS else [None]
+    parts = plan.parts(ASYNC_PIPELINE_PARTS) if W >= HOST_PIPELINE_MIN_WINDOWS else [None]
     for part in parts:
         plan.run(xop, z, ldz, part=part)
         r0, r1 = (min(part[0] * wh, n), min(part[1] * wh, n)) if part is not None else (0, n)

@@ -262,7 +262,9 @@ def test_host_pipelined_path(cuda_ok):
 @pytest.mark.parametrize("big", [False, True])
 def test_async_requests_match_sync(cuda_ok, big):
     """spmm_hybrid_async with three requests in flight (different X each, pinned torch and
-    numpy inputs) returns exactly what spmm_hybrid returns for each of them."""
+    numpy inputs) returns what spmm_hybrid returns for each of them: bit for bit when the
+    product runs as one launch, to fp32 summation order when it runs in row ranges (the async
+    path uses fewer, larger ranges than the synchronous one, so warp-range cuts differ)."""
     import gen_graphs as gg
 
     n, rr, cc = gg.power_law(70000 if big else 3000, 24.0, seed=5)
@@ -275,12 +277,17 @@ def test_async_requests_match_sync(cuda_ok, big):
            torch.from_numpy(xs[2]).float()]
     reqs = [hc.spmm_hybrid_async(ws, asg, x) for x in ins]
     got = [r.result() for r in reqs]
+    def same(gz, wz):
+        if big:
+            return np.abs(gz - wz).max() <= 1e-5 * np.abs(wz).max()
+        return np.array_equal(gz, wz)
+
     for x, g in zip(ins, got):
         want = hc.spmm_hybrid(ws, asg, x)
         assert type(g.z.data) is type(want.z.data)
         gz = g.z.data if isinstance(g.z.data, np.ndarray) else g.z.data.numpy()
         wz = want.z.data if isinstance(want.z.data, np.ndarray) else want.z.data.numpy()
-        assert np.array_equal(gz, wz)
+        assert same(gz, wz)
         assert g.stats == want.stats
     assert orc.max_rel_err(got[0].z.data, orc.spmm_exact(a, xs[0])) <= BF16_TOL
     # caller-owned pinned result buffers (a ring of two, three requests)
@@ -291,7 +298,7 @@ def test_async_requests_match_sync(cuda_ok, big):
     z2, z0 = reqs[1].result().z.data, reqs[2].result().z.data
     as_np = lambda v: v if isinstance(v, np.ndarray) else v.numpy()  # noqa: E731
     for gz, x in ((z1, ins[1]), (z2, ins[2]), (z0, ins[0])):
-        assert np.array_equal(as_np(gz), as_np(hc.spmm_hybrid(ws, asg, x).z.data))
+        assert same(as_np(gz), as_np(hc.spmm_hybrid(ws, asg, x).z.data))
     with pytest.raises(ValueError, match="out must be"):
         hc.spmm_hybrid_async(ws, asg, ins[1], out=torch.empty(n, 8))
     with pytest.raises(ValueError, match="host operand"):

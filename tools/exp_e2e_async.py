@@ -46,7 +46,13 @@ for _ in range(k):
     del r
 torch.cuda.synchronize()
 res = {"sync_ms": round((time.perf_counter() - t) / k * 1e3, 3)}
-for depth in (1, 2, 3):
-    for use_ring in (False, True):
-        res[f"async_d{depth}_{'ring' if use_ring else 'alloc'}_ms"] = round(run(depth, use_ring), 3)
+if os.environ.get("PARTS_SWEEP"):
+    from paper_2412_08902_b200 import executors as ex
+    for parts in (1, 2, 4, 8, 1, 2, 4, 8):
+        ex.ASYNC_PIPELINE_PARTS = parts
+        res.setdefault(f"async_d2_ring_parts{parts}_ms", []).append(round(run(2, True), 3))
+else:
+    for depth in (1, 2, 3):
+        for use_ring in (False, True):
+            res[f"async_d{depth}_{'ring' if use_ring else 'alloc'}_ms"] = round(run(depth, use_ring), 3)
 print(json.dumps(res), flush=True)
