@@ -272,13 +272,12 @@ def run_ours(args):
         tev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
         graph = None
         if world == 1 and use_graph:  # one graph launch per step (SpmmGraph's capture of plan.run)
-            if plan.n_tile:
-                plan.scratch()
-            plan.run(xop, z, ldz)
+            scr = plan.new_scratch() if plan.n_tile else None  # the graph's own partial-sum buffer
+            plan.run(xop, z, ldz, scratch=scr)
             torch.cuda.synchronize()
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph):
-                plan.run(xop, z, ldz)
+                plan.run(xop, z, ldz, scratch=scr)
 
         def step(i=None):
             if world == 1:

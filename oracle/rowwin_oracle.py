@@ -523,6 +523,33 @@ def _loa_lib():
     return _LOA_LIB or None
 
 
+def spmm_exact_c(row_ptr, col_idx, values, x: np.ndarray, nthreads: int | None = None) -> np.ndarray:
+    """Exact float64 Z = A X through oracle/spmm_oracle.c (same math as spmm_exact: float64
+    products summed per row in CSR order), multi-threaded for BASELINE-size checks (C2: 115 M
+    entries x 128 features).  Raises if liboracle.so is not built."""
+    import ctypes
+
+    lib = _loa_lib()
+    if not lib:
+        raise RuntimeError("oracle/liboracle.so is not built (make -C oracle)")
+    if not hasattr(lib, "_spmm_typed"):
+        lib.oracle_spmm_f64.restype = ctypes.c_int
+        lib.oracle_spmm_f64.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
+                                        ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p,
+                                        ctypes.c_int64, ctypes.c_int32]
+        lib._spmm_typed = True
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+    ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+    va = np.ascontiguousarray(values, dtype=np.float64)
+    xd = np.ascontiguousarray(x, dtype=np.float64)
+    n = rp.size - 1
+    z = np.empty((n, xd.shape[1]), dtype=np.float64)
+    nt = nthreads or max(1, min(64, os.cpu_count() or 1))
+    lib.oracle_spmm_f64(rp.ctypes.data, ci.ctypes.data, va.ctypes.data, n, xd.ctypes.data, xd.shape[1],
+                        xd.shape[1], z.ctypes.data, z.shape[1], nt)
+    return z
+
+
 def _loa_c(lib, adj: Csr, vw: int, group_size: int) -> list[list[int]]:
     n = adj.num_rows
     rp = np.ascontiguousarray(adj.row_ptr, dtype=np.int64)

@@ -251,13 +251,23 @@ class HybridPlan:
             self._cache_d = {}
         return self._cache_d
 
-    def scratch(self) -> torch.Tensor:
-        """Partial-sum slots of the tile kernel (engine 2); one per plan, stream-ordered use."""
-        if getattr(self, "_scratch", None) is None:
-            n = _lib.ctypes.c_int64(0)
-            _lib.check(_lib.lib().hcs_tile_scratch_floats(_lib.ctypes.byref(n)))
-            self._scratch = torch.empty(max(int(n.value), 1), dtype=torch.float32, device=self.tile_list.device)
-        return self._scratch
+    def new_scratch(self) -> torch.Tensor:
+        """A fresh partial-sum buffer for the tile kernel's split windows (include/hcspmm.h: a
+        workspace must not be shared by launches that may run concurrently)."""
+        n = _lib.ctypes.c_int64(0)
+        _lib.check(_lib.lib().hcs_tile_scratch_floats(_lib.ctypes.byref(n)))
+        return torch.empty(max(int(n.value), 1), dtype=torch.float32, device=self.tile_list.device)
+
+    def scratch(self, stream: int | None = None) -> torch.Tensor:
+        """Partial-sum slots of the tile kernel, one buffer per CUDA stream: launches on one
+        stream are ordered, so they may share it; launches on different streams (side streams,
+        a replayed SpmmGraph -- which owns its own buffer -- next to eager calls) never do."""
+        key = _lib.stream() if stream is None else int(stream)
+        bufs = self.__dict__.setdefault("_scratch_by_stream", {})
+        buf = bufs.get(key)
+        if buf is None:
+            buf = bufs[key] = self.new_scratch()
+        return buf
 
     def launches_per_run(self, dim: int) -> int:
         """Kernels of one run(): engine 2 = tile kernel + fix-up, plus the scalar kernel."""
@@ -283,10 +293,12 @@ class HybridPlan:
             self._cache[key] = out
         return self._cache[key]
 
-    def run(self, xop: DeviceOperand, z: torch.Tensor, ldz: int, stream=None, tile_events=None, part=None) -> None:
+    def run(self, xop: DeviceOperand, z: torch.Tensor, ldz: int, stream=None, tile_events=None, part=None,
+            scratch: torch.Tensor | None = None) -> None:
         """Launch K4 (tile windows) then K3 (scalar + empty windows) on the current stream.
         tile_events: optional (start, end) torch.cuda.Event pair recorded around K4.
-        part: optional (w0, w1, t0, t1, s0, s1) from parts(): only windows [w0, w1)."""
+        part: optional (w0, w1, t0, t1, s0, s1) from parts(): only windows [w0, w1).
+        scratch: the tile kernel's partial-sum buffer (default: this stream's, see scratch())."""
         csr = self.windows.csr
         s = _lib.stream() if stream is None else stream
         t0, t1 = (0, self.n_tile) if part is None else part[2:4]
@@ -294,7 +306,8 @@ class HybridPlan:
         if tile_events is not None:
             tile_events[0].record()
         if t1 > t0:
-            scratch = self.scratch()
+            if scratch is None:
+                scratch = self.scratch(s)
             _lib.call("hcs_spmm_tile", self.tile_list.data_ptr() + 4 * t0, t1 - t0, self.chunk_ptr.data_ptr() + 8 * t0,
                       self.gidx.data_ptr(), self.ent_ptr.data_ptr(), self.ent.data_ptr(), self.ent_dtype,
                       csr.num_rows, self.windows.window_height, xop.t.data_ptr(), xop.dtype_code, xop.rows, xop.dim,
@@ -522,16 +535,17 @@ class SpmmGraph:
         self.xop, _ = stage_operand(x, precision, dev, tf32_round=(precision == "tf32" and self.plan.n_tile > 0))
         self.z, self.ldz = _alloc_z(ws.num_rows, self.xop.dim, dev)
         self.stats = ExecStats(**self.plan.stats.as_dict())
-        if self.plan.n_tile:
-            self.plan.scratch()  # allocated before capture
+        # the graph owns its partial-sum buffer (allocated before capture): a replay may run
+        # next to eager products of the same plan on other streams
+        self.scratch = self.plan.new_scratch() if self.plan.n_tile else None
         side = torch.cuda.Stream(device=dev)
         side.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(side):  # warm-up outside the capture (module loading, attributes)
-            self.plan.run(self.xop, self.z, self.ldz)
+            self.plan.run(self.xop, self.z, self.ldz, scratch=self.scratch)
         torch.cuda.current_stream(dev).wait_stream(side)
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
-            self.plan.run(self.xop, self.z, self.ldz)
+            self.plan.run(self.xop, self.z, self.ldz, scratch=self.scratch)
         self.launches = self.plan.launches_per_run(self.xop.dim)
 
     def replay(self) -> torch.Tensor:

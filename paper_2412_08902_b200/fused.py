@@ -77,7 +77,7 @@ def fused_aggregate_update(windows, assignment, x, m: torch.Tensor, precision: s
         _lib.call("hcs_gcn_tile", plan.tile_list.data_ptr(), plan.n_tile, plan.chunk_ptr.data_ptr(),
                   plan.gidx.data_ptr(), plan.ent_ptr.data_ptr(), plan.ent.data_ptr(), plan.ent_dtype, csr.num_rows,
                   ws.window_height, xop.t.data_ptr(), xop.dtype_code, xop.rows, dim, xop.ld, zp, ldz, m.data_ptr(),
-                  d_out, out.data_ptr(), d_out, plan.scratch().data_ptr(), plan.scratch().numel() * 4, s)
+                  d_out, out.data_ptr(), d_out, plan.scratch(s).data_ptr(), plan.scratch(s).numel() * 4, s)
     if plan.scalar_list.numel():
         _lib.call("hcs_gcn_scalar", csr.row_ptr.data_ptr(), csr.col_idx.data_ptr(), plan.scalar_vals.data_ptr(),
                   plan.scalar_vals_code, csr.num_rows, ws.window_height, plan.scalar_list.data_ptr(),

@@ -47,7 +47,8 @@ class GcnAggregateUpdate(torch.autograd.Function):
             shard.all_reduce(gw)  # grad_W = sum over ranks of z_r^T G_r
         gx = None
         if ctx.needs_input_grad[0]:
-            # (A^T G)[rows_r] = A_r G for the symmetric (gcn) operator: needs every rank's G rows
+            # grad_X = (A^T G) W^T over the backward windows (A^T's; the forward windows when A is
+            # symmetric); sharded: (A^T G)[rows_r] needs every rank's G rows
             g_full = g if shard is None else shard.all_gather_rows(g)
             gx, _ = fused_aggregate_update(ctx.windows_t, ctx.assignment, g_full, w.t(), ctx.precision,
                                            want_z=False)
@@ -56,11 +57,32 @@ class GcnAggregateUpdate(torch.autograd.Function):
         return gx, gw, None, None, None, None, None
 
 
+def backward_windows(windows: WindowSet, shard=None) -> WindowSet:
+    """Row windows of A^T for grad_X = A^T (G W^T) (gnn.py:181-183).  A symmetric operator (gcn /
+    gin / raw on an undirected graph) is its own transpose, so the forward windows are reused;
+    otherwise A^T is built and partitioned once and cached on the forward windows.  A sharded
+    rank holds only its rows of A, which do not determine its rows of A^T: pass windows_t."""
+    if getattr(windows.csr, "symmetric", False):
+        return windows
+    if shard is not None:
+        raise ValueError("a sharded layer over a non-symmetric operator needs windows_t (this rank's "
+                         "row windows of A^T)")
+    cached = getattr(windows, "_transpose_windows", None)
+    if cached is None:
+        from .gnn import transpose_csr
+        from .windows import partition
+
+        cached = partition(transpose_csr(windows.csr), windows.window_height)
+        windows._transpose_windows = cached
+    return cached
+
+
 def gcn_layer(x, w, windows, windows_t=None, assignment=None, precision="bf16", shard=None):
     if assignment is None:
         assignment = Assignment(windows.codes)
-    out = GcnAggregateUpdate.apply(x, w, windows, windows_t if windows_t is not None else windows, assignment,
-                                   precision, shard)
+    if windows_t is None:
+        windows_t = backward_windows(windows, shard)
+    out = GcnAggregateUpdate.apply(x, w, windows, windows_t, assignment, precision, shard)
     if shard is not None:
         out = shard.all_gather_rows_autograd(out)
     return out

@@ -42,6 +42,9 @@ def test_spmm_restatement_matches_reference(name):
     assert orc.max_rel_err(z32, g["z_f32"]) <= 1e-6
     exact = orc.spmm_exact(csr, x)
     assert orc.max_rel_err(exact, g["z_f64"]) <= 1e-12
+    # the multi-threaded C restatement used for the full-size (C2/C3) checks
+    exact_c = orc.spmm_exact_c(csr.row_ptr, csr.col_idx, csr.values, x, nthreads=3)
+    assert orc.max_rel_err(exact_c, g["z_f64"]) <= 1e-12
     assert orc.max_rel_err(orc.spmm_hybrid(w, g["codes"], x, "f64"), g["z_f64"]) <= 1e-13
 
 
