@@ -58,6 +58,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--sweep-dims", action="store_true", help="also report dims 32/64/128")
     p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--launch-check", action="store_true",
+                   help="test hook: start the ranks, rendezvous over gloo, print the world rank 0 saw, exit")
     return p.parse_args()
 
 
@@ -68,6 +70,12 @@ GATHER_PEAK_GBPS = 19470.0
 E2E_IN_FLIGHT = 2  # outstanding spmm_hybrid_async requests in the e2e measurement
 E2E_REPS = 3       # e2e value = median over this many timed runs of the request loop
 EXTRA: dict = {}  # multi-GPU timings added to the JSON line
+
+
+def exchange_parts() -> int:
+    """Row ranges per step in multi-GPU mode: the all-gather of range k overlaps the SpMM of
+    range k+1, so only the last range's exchange is exposed (1/parts of the volume)."""
+    return max(1, int(os.environ.get("HCS_EXCHANGE_PARTS", "8")))
 
 
 def peaks():
@@ -132,6 +140,43 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
                 "samples": len(sm)}
+
+
+def _free_port() -> int:
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def launch_ranks(args) -> int | None:
+    """`--gpus N` without a torchrun environment: start N ranks of this script (one process per
+    GPU) with torch.distributed.run on 127.0.0.1, the way the driver does, and return their exit
+    code.  Under torchrun (WORLD_SIZE set) the world size must equal --gpus; a mismatch fails
+    loudly instead of silently measuring fewer GPUs.  Returns None when this process is a rank."""
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is not None:
+        if int(world_env) != args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}: launch with "
+                             f"--nproc-per-node {args.gpus} or drop --gpus")
+        return None
+    if args.gpus <= 1:
+        return None
+    shared = os.environ.get("HCS_BENCH_SHARED_GPU") == "1"
+    if (args.impl != "reference" and not args.launch_check and not shared
+            and torch.cuda.device_count() < args.gpus):
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but only {torch.cuda.device_count()} CUDA device(s) are "
+                         f"visible (HCS_BENCH_SHARED_GPU=1 runs every rank on cuda:0 over gloo, for tests)")
+    env = dict(os.environ)
+    if not shared:  # print the NCCL communicator set-up (ranks, devices, transport) once per rank
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd, env=env).returncode
 
 
 def dist_setup(args):
@@ -258,7 +303,7 @@ def run_ours(args):
             # bf16.  The rank's windows run in `parts` nnz-balanced ranges; each range's rows are
             # all-gathered (padded to the largest rank's range) while the next range computes.
             gloo = dist.get_backend() != "nccl"
-            nparts = max(1, int(os.environ.get("HCS_EXCHANGE_PARTS", "2")))
+            nparts = exchange_parts()
             parts = plan.parts(nparts)
             nloc = local_a.num_rows
             spans = [(min(p_[0] * 16, nloc), min(p_[1] * 16, nloc)) for p_ in parts]
@@ -382,6 +427,19 @@ def run_ours(args):
                 torch.cuda.synchronize()
                 reps.append((time.perf_counter() - t1) / k)
             e2e_s = statistics.median(reps)
+            # the drop-in call: a rowwin caller passes a float64 DenseMatrix (pageable numpy) and
+            # gets numpy back; every byte of X crosses PCIe as float64 and is converted on the GPU
+            x64 = hc.DenseMatrix(x.double().cpu().numpy())
+            for _ in range(2):
+                hc.spmm_hybrid(ws, asg, x64, precision=args.precision)
+            kd = max(3, min(steps, 10))
+            t1 = time.perf_counter()
+            for _ in range(kd):
+                r = hc.spmm_hybrid(ws, asg, x64, precision=args.precision)
+                del r
+            torch.cuda.synchronize()
+            dropin_s = (time.perf_counter() - t1) / kd
+            del x64
             e2e = {"value": 2.0 * nnz * dim / e2e_s / 1e9, "unit": "GFLOP/s",
                    "h2d_bytes_per_step": int(xh.numel() * xh.element_size()),
                    "d2h_bytes_per_step": out_bytes,
@@ -392,7 +450,12 @@ def run_ours(args):
                    "in_flight": E2E_IN_FLIGHT,
                    "reps_ms": [round(v * 1e3, 4) for v in reps], "requests_per_rep": k,
                    "sync_ms_per_step": sync_s * 1e3,
-                   "sync_api": "paper_2412_08902_b200.spmm_hybrid(windows, assignment, pinned host bf16 X) -> host fp32 Z"}
+                   "sync_api": "paper_2412_08902_b200.spmm_hybrid(windows, assignment, pinned host bf16 X) -> host fp32 Z",
+                   "dropin": {"value": 2.0 * nnz * dim / dropin_s / 1e9, "unit": "GFLOP/s",
+                              "ms_per_step": dropin_s * 1e3,
+                              "h2d_bytes_per_step": int(n * dim * 8), "d2h_bytes_per_step": out_bytes,
+                              "api": ("paper_2412_08902_b200.spmm_hybrid(windows, assignment, DenseMatrix(float64 "
+                                      "numpy X, pageable)) -> numpy float32 Z: the rowwin caller's drop-in call")}}
         return ms, tile_ms, sampler.summary(), e2e
 
     dim = args.dim
@@ -448,6 +511,10 @@ def run_ours(args):
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "traffic_source": ("committed constant: dram__bytes_read.sum + dram__bytes_write.sum of one "
+                                        "k_tile_warp launch from an ncu --set full capture of this config "
+                                        "(profiles/ncu_traffic.json); DRAM counters cannot be read inside "
+                                        "an un-profiled run") if traffic is not None else None,
                      "kernel": ("whole step (CUDA graph: k_tile_warp + fix-up + K3)" if use_graph else
                                 "k_tile_warp (+ k_tile_warp_fixup)") if plan.n_tile else "k_spmm_scalar_w",
                      "kernel_ms": tile_ms, "algorithmic_bytes": tile_bytes,
@@ -464,7 +531,7 @@ def run_ours(args):
                                                                           * 1e6) * 1e3
                                 if gather_bytes else None}},
         "gpu_launches": plan.launches_per_run(dim) * args.steps * (
-            max(1, int(os.environ.get("HCS_EXCHANGE_PARTS", "2"))) if world > 1 else 1),
+            exchange_parts() if world > 1 else 1),
         "clocks": clocks,
     }
     if e2e is not None:
@@ -481,7 +548,7 @@ def run_ours(args):
                              "l2_gather_GBps": tile_ncols * d * s / (t2 * 1e-3) / 1e9 if t2 else None}
         out["dims"] = sweep
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(adj, dim, args.cpu_budget)
+        out["cpu_baseline"] = cpu_baseline(a, dim, args.cpu_budget)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -490,18 +557,46 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def cpu_baseline(adj, dim, budget):
-    from oracle.baseline import sampled_gflops
+def host_operator(config: str, seed: int, a=None):
+    """Host copies (row_ptr, col_idx, float64 values, n) of the benchmark's gcn operator: the
+    same seeded graph as the GPU arm, normalised by normalize_adj (bit-identical to the
+    reference's gnn.normalize_adj; tests/test_gpu_gnn.py) -- input preparation, not timed."""
+    if a is None:
+        _, a, _ = make_graph(config, seed)
+    vals = a.values_f64 if getattr(a, "values_f64", None) is not None else a.values.double()
+    return a.row_ptr.cpu().numpy(), a.col_idx.cpu().numpy(), vals.cpu().numpy(), a.num_rows
+
+
+def reference_cpu(rp, ci, vals, n, dim, steps, warmup) -> dict:
+    """The reference (baseline/_ref) on the host cores, or the oracle's numpy port if absent."""
+    from oracle import reference_arm
     from paper_2412_08902_b200 import graphgen
 
-    rp = adj.row_ptr.cpu().numpy()
-    ci = adj.col_idx.cpu().numpy()
-    x = graphgen.dense_features(adj.num_rows, dim, seed=1).float().cpu().numpy()
-    r = sampled_gflops(rp, ci, x, budget_s=budget)
+    x = graphgen.dense_features(n, dim, seed=1).float().cpu().numpy()  # the GPU arm's X, exactly
+    if reference_arm.load_reference() is not None:
+        r = reference_arm.timed_steps(rp, ci, vals, n, x, steps=steps, warmup=warmup)
+        sample = (f"stratified sample: every {r['stride']}th window ({r['windows_per_step']} windows, "
+                  f"{r['nnz_per_step']} nnz) per step, split over {r['processes']} forked processes each "
+                  f"calling the unmodified rowwin.executors.spmm_hybrid(windows, classify_windows(default_model(), "
+                  f"windows), X, precision='f32', threads=1) from baseline/_ref; {r['steps']} timed steps of "
+                  f"{r['ms_per_step']:.0f} ms; single-process rate {r['single_core_gflops']:.4f} GFLOP/s "
+                  f"(1 core used of {r['os_cpu_count']}); host {r['cpu_model']}, "
+                  f"OPENBLAS_NUM_THREADS={r['OPENBLAS_NUM_THREADS']}")
+        return {"value": r["gflops"], "unit": "GFLOP/s", "cores": r["processes"], "kind": "reference",
+                "sample": sample, "ms_per_step": r["ms_per_step"], "single_core_gflops": r["single_core_gflops"],
+                "host": {k: r[k] for k in ("cpu_model", "os_cpu_count", "OPENBLAS_NUM_THREADS", "numpy")}}
+    from oracle.baseline import sampled_gflops
+
+    r = sampled_gflops(rp, ci, x, budget_s=10.0)
     return {"value": r["gflops"], "unit": "GFLOP/s", "cores": r["cores"], "kind": "port",
-            "sample": (f"{r['windows']} windows (every 73rd first, then the rest) of the same gcn-normalised graph, "
-                       f"{r['nnz']} nnz, reference hybrid SpMM restated in numpy float32, {r['seconds']:.1f} s, "
-                       f"extrapolated by nnz")}
+            "sample": (f"baseline/_ref absent: oracle numpy restatement, {r['windows']} windows, {r['nnz']} nnz, "
+                       f"{r['seconds']:.1f} s"), "ms_per_step": r["seconds"] * 1e3}
+
+
+def cpu_baseline(a, dim, budget):
+    """The bench line's cpu_baseline: the reference arm's measurement, 2 timed steps."""
+    rp, ci, vals, n = host_operator("c2", 0, a)
+    return reference_cpu(rp, ci, vals, n, dim, steps=2, warmup=1)
 
 
 # ----------------------------------------------------------------------------- C3: 2-layer GCN epoch
@@ -627,51 +722,62 @@ def run_c4(args):
     print(json.dumps(out), flush=True)
 
 
+# ----------------------------------------------------------------------------- launcher test hook
+def run_launch_check(args):
+    """Every rank joins a gloo group and reports (rank, local rank, pid); rank 0 prints them."""
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    info = [rank, int(os.environ.get("LOCAL_RANK", "0")), os.getpid()]
+    seen = [info]
+    if world > 1:
+        dist.init_process_group("gloo")
+        seen = [None] * world
+        dist.all_gather_object(seen, info)
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"n_gpus": world, "gpus_arg": args.gpus, "ranks": seen}), flush=True)
+
+
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args):
+    """The reference arm: the unmodified reference (baseline/_ref) on the host cores, same graph,
+    X, metric and unit as our arm.  Under torchrun only rank 0 runs; the others exit 0."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
-    from oracle.baseline import sampled_gflops
-    from paper_2412_08902_b200 import graphgen
-
-    if args.config == "c2":
-        adj = graphgen.reddit_shaped(seed=args.seed)
-    elif args.config == "c1":
-        adj = graphgen.cora_shaped(seed=args.seed)
-    else:
-        adj = graphgen.rmat(24, 33, seed=args.seed)
-    rp = adj.row_ptr.cpu().numpy()
-    ci = adj.col_idx.cpu().numpy()
-    n = adj.num_rows
-    nnz = int(rp[-1]) + n  # + gcn self loops
-    x = graphgen.dense_features(n, args.dim, seed=1).float().cpu().numpy()
-    budget = max(1.0, min(10.0, 150.0 / max(1, args.steps + args.warmup)))
-    vals = []
-    for i in range(args.warmup + args.steps):
-        r = sampled_gflops(rp, ci, x, budget_s=budget)
-        if i >= args.warmup:
-            vals.append(r)
-    g = statistics.mean(v["gflops"] for v in vals)
-    ms = 2.0 * nnz * args.dim / (g * 1e9) * 1e3
-    out = {"metric": "SpMM GFLOP/s (2*nnz*N/t)", "value": g, "unit": "GFLOP/s", "impl": "reference",
-           "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+    cfg = args.config if args.config in ("c1", "c2", "c5") else "c2"
+    _, a, wl_name = make_graph(cfg, args.seed, args.graph)
+    rp, ci, vals, n = host_operator(cfg, args.seed, a)
+    nnz = int(rp[-1])
+    del a
+    torch.cuda.empty_cache()
+    r = reference_cpu(rp, ci, vals, n, args.dim, steps=args.steps, warmup=args.warmup)
+    out = {"metric": "SpMM GFLOP/s (2*nnz*N/t)", "value": r["value"], "unit": "GFLOP/s", "impl": "reference",
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-           "data": "synthetic (same seeded graph and X as the GPU arm)",
-           "config": {"workload": f"{args.config} reference hybrid SpMM (rowwin algorithm, numpy f32) dim {args.dim}",
+           "data": "synthetic (same seeded graph, operator and X as the GPU arm)",
+           "config": {"workload": wl_name + f", reference hybrid SpMM (rowwin, f32) on a window sample, dim {args.dim}",
                       "n": n, "nnz": nnz, "dim": args.dim},
-           "cpu_baseline": {"value": g, "unit": "GFLOP/s", "cores": vals[0]["cores"], "kind": "port",
-                            "sample": f"per step {vals[0]['windows']} windows / {vals[0]['nnz']} nnz in "
-                                      f"~{budget:.1f} s, extrapolated by nnz"},
-           "e2e": {"value": g, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+           "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+           "e2e": {"value": r["value"], "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if "host" in r:
+        out["cpu_baseline"]["host"] = r["host"]
+        out["cpu_baseline"]["single_core_gflops"] = r["single_core_gflops"]
     print(json.dumps(out), flush=True)
 
 
 if __name__ == "__main__":
     a = parse()
-    if a.impl == "reference":
+    rc = launch_ranks(a)
+    if rc is not None:
+        sys.exit(rc)
+    if a.launch_check:
+        run_launch_check(a)
+    elif a.impl == "reference":
         run_reference(a)
     elif a.config == "c3":
         run_c3(a)

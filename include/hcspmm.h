@@ -101,15 +101,14 @@ int hcs_spmm_scalar(const int64_t* row_ptr, const int32_t* col_idx, const void* 
 int hcs_set_scalar_variant(int variant);
 
 /* ---------------------------------------------------------------- K4
- * executors.py:111-141 tile_window for every window of a tile plan.  Engines
- * (hcs_set_tile_engine): 2 = default, warp-independent workers (each warp owns a
- * balanced range of (window, 32-feature slice, 64-column chunk) work with its own
- * cp.async ring and mma.sync m16n8k16, fp32 register accumulators; cut windows are
- * summed in warp order by a fix-up launch -> deterministic); 1 = warp-specialised
- * cp.async/TMA pipeline with mma.sync; 0 = the same pipeline with tcgen05.mma
- * (M = 128 features, N = 16 rows, TMEM accumulators).
- * workspace: >= hcs_tile_scratch_floats() floats (engine 2 partial sums; unused by 0/1);
- * one workspace must not be shared by launches that can run concurrently. */
+ * executors.py:111-141 tile_window for every window of a tile plan, on warp-independent
+ * workers: each warp owns a balanced range of (window, feature slice, 64-column chunk) work
+ * with its own cp.async ring and mma.sync (bf16 m16n8k16, or tf32 m16n8k8 for an fp32 plan),
+ * fp32 register accumulators; windows cut by a warp boundary are summed in warp order by a
+ * fix-up launch, so results are deterministic.  (Round 1's warp-specialised tcgen05 / mma.sync
+ * pipeline engines were removed in round 2: DESIGN.md section 4.)
+ * workspace: >= hcs_tile_scratch_floats() floats (split-window partial sums); one workspace
+ * must not be shared by launches that can run concurrently. */
 int hcs_tile_scratch_floats(int64_t* floats);
 /* engine 2 row-slice width in 16-B vectors: 0 auto (8 for dim > 32, else 4), 4 or 8 */
 int hcs_set_tile_slice(int vectors);
@@ -131,11 +130,12 @@ int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk
  * the SpMM of the listed windows with the feature GEMM fused into the window
  * epilogue:  out[rows] = (A_w X) M,  and z[rows] = A_w X when z != NULL
  * (forward z_cache).  M is an fp32 [dim x d_out] row-major device matrix: W for the
- * forward, W^T for the backward grad_X = (A^T G) W^T.  dim, d_out <= 128.
- * hcs_gcn_tile takes the tile plan of K2 (bf16) and the K4 workspace
- * (hcs_tile_scratch_floats); d_out <= 64 runs on the warp-independent kernel (window
- * partials cut by warp ranges are summed in warp order), larger d_out on the pipelined
- * kernel.  hcs_gcn_scalar takes a window list. */
+ * forward, W^T for the backward grad_X = (A^T G) W^T.
+ * hcs_gcn_tile takes the tile plan of K2 and the K4 workspace (hcs_tile_scratch_floats);
+ * d_out <= 64; bf16 plan: dim <= 128 (M^T staged in shared memory as bf16); fp32 plan (tf32):
+ * any dim, M RNA-rounded to tf32 by the caller.  Window partials cut by warp ranges are summed
+ * in warp order.  hcs_gcn_scalar takes a window list; dim, d_out <= 128.  Larger shapes run
+ * unfused: SpMM, then hcs_gemm. */
 int hcs_gcn_tile(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
                  const int64_t* ent_ptr, const void* ent, int ent_dtype, int64_t n_rows, int32_t wh, const void* x,
                  int x_dtype, int64_t x_rows, int32_t dim, int64_t ldx, float* z, int64_t ldz, const float* m,
@@ -144,6 +144,20 @@ int hcs_gcn_scalar(const int64_t* row_ptr, const int32_t* col_idx, const void* v
                    int64_t n_rows, int32_t wh, const int32_t* win_list, int64_t n_list, const void* x, int x_dtype,
                    int64_t x_rows, int32_t dim, int64_t ldx, float* z, int64_t ldz, const float* m, int32_t d_out,
                    float* out, int64_t ldo, void* stream);
+
+/* ---------------------------------------------------------------- K7 grad_W + dense update
+ * gnn.py:188 (unfused) / 195-199 (fused, ascending-window accumulation): grad_W = Z^T G.
+ * hcs_grad_w: C[M x N] = A^T B for A [K x M] (z_cache), B [K x N] (grad_out), fp32 row-major
+ * (lda, ldb multiples of 4, 16-byte aligned); deterministic split-K over K (fixed row slices,
+ * partials summed in slice order by a second launch), mma.sync tf32 (RNA) with fp32 accumulate.
+ * workspace: hcs_grad_w_workspace_bytes(K, M, N).
+ * hcs_gemm: C[K x N] = A[K x M] B[M x N] (gnn.py:142-143, 189, 202 -- the x_next = Z W and
+ * G W^T updates of the unfused mode and of shapes beyond the fused epilogues), same numerics. */
+int hcs_grad_w_workspace_bytes(int64_t K, int32_t M, int32_t N, size_t* bytes);
+int hcs_grad_w(const float* a, int64_t lda, const float* b, int64_t ldb, int64_t K, int32_t M, int32_t N, float* c,
+               int64_t ldc, void* workspace, size_t ws_bytes, void* stream);
+int hcs_gemm(const float* a, int64_t lda, const float* b, int64_t ldb, int64_t K, int32_t M, int32_t N, float* c,
+             int64_t ldc, void* stream);
 
 /* ---------------------------------------------------------------- K8 LOA
  * layout.py:186-263 build_windows_optimized (paper Alg. 6): greedy 16-vertex groups
@@ -164,21 +178,6 @@ int hcs_loa(const int64_t* row_ptr, const int32_t* col_idx, int64_t n, int32_t v
  * v_out32 (optional) receives the float32 copy used by the kernels. */
 int hcs_normalize_values(int kind, const int64_t* row_ptr, const int32_t* col, const double* v_in, int64_t n,
                          double* workspace_deg, double* v_out, float* v_out32, void* stream);
-
-/* tile-path engine: -1 auto (= 2), 0 tcgen05.mma pipeline, 1 mma.sync pipeline,
- * 2 warp-independent mma.sync workers (see K4) */
-int hcs_set_tile_engine(int engine);
-
-/* debug: tile-kernel experiment switches (bit0 skip MMA, bit1 skip slab build,
- * bit2 skip X gathers; results are wrong when set), 0 = normal */
-int hcs_debug_tile_switches(int bits);
-
-/* tile-path producer (X-row gather) warps per CTA: 4 (default), 8 or 16 */
-int hcs_set_tile_producers(int np);
-
-/* debug: per-CTA wait-time counters of the tile kernel (16 per CTA; enable=1 on,
- * 0 off; host_out != NULL copies the first n counters and clears them) */
-int hcs_debug_tile_profile(int enable, unsigned long long* host_out, int n);
 
 /* elementwise helpers used by the Python layer (fp32 -> bf16 RNE, fp32 -> tf32 RNA) */
 int hcs_convert(const float* src, void* dst, int64_t n, int dst_kind, void* stream);

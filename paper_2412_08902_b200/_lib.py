@@ -55,18 +55,17 @@ _SIGS = {
                                      I64, P, I32, P, I64, P, SZ, P]),
     "hcs_gcn_scalar": (ctypes.c_int, [P, P, P, ctypes.c_int, I64, I32, P, I64, P, ctypes.c_int, I64, I32, I64, P,
                                        I64, P, I32, P, I64, P]),
+    "hcs_grad_w_workspace_bytes": (ctypes.c_int, [I64, I32, I32, ctypes.POINTER(SZ)]),
+    "hcs_grad_w": (ctypes.c_int, [P, I64, P, I64, I64, I32, I32, P, I64, P, SZ, P]),
+    "hcs_gemm": (ctypes.c_int, [P, I64, P, I64, I64, I32, I32, P, I64, P]),
     "hcs_loa_workspace_bytes": (ctypes.c_int, [I64, ctypes.POINTER(SZ)]),
     "hcs_loa": (ctypes.c_int, [P, P, I64, I32, I32, P, P, P, P, P, SZ, P]),
     "hcs_convert": (ctypes.c_int, [P, P, I64, ctypes.c_int, P]),
     "hcs_normalize_values": (ctypes.c_int, [ctypes.c_int, P, P, P, I64, P, P, P, P]),
-    "hcs_debug_tile_profile": (ctypes.c_int, [ctypes.c_int, P, ctypes.c_int]),
-    "hcs_set_tile_engine": (ctypes.c_int, [ctypes.c_int]),
     "hcs_io_count": (ctypes.c_int, [ctypes.c_char_p, I64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(I64),
                                     ctypes.POINTER(ctypes.c_int)]),
     "hcs_io_parse": (ctypes.c_int, [ctypes.c_char_p, I64, ctypes.c_int, ctypes.c_int, I64, ctypes.c_int, P, P, P,
                                     ctypes.POINTER(ctypes.c_int)]),
-    "hcs_set_tile_producers": (ctypes.c_int, [ctypes.c_int]),
-    "hcs_debug_tile_switches": (ctypes.c_int, [ctypes.c_int]),
 }
 
 

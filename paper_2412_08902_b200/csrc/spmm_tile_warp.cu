@@ -2,8 +2,9 @@
 // tile_window) on sm_100a.
 //
 // Measured on B200 (profiles/r01_tile_switches_pipeline_engine_c2.txt): the warp-specialised
-// producer/builder/MMA pipeline of spmm_tile.cu spends ~3.8 ms of its 5.0 ms (C2, N = 128)
-// in per-chunk cross-warp hand-offs alone.  Here every warp is an independent worker with
+// producer/builder/MMA pipeline of round 1's first engine (cp.async/TMA producers, tcgen05.mma
+// or mma.sync consumer; removed in round 2, in git history as csrc/spmm_tile.cu) spent ~3.8 ms of
+// its 5.0 ms (C2, N = 128) in per-chunk cross-warp hand-offs alone.  Here every warp is an independent worker with
 // its own cp.async ring, so no barrier is shared between warps on the per-chunk path:
 //
 //   unit  = (TILE window t, feature slice f) with 32- or 64-feature slices (SWV = 4 / 8
@@ -539,11 +540,19 @@ constexpr int kTfSmem = kTfWarps * kTfPerWarp + 128;
 static_assert(kTfSmem <= 227 * 1024, "smem");
 __device__ __forceinline__ int swz_tf(int k, int v) { return v ^ ((2 * k) & 6); }
 
+// FUSED (K6/K7 in tf32): after each (window, 32-feature slice) unit the warp multiplies its 16 x 32
+// aggregated slice (tf32 A fragments taken from the accumulators, features permuted within each
+// 8-block so no shuffle is needed) by the slice's 32 x d_out block of M (tf32-rounded, read from
+// global / L1: the kernel's shared memory is full) into an out accumulator; window partials cut by
+// a warp boundary go to oscratch and are summed in warp order by k_tile_warp_fixup_out.
+template <bool FUSED>
 __global__ void __launch_bounds__(kTfWarps * 32, 1)
     k_tile_warp_tf32(const int32_t* __restrict__ tile_list, int64_t T, const int64_t* __restrict__ chunk_ptr,
                      const int32_t* __restrict__ gidx, const int64_t* __restrict__ ent_ptr,
                      const uint2* __restrict__ ent, int64_t n_rows, int wh, const float* __restrict__ x, int64_t ldx,
-                     int dim, int FS, float* __restrict__ z, int64_t ldz, float* __restrict__ scratch) {
+                     int dim, int FS, float* __restrict__ z, int64_t ldz, float* __restrict__ scratch,
+                     const float* __restrict__ mw, int d_out, float* __restrict__ out, int64_t ldo,
+                     float* __restrict__ oscratch) {
   constexpr int NI = 16;
   extern __shared__ uint8_t tsmem_raw[];
   uint8_t* tsmem = (uint8_t*)(((uintptr_t)tsmem_raw + 127) & ~(uintptr_t)127);
@@ -640,6 +649,10 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
   float acc[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+  constexpr int NO = FUSED ? kFusedOutMax / 8 : 1;
+  float oacc[NO][4];
+#pragma unroll
+  for (int i = 0; i < NO; ++i) oacc[i][0] = oacc[i][1] = oacc[i][2] = oacc[i][3] = 0.f;
   int s0 = 0;
   {  // the slab starts zeroed and is kept zero between chunks (entries are undone after use)
     const int4 zero4 = make_int4(0, 0, 0, 0);
@@ -698,16 +711,62 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
     if (unit_done || p0.fi + 1 == b) {
       const int64_t rs = (int64_t)__ldg(tile_list + p0.t) * wh;
       const int rows = (int)(n_rows - rs < wh ? n_rows - rs : wh);
-      if (!in_head && unit_done) {
-        store_slice<4>(z, ldz, rs, rows, dim, p0.f, acc, lane);
-      } else {
-        float* slot = scratch + (gw * 2 + (in_head ? 0 : 1)) * WarpCfg<4>::kSlot;
+      if (z != nullptr) {
+        if (!in_head && unit_done) {
+          store_slice<4>(z, ldz, rs, rows, dim, p0.f, acc, lane);
+        } else {
+          float* slot = scratch + (gw * 2 + (in_head ? 0 : 1)) * WarpCfg<4>::kSlot;
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
+          for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) slot[(nt * 4 + q) * 32 + lane] = acc[nt][q];
+            for (int q = 0; q < 4; ++q) slot[(nt * 4 + q) * 32 + lane] = acc[nt][q];
+        }
       }
       in_head = false;
+      if (FUSED) {
+        // oacc += Z_slice (16 x 32) . M[32 f .. 32 f + 31, :]; within each 8-feature block the MMA's
+        // k index t <-> feature 2t and t + 4 <-> 2t + 1 (the accumulator layout), on both operands
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          uint32_t af[4];
+          asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(af[0]) : "f"(acc[nt][0]));
+          asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(af[1]) : "f"(acc[nt][2]));
+          asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(af[2]) : "f"(acc[nt][1]));
+          asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(af[3]) : "f"(acc[nt][3]));
+          const int k0 = p0.f * 32 + nt * 8 + 2 * t4;
+#pragma unroll
+          for (int n8 = 0; n8 < NO; ++n8) {
+            if (n8 * 8 < d_out) {
+              const int col = n8 * 8 + g8;
+              const uint32_t b0 = (k0 < dim && col < d_out) ? __float_as_uint(__ldg(mw + (int64_t)k0 * d_out + col)) : 0u;
+              const uint32_t b1 =
+                  (k0 + 1 < dim && col < d_out) ? __float_as_uint(__ldg(mw + (int64_t)(k0 + 1) * d_out + col)) : 0u;
+              mma_tf32_1688(oacc[n8], af, b0, b1);
+            }
+          }
+        }
+        const bool win_head = (int64_t)FS * (p0.base - c0) < a;  // window began in an earlier warp's range
+        const bool win_done = unit_done && p0.f == FS - 1;
+        if (win_done || p0.fi + 1 == b) {
+          if (win_done && !win_head) {
+#pragma unroll
+            for (int n8 = 0; n8 < NO; ++n8)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const int r = g8 + 8 * (q >> 1), col = n8 * 8 + 2 * t4 + (q & 1);
+                if (r < rows && col < d_out) out[(rs + r) * ldo + col] = oacc[n8][q];
+              }
+          } else {
+            float* slot = oscratch + (gw * 2 + (win_head ? 0 : 1)) * kOutSlot;
+#pragma unroll
+            for (int n8 = 0; n8 < NO; ++n8)
+#pragma unroll
+              for (int q = 0; q < 4; ++q) slot[(n8 * 4 + q) * 32 + lane] = oacc[n8][q];
+          }
+#pragma unroll
+          for (int i = 0; i < NO; ++i) oacc[i][0] = oacc[i][1] = oacc[i][2] = oacc[i][3] = 0.f;
+        }
+      }
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
     }
@@ -726,23 +785,41 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
   cp_async_wait<0>();
 }
 
+__global__ void k_tile_warp_fixup_out(const int32_t* __restrict__ tile_list, int64_t T,
+                                      const int64_t* __restrict__ chunk_ptr, int64_t n_rows, int wh, int FS,
+                                      int d_out, float* __restrict__ out, int64_t ldo,
+                                      const float* __restrict__ oscratch, int64_t nwarps);
+
+// tf32 SpMM (m == nullptr) or fused GCN layer (m = tf32-rounded M [dim x d_out], d_out <= 64; z may
+// be nullptr when no z_cache is wanted).
 int spmm_tile_warp_tf32(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
                         const int64_t* ent_ptr, const uint2* ent, int64_t n_rows, int wh, const float* x, int64_t ldx,
-                        int dim, float* z, int64_t ldz, float* scratch, int64_t scratch_floats, cudaStream_t st) {
+                        int dim, float* z, int64_t ldz, float* scratch, int64_t scratch_floats, cudaStream_t st,
+                        const float* m = nullptr, int d_out = 0, float* out = nullptr, int64_t ldo = 0) {
   const int FS = (dim + 31) / 32;
   const int grid = num_sms();
   const int64_t nwarps = (int64_t)grid * kTfWarps;
-  HCS_REQUIRE(scratch != nullptr && scratch_floats >= nwarps * 2 * WarpCfg<4>::kSlot, HCS_EINVAL,
-              "tile scratch too small");
-  HCS_CUDA(cudaFuncSetAttribute(k_tile_warp_tf32, cudaFuncAttributeMaxDynamicSharedMemorySize, kTfSmem));
-  k_tile_warp_tf32<<<grid, kTfWarps * 32, kTfSmem, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh,
-                                                         x, ldx, dim, FS, z, ldz, scratch);
+  const bool fused = m != nullptr;
+  const int64_t need = nwarps * 2 * (WarpCfg<4>::kSlot + (fused ? kOutSlot : 0));
+  HCS_REQUIRE(scratch != nullptr && scratch_floats >= need, HCS_EINVAL, "tile scratch too small");
+  float* oscratch = scratch + nwarps * 2 * WarpCfg<4>::kSlot;
+  auto kern = fused ? k_tile_warp_tf32<true> : k_tile_warp_tf32<false>;
+  HCS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kTfSmem));
+  kern<<<grid, kTfWarps * 32, kTfSmem, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim,
+                                             FS, z, ldz, scratch, m, d_out, out, ldo, oscratch);
   HCS_LAUNCH_CHECK("k_tile_warp_tf32");
   const int fix_threads = 256;
   const int fix_blocks = (int)((nwarps * 32 + fix_threads - 1) / fix_threads);
-  k_tile_warp_fixup<4><<<fix_blocks, fix_threads, 0, st>>>(tile_list, n_tile, chunk_ptr, n_rows, wh, dim, FS, z, ldz,
-                                                            scratch, nwarps, 0);
-  HCS_LAUNCH_CHECK("k_tile_warp_fixup");
+  if (z != nullptr) {
+    k_tile_warp_fixup<4><<<fix_blocks, fix_threads, 0, st>>>(tile_list, n_tile, chunk_ptr, n_rows, wh, dim, FS, z,
+                                                              ldz, scratch, nwarps, 0);
+    HCS_LAUNCH_CHECK("k_tile_warp_fixup");
+  }
+  if (fused) {
+    k_tile_warp_fixup_out<<<fix_blocks, fix_threads, 0, st>>>(tile_list, n_tile, chunk_ptr, n_rows, wh, FS, d_out,
+                                                               out, ldo, oscratch, nwarps);
+    HCS_LAUNCH_CHECK("k_tile_warp_fixup_out");
+  }
   return HCS_OK;
 }
 
@@ -878,6 +955,70 @@ int64_t tile_warp_scratch_floats() {
 }
 
 }  // namespace hcs
+
+using namespace hcs;
+
+// K4: tile windows on the tensor cores (executors.py:111-141 tile_window for every window of
+// tile_list).  bf16 plan + bf16 X: k_tile_warp (mma.sync m16n8k16); fp32 plan + tf32-rounded fp32
+// X: k_tile_warp_tf32 (m16n8k8).  workspace: >= hcs_tile_scratch_floats() floats.
+extern "C" int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
+                             const int64_t* ent_ptr, const void* ent, int ent_dtype, int64_t n_rows, int32_t wh,
+                             const void* x, int x_dtype, int64_t x_rows, int32_t dim, int64_t ldx, float* z,
+                             int64_t ldz, void* workspace, size_t ws_bytes, void* stream) {
+  HCS_REQUIRE(wh > 0 && wh <= 16, HCS_EINVAL, "tile path supports window heights 1..16 (got %d)", wh);
+  HCS_REQUIRE(dim > 0, HCS_EINVAL, "dim must be positive");
+  HCS_REQUIRE(((uintptr_t)x & 15) == 0, HCS_EINVAL, "x must be 16-byte aligned");
+  HCS_REQUIRE(x_dtype == ent_dtype, HCS_EINVAL, "x and plan dtypes differ (%d vs %d)", x_dtype, ent_dtype);
+  HCS_REQUIRE(((uintptr_t)z & 7) == 0 && ldz % 2 == 0, HCS_EINVAL, "z must be 8-byte aligned with even ldz");
+  if (x_dtype == HCS_DTYPE_F32) {
+    HCS_REQUIRE(ldx % 4 == 0 && ldx >= ((dim + 3) / 4) * 4, HCS_EINVAL, "ldx must be a multiple of 4 covering dim");
+    if (n_tile == 0) return HCS_OK;
+    return spmm_tile_warp_tf32(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, (const uint2*)ent, n_rows, wh,
+                               (const float*)x, ldx, dim, z, ldz, (float*)workspace,
+                               (int64_t)(ws_bytes / sizeof(float)), as_stream(stream));
+  }
+  HCS_REQUIRE(x_dtype == HCS_DTYPE_BF16, HCS_EINVAL, "tile path: x dtype must be bf16 or f32 (tf32)");
+  HCS_REQUIRE(ldx % 8 == 0 && ldx >= ((dim + 7) / 8) * 8, HCS_EINVAL, "ldx must be a multiple of 8 covering dim");
+  if (n_tile == 0) return HCS_OK;
+  return spmm_tile_warp(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, (const uint32_t*)ent, n_rows, wh,
+                        (const __nv_bfloat16*)x, x_rows, ldx, dim, z, ldz, (float*)workspace,
+                        (int64_t)(ws_bytes / sizeof(float)), as_stream(stream));
+}
+
+// K6/K7: tile windows with the fused GCN epilogue: out = (A_w X) M per TILE window, plus
+// z = A_w X when z != NULL (the forward z_cache).  M: fp32 [dim x d_out] row-major device matrix
+// (W forward, W^T backward).  bf16: dim <= 128, d_out <= 64; tf32 (fp32 plan + X, M already
+// RNA-rounded to tf32 by the caller): any dim, d_out <= 64.
+extern "C" int hcs_gcn_tile(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
+                            const int64_t* ent_ptr, const void* ent, int ent_dtype, int64_t n_rows, int32_t wh,
+                            const void* x, int x_dtype, int64_t x_rows, int32_t dim, int64_t ldx, float* z,
+                            int64_t ldz, const float* m, int32_t d_out, float* out, int64_t ldo, void* workspace,
+                            size_t ws_bytes, void* stream) {
+  HCS_REQUIRE(wh > 0 && wh <= 16, HCS_EINVAL, "tile path supports window heights 1..16 (got %d)", wh);
+  HCS_REQUIRE(d_out > 0 && d_out <= kFusedOutMax, HCS_EINVAL, "fused GCN tile path needs 1 <= d_out <= %d (got %d)",
+              kFusedOutMax, d_out);
+  HCS_REQUIRE(x_dtype == ent_dtype, HCS_EINVAL, "x and plan dtypes differ (%d vs %d)", x_dtype, ent_dtype);
+  HCS_REQUIRE(((uintptr_t)x & 15) == 0, HCS_EINVAL, "x must be 16-byte aligned");
+  HCS_REQUIRE(m != nullptr && out != nullptr && ldo >= d_out, HCS_EINVAL, "fused GCN: bad M / out arguments");
+  HCS_REQUIRE(z == nullptr || (((uintptr_t)z & 7) == 0 && ldz % 2 == 0), HCS_EINVAL,
+              "z must be 8-byte aligned with even ldz");
+  cudaStream_t st = as_stream(stream);
+  if (x_dtype == HCS_DTYPE_F32) {
+    HCS_REQUIRE(dim > 0 && ldx % 4 == 0 && ldx >= ((dim + 3) / 4) * 4, HCS_EINVAL,
+                "ldx must be a multiple of 4 covering dim");
+    if (n_tile == 0) return HCS_OK;
+    return spmm_tile_warp_tf32(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, (const uint2*)ent, n_rows, wh,
+                               (const float*)x, ldx, dim, z, ldz, (float*)workspace,
+                               (int64_t)(ws_bytes / sizeof(float)), st, m, d_out, out, ldo);
+  }
+  HCS_REQUIRE(x_dtype == HCS_DTYPE_BF16, HCS_EINVAL, "tile path: x dtype must be bf16 or f32 (tf32)");
+  HCS_REQUIRE(dim > 0 && dim <= 128, HCS_EINVAL, "fused bf16 GCN tile path needs 1 <= d_in <= 128 (got %d)", dim);
+  HCS_REQUIRE(ldx % 8 == 0 && ldx >= ((dim + 7) / 8) * 8, HCS_EINVAL, "ldx must be a multiple of 8 covering dim");
+  if (n_tile == 0) return HCS_OK;
+  return gcn_tile_warp(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, (const uint32_t*)ent, n_rows, wh,
+                       (const __nv_bfloat16*)x, ldx, dim, z, ldz, m, d_out, out, ldo, (float*)workspace,
+                       (int64_t)(ws_bytes / sizeof(float)), st);
+}
 
 // Experiment switch: the fused kernel's NPR = 3 variant for a single 33..48-feature slice (1, default) or the full one (0).
 extern "C" int hcs_set_tile_npr3(int on) {

@@ -596,18 +596,6 @@ def spmm_auto(csr, x, assignment_for, precision: str = "bf16", threads: int = 1)
     return spmm_hybrid(windows, assignment_for(windows), x, precision=precision, threads=threads)
 
 
-_ENGINES = {"auto": -1, "tcgen05": 0, "mma_sync": 1, "warp": 2}
-
-
-def set_tile_engine(engine: str = "auto") -> None:
-    """Select the tile-path kernel: "warp" (warp-independent mma.sync workers; the
-    default, "auto"), "mma_sync" / "tcgen05" (the warp-specialised cp.async pipeline
-    with mma.sync m16n8k16 or tcgen05.mma + TMEM accumulators)."""
-    if engine not in _ENGINES:
-        raise ValueError(f"engine must be one of {sorted(_ENGINES)}, got {engine!r}")
-    _lib.call("hcs_set_tile_engine", _ENGINES[engine])
-
-
 _SCALAR_VARIANTS = {"auto": 0, "block": 1, "warp16": 2}
 
 

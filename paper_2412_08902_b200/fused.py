@@ -1,4 +1,4 @@
-"""Fused GCN aggregation + update (K6 forward, K7 backward) and grad_W.
+"""Fused GCN aggregation + update (K6 forward, K7 backward), grad_W and the dense update.
 
 Reference: gnn.py:147-159 (fused forward: per window z_w = A_w X, out[rows] = z_w W,
 z_cache[rows] = z_w) and gnn.py:195-205 (fused backward).  Here one launch per path
@@ -6,12 +6,11 @@ z_cache[rows] = z_w) and gnn.py:195-205 (fused backward).  Here one launch per p
 window and multiplies the on-chip 16 x d_in tile by M before writing the output rows:
     forward   out = (A X) W,      z = A X   (z_cache, needed for grad_W)
     backward  grad_X = (A^T G) W^T          (the reference's A^T (G W^T))
-grad_W = Z^T G is a plain dense GEMM (d_in x n times n x d_out, K = n) and is left to
-cuBLAS via torch.matmul on TF32 tensor cores (fp32 accumulate; deterministic for a fixed
-shape).  Measured at C3 (n = 232,965): the fp32 SIMT GEMM took 303-330 us per call.
-
-Sizes outside the fused kernels' on-chip budget (d_in or d_out > 128) run the same
-math as two GPU passes (SpMM kernel, then a cuBLAS GEMM).
+Fused shapes: d_out <= 64; bf16 d_in <= 128; tf32 any d_in on tile windows (M rounded to tf32),
+d_in <= 128 on scalar windows.  Other shapes run the same math unfused: the SpMM kernels, then
+the hand-written tall-skinny GEMM (csrc/dense.cu hcs_gemm).
+grad_W = Z^T G (gnn.py:188, 195-199) is csrc/dense.cu hcs_grad_w: a deterministic split-K
+tf32 tensor-core GEMM (fixed row slices summed in slice order).  No GCN pass calls cuBLAS.
 """
 
 from __future__ import annotations
@@ -21,33 +20,51 @@ import torch
 from . import _lib
 from .executors import _alloc_z, get_plan, stage_operand
 
-FUSED_MAX_DIM = 128
+FUSED_MAX_DIM = 128      # scalar-window fused epilogue (d_in and d_out), bf16 tile epilogue (d_in)
+FUSED_TILE_MAX_OUT = 64  # tile-window fused epilogues (out accumulators in registers)
 
 
-GRAD_W_SPLIT = 2048  # rows per K-slice of the split-K grad_W GEMM
+def _f32_2d(t: torch.Tensor, dev) -> torch.Tensor:
+    t = t.to(device=dev, dtype=torch.float32)
+    if t.dim() != 2:
+        raise ValueError("dense operands must be 2-dimensional")
+    if t.stride(1) != 1 or t.stride(0) < t.shape[1]:
+        t = t.contiguous()
+    return t
 
 
 def grad_weight(z: torch.Tensor, g: torch.Tensor) -> torch.Tensor:
-    """Z^T G as a deterministic split-K GEMM: K = n rows in slices of GRAD_W_SPLIT, one batched
-    TF32 tensor-core GEMM over the slices (a CTA per slice instead of one per 64 x 64 output
-    tile: the plain GEMM took 125 us at C3), then the slice partials summed in slice order."""
-    z, g = z.float(), g.float()
-    n = int(z.shape[0])
-    s = n // GRAD_W_SPLIT
-    prev = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = True
-    try:
-        if s < 2:
-            return z.t() @ g
-        head = s * GRAD_W_SPLIT
-        zb = z[:head].reshape(s, GRAD_W_SPLIT, z.shape[1])
-        gb = g[:head].reshape(s, GRAD_W_SPLIT, g.shape[1])
-        out = torch.bmm(zb.transpose(1, 2), gb).sum(0)
-        if head < n:
-            out = out + z[head:].t() @ g[head:]
+    """Z^T G (grad_W, gnn.py:188) on the hand-written deterministic split-K kernel."""
+    dev = z.device
+    z, g = _f32_2d(z, dev), _f32_2d(g, dev)
+    K, M, N = int(z.shape[0]), int(z.shape[1]), int(g.shape[1])
+    if int(g.shape[0]) != K:
+        raise ValueError(f"z has {K} rows, grad has {int(g.shape[0])}")
+    out = torch.empty((M, N), dtype=torch.float32, device=dev)
+    if M == 0 or N == 0:
         return out
-    finally:
-        torch.backends.cuda.matmul.allow_tf32 = prev
+    wsb = _lib.ctypes.c_size_t(0)
+    _lib.check(_lib.lib().hcs_grad_w_workspace_bytes(K, M, N, _lib.ctypes.byref(wsb)))
+    ws = torch.empty(max(int(wsb.value) // 4, 1), dtype=torch.float32, device=dev)
+    _lib.call("hcs_grad_w", z.data_ptr(), z.stride(0), g.data_ptr(), g.stride(0), K, M, N, out.data_ptr(), N,
+              ws.data_ptr(), ws.numel() * 4, _lib.stream())
+    return out
+
+
+def dense_matmul(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """a [K x M] @ b [M x N] on the hand-written tall-skinny tf32 GEMM (csrc/dense.cu)."""
+    dev = a.device
+    a, b = _f32_2d(a, dev), _f32_2d(b, dev)
+    K, M, N = int(a.shape[0]), int(a.shape[1]), int(b.shape[1])
+    if int(b.shape[0]) != M:
+        raise ValueError(f"inner dimensions differ: {M} vs {int(b.shape[0])}")
+    out = torch.empty((K, N), dtype=torch.float32, device=dev)
+    if K and N and M:
+        _lib.call("hcs_gemm", a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), K, M, N, out.data_ptr(), N,
+                  _lib.stream())
+    elif K and N:
+        out.zero_()
+    return out
 
 
 def fused_aggregate_update(windows, assignment, x, m: torch.Tensor, precision: str, want_z: bool):
@@ -61,23 +78,30 @@ def fused_aggregate_update(windows, assignment, x, m: torch.Tensor, precision: s
     if int(m.shape[0]) != dim:
         raise ValueError(f"X has {dim} features, weight expects {int(m.shape[0])}")
     n = ws.num_rows
-    if dim > FUSED_MAX_DIM or d_out > FUSED_MAX_DIM or (plan.n_tile and precision != "bf16"):
-        # outside the fused kernels' on-chip budget, or tf32 tile windows (the fused tile
-        # epilogue is bf16-only): SpMM kernels, then a cuBLAS GEMM on the device
+    has_scalar = plan.scalar_list.numel() > 0
+    fused = ((not plan.n_tile or (d_out <= FUSED_TILE_MAX_OUT and (precision == "tf32" or dim <= FUSED_MAX_DIM)))
+             and (not has_scalar or (dim <= FUSED_MAX_DIM and d_out <= FUSED_MAX_DIM)))
+    if not fused:
+        # outside the fused kernels' on-chip budget: SpMM kernels, then the dense update kernel
         z, ldz = _alloc_z(n, dim, dev)
         plan.run(xop, z, ldz)
         zz = z[:, :dim]
-        return zz @ m, (zz if want_z else None)
+        return dense_matmul(zz, m), (zz if want_z else None)
     z, ldz = _alloc_z(n, dim, dev) if want_z else (None, 0)
     out = torch.empty((n, d_out), dtype=torch.float32, device=dev)
     csr = ws.csr
     s = _lib.stream()
     zp = z.data_ptr() if z is not None else None
     if plan.n_tile:
+        mt = m
+        if precision == "tf32":  # the tile epilogue's B operand: M rounded to tf32 (RNA)
+            mt = torch.empty_like(m)
+            _lib.call("hcs_convert", m.data_ptr(), mt.data_ptr(), m.numel(), _lib.DTYPE_F32, s)
+        scr = plan.scratch(s)
         _lib.call("hcs_gcn_tile", plan.tile_list.data_ptr(), plan.n_tile, plan.chunk_ptr.data_ptr(),
                   plan.gidx.data_ptr(), plan.ent_ptr.data_ptr(), plan.ent.data_ptr(), plan.ent_dtype, csr.num_rows,
-                  ws.window_height, xop.t.data_ptr(), xop.dtype_code, xop.rows, dim, xop.ld, zp, ldz, m.data_ptr(),
-                  d_out, out.data_ptr(), d_out, plan.scratch(s).data_ptr(), plan.scratch(s).numel() * 4, s)
+                  ws.window_height, xop.t.data_ptr(), xop.dtype_code, xop.rows, dim, xop.ld, zp, ldz, mt.data_ptr(),
+                  d_out, out.data_ptr(), d_out, scr.data_ptr(), scr.numel() * 4, s)
     if plan.scalar_list.numel():
         _lib.call("hcs_gcn_scalar", csr.row_ptr.data_ptr(), csr.col_idx.data_ptr(), plan.scalar_vals.data_ptr(),
                   plan.scalar_vals_code, csr.num_rows, ws.window_height, plan.scalar_list.data_ptr(),

@@ -191,9 +191,11 @@ def forward(layer: GnnLayer, a_norm, x, mode: str = "unfused", assignment: Assig
     host = not isinstance(x.data if isinstance(x, DenseMatrix) else x, torch.Tensor)
     traffic = TrafficReport()
     if mode == "unfused":
+        from .fused import dense_matmul
+
         z = spmm_hybrid(windows, assignment, x, precision=precision).z.data
         z = torch.as_tensor(z, device=dev)
-        x_next = z @ w
+        x_next = dense_matmul(z, w)
         traffic.intermediate_writes = n * layer.d_in
         traffic.intermediate_reads = n * layer.d_in
         traffic.pass_launches = 2
@@ -231,7 +233,9 @@ def backward(layer: GnnLayer, a_norm, z_cache, grad_out, mode: str = "unfused",
 
     grad_w = grad_weight(z, g)
     if mode == "unfused":
-        grad_z = g @ w.t()
+        from .fused import dense_matmul
+
+        grad_z = dense_matmul(g, w.t())
         traffic.intermediate_writes = a.num_rows * layer.d_in
         traffic.intermediate_reads = a.num_rows * layer.d_in
         traffic.pass_launches = 2

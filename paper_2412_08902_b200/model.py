@@ -62,7 +62,7 @@ def backward_windows(windows: WindowSet, shard=None) -> WindowSet:
     gin / raw on an undirected graph) is its own transpose, so the forward windows are reused;
     otherwise A^T is built and partitioned once and cached on the forward windows.  A sharded
     rank holds only its rows of A, which do not determine its rows of A^T: pass windows_t."""
-    if getattr(windows.csr, "symmetric", False):
+    if getattr(windows.csr, "symmetric", False) or getattr(windows.csr, "global_symmetric", False):
         return windows
     if shard is not None:
         raise ValueError("a sharded layer over a non-symmetric operator needs windows_t (this rank's "

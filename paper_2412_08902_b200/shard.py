@@ -98,7 +98,11 @@ class Shard:
         return cls(shard_window_ranges(a.row_ptr, a.num_rows, world, wh), rank, a.num_rows, wh, group)
 
     def local_operator(self, a: DeviceCsr) -> DeviceCsr:
-        return row_slice(a, self.row0, self.row1)
+        """This rank's rows of A.  A row slice is not symmetric itself; `global_symmetric` records
+        that the full operator is, so the backward can reuse the forward windows (A^T = A)."""
+        loc = row_slice(a, self.row0, self.row1)
+        loc.global_symmetric = bool(getattr(a, "symmetric", False) or getattr(a, "global_symmetric", False))
+        return loc
 
     def all_gather_rows(self, local: torch.Tensor) -> torch.Tensor:
         return allgather_rows(local.contiguous(), self.ranges, self.n_rows, self.wh, self.group)

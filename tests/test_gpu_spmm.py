@@ -169,21 +169,15 @@ def test_large_powerlaw_tile_path_checksum(cuda_ok):
         assert float((res.z.data[r].double() - exact).abs().max()) / scale <= BF16_TOL
 
 
-@pytest.mark.parametrize("engine", ["tcgen05", "mma_sync", "warp"])
+@pytest.mark.parametrize("precision", ["bf16", "tf32"])
 @pytest.mark.parametrize("dim", [8, 32, 40, 64, 128, 200])
-def test_tile_engines_agree(cuda_ok, engine, dim):
-    """Both tensor-core engines of the tile path against the exact product."""
-    from paper_2412_08902_b200.executors import set_tile_engine
-
+def test_tile_path_dims(cuda_ok, precision, dim):
+    """The tile path (every window on the tensor cores) against the exact product."""
     a = plaw8k_csr()
     x = orc.random_dense(a.num_cols, dim, seed=dim)
     ws = hc.partition(to_hc(a))
-    try:
-        set_tile_engine(engine)
-        res = hc.spmm_tile(ws, hc.DenseMatrix(x))
-    finally:
-        set_tile_engine("auto")
-    assert orc.max_rel_err(res.z.data, orc.spmm_exact(a, x)) <= BF16_TOL
+    res = hc.spmm_tile(ws, hc.DenseMatrix(x), precision=precision)
+    assert orc.max_rel_err(res.z.data, orc.spmm_exact(a, x)) <= (BF16_TOL if precision == "bf16" else 1e-3)
 
 
 @pytest.mark.parametrize("vectors", [4, 8])
