@@ -184,15 +184,15 @@ def dist_setup(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
-        import torch.distributed as dist
+        from paper_2412_08902_b200.shard import init_process_group
 
         if os.environ.get("HCS_BENCH_SHARED_GPU") == "1":
             # test mode for a 1-GPU box: every rank on cuda:0, gloo collectives
             torch.cuda.set_device(0)
-            dist.init_process_group("gloo")
+            init_process_group("gloo")
         else:
             torch.cuda.set_device(local)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            init_process_group("nccl", device=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     return world, rank, local

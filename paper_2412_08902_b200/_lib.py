@@ -121,6 +121,33 @@ def stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
+_NVTX = None
+
+
+def nvtx(name: str):
+    """Decorator: an NVTX range around each call (visible in nsys / ncu --nvtx timelines; a
+    no-op cost of a few hundred ns without a profiler attached)."""
+    import functools
+
+    def deco(fn):
+        @functools.wraps(fn)
+        def wrapper(*args, **kwargs):
+            global _NVTX
+            if _NVTX is None:
+                _NVTX = torch.cuda.is_available()
+            if not _NVTX:
+                return fn(*args, **kwargs)
+            torch.cuda.nvtx.range_push(name)
+            try:
+                return fn(*args, **kwargs)
+            finally:
+                torch.cuda.nvtx.range_pop()
+
+        return wrapper
+
+    return deco
+
+
 def ptr(t: torch.Tensor | None) -> int | None:
     if t is None:
         return None

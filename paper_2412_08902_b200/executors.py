@@ -201,6 +201,7 @@ class HybridPlan:
     """K2 execution plan for (windows, assignment, precision): TILE window list with
     packed 64-column chunks, SCALAR/empty window list, and the ExecStats."""
 
+    @_lib.nvtx("hcs.tile_plan")
     def __init__(self, windows, codes: torch.Tensor, precision: str):
         dev = windows.csr.device
         self.windows = windows
@@ -283,16 +284,22 @@ class HybridPlan:
             starts = rp[torch.clamp(torch.arange(W + 1, device=rp.device) * wh, max=n)].cpu().numpy()
             targets = (np.arange(1, k) * int(starts[-1])) // k
             bounds = [0] + [int(v) for v in np.searchsorted(starts, targets, side="left")] + [W]
-            tl = self.tile_list.cpu().numpy()
-            sl = self.scalar_list.cpu().numpy()
-            out = []
-            for i in range(k):
-                w0, w1 = bounds[i], max(bounds[i], bounds[i + 1])
-                out.append((w0, w1, int(np.searchsorted(tl, w0)), int(np.searchsorted(tl, w1)),
-                            int(np.searchsorted(sl, w0)), int(np.searchsorted(sl, w1))))
-            self._cache[key] = out
+            self._cache[key] = self.parts_from_bounds(bounds)
         return self._cache[key]
 
+    def parts_from_bounds(self, bounds) -> list[tuple[int, int, int, int, int, int]]:
+        """Window bounds b_0 <= ... <= b_k -> parts (w0, w1, t0, t1, s0, s1) for run(part=...)."""
+        if "lists_host" not in self._cache:
+            self._cache["lists_host"] = (self.tile_list.cpu().numpy(), self.scalar_list.cpu().numpy())
+        tl, sl = self._cache["lists_host"]
+        out = []
+        for i in range(len(bounds) - 1):
+            w0, w1 = int(bounds[i]), max(int(bounds[i]), int(bounds[i + 1]))
+            out.append((w0, w1, int(np.searchsorted(tl, w0)), int(np.searchsorted(tl, w1)),
+                        int(np.searchsorted(sl, w0)), int(np.searchsorted(sl, w1))))
+        return out
+
+    @_lib.nvtx("hcs.spmm")
     def run(self, xop: DeviceOperand, z: torch.Tensor, ldz: int, stream=None, tile_events=None, part=None,
             scratch: torch.Tensor | None = None) -> None:
         """Launch K4 (tile windows) then K3 (scalar + empty windows) on the current stream.
@@ -378,6 +385,7 @@ def _wrap_result(z: torch.Tensor, dim: int, was_host, stats: ExecStats) -> SpmmR
     return SpmmResult(DenseMatrix(out if out.is_contiguous() else out.contiguous()), stats)
 
 
+@_lib.nvtx("hcs.spmm_hybrid")
 def spmm_hybrid(windows, assignment: Assignment, x, precision: str = "bf16", threads: int = 1,
                 tile_cols: int = 8, dim_tile: int = 16) -> SpmmResult:
     """executors.py:234-251: TILE windows on tensor cores, SCALAR windows on CUDA cores."""
@@ -564,6 +572,7 @@ def spmm_tile(windows, x, precision: str = "bf16", tile_cols: int = 8, dim_tile:
     return spmm_hybrid(ws, asg, x, precision=precision, threads=threads)
 
 
+@_lib.nvtx("hcs.spmm_scalar")
 def spmm_scalar(csr, x, precision: str = "bf16", window_height: int = 16) -> SpmmResult:
     """executors.py:191-213: every row on the CUDA-core path (no partition needed)."""
     xrows = x.rows if isinstance(x, DenseMatrix) else int(x.shape[0])

@@ -33,6 +33,7 @@ def _f32_2d(t: torch.Tensor, dev) -> torch.Tensor:
     return t
 
 
+@_lib.nvtx("hcs.grad_w")
 def grad_weight(z: torch.Tensor, g: torch.Tensor) -> torch.Tensor:
     """Z^T G (grad_W, gnn.py:188) on the hand-written deterministic split-K kernel."""
     dev = z.device
@@ -51,63 +52,98 @@ def grad_weight(z: torch.Tensor, g: torch.Tensor) -> torch.Tensor:
     return out
 
 
-def dense_matmul(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
-    """a [K x M] @ b [M x N] on the hand-written tall-skinny tf32 GEMM (csrc/dense.cu)."""
+@_lib.nvtx("hcs.gemm")
+def dense_matmul(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """a [K x M] @ b [M x N] on the hand-written tall-skinny tf32 GEMM (csrc/dense.cu).
+    `out`: optional fp32 [K x N] destination with unit column stride (e.g. a row slice)."""
     dev = a.device
     a, b = _f32_2d(a, dev), _f32_2d(b, dev)
     K, M, N = int(a.shape[0]), int(a.shape[1]), int(b.shape[1])
     if int(b.shape[0]) != M:
         raise ValueError(f"inner dimensions differ: {M} vs {int(b.shape[0])}")
-    out = torch.empty((K, N), dtype=torch.float32, device=dev)
+    if out is None:
+        out = torch.empty((K, N), dtype=torch.float32, device=dev)
+    elif out.dtype != torch.float32 or tuple(out.shape) != (K, N) or out.stride(1) != 1:
+        raise ValueError(f"out must be float32 ({K}, {N}) with unit column stride")
     if K and N and M:
-        _lib.call("hcs_gemm", a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), K, M, N, out.data_ptr(), N,
-                  _lib.stream())
+        _lib.call("hcs_gemm", a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), K, M, N, out.data_ptr(),
+                  out.stride(0), _lib.stream())
     elif K and N:
         out.zero_()
     return out
 
 
+class FusedLayer:
+    """One GCN aggregation + update over a WindowSet: out = (A X) M (and z = A X), staged once and
+    launched for all windows or for row-window parts (plan.parts / window bounds), so a sharded
+    layer can start exchanging part k's rows while part k+1 computes (model.ShardedGcnLayer)."""
+
+    def __init__(self, windows, assignment, x, m: torch.Tensor, precision: str, want_z: bool):
+        ws = windows
+        dev = ws.csr.device
+        self.ws, self.precision = ws, precision
+        self.plan = plan = get_plan(ws, assignment, precision)
+        self.xop, _ = stage_operand(x, precision, dev, tf32_round=(precision == "tf32" and plan.n_tile > 0))
+        self.m = m = m.to(device=dev, dtype=torch.float32).contiguous()
+        self.dim, self.d_out = dim, d_out = self.xop.dim, int(m.shape[1])
+        if int(m.shape[0]) != dim:
+            raise ValueError(f"X has {dim} features, weight expects {int(m.shape[0])}")
+        n = ws.num_rows
+        has_scalar = plan.scalar_list.numel() > 0
+        self.fused = ((not plan.n_tile or (d_out <= FUSED_TILE_MAX_OUT and (precision == "tf32" or dim <= FUSED_MAX_DIM)))
+                      and (not has_scalar or (dim <= FUSED_MAX_DIM and d_out <= FUSED_MAX_DIM)))
+        # outside the fused kernels' on-chip budget: SpMM kernels, then the dense update kernel
+        self.want_z = want_z
+        self.z, self.ldz = _alloc_z(n, dim, dev) if (want_z or not self.fused) else (None, 0)
+        self.out = torch.empty((n, d_out), dtype=torch.float32, device=dev)
+        self.mt = m
+        if self.fused and plan.n_tile and precision == "tf32":  # tile epilogue B operand: M rounded to tf32
+            self.mt = torch.empty_like(m)
+            _lib.call("hcs_convert", m.data_ptr(), self.mt.data_ptr(), m.numel(), _lib.DTYPE_F32, _lib.stream())
+
+    def parts(self, bounds) -> list:
+        """Window bounds (local window ids) -> parts for run()."""
+        return self.plan.parts_from_bounds(bounds)
+
+    def run(self, part=None) -> None:
+        """Launch the kernels of windows part = (w0, w1, t0, t1, s0, s1) (all windows if None)."""
+        plan, ws, xop = self.plan, self.ws, self.xop
+        dim, d_out = self.dim, self.d_out
+        n = ws.num_rows
+        if not self.fused:
+            plan.run(xop, self.z, self.ldz, part=part)
+            r0, r1 = (0, n) if part is None else (min(part[0] * ws.window_height, n), min(part[1] * ws.window_height, n))
+            if r1 > r0:
+                dense_matmul(self.z[r0:r1, :dim], self.m, out=self.out[r0:r1])
+            return
+        t0, t1 = (0, plan.n_tile) if part is None else part[2:4]
+        s0, s1 = (0, int(plan.scalar_list.numel())) if part is None else part[4:6]
+        csr = ws.csr
+        s = _lib.stream()
+        zp = self.z.data_ptr() if self.z is not None else None
+        if t1 > t0:
+            scr = plan.scratch(s)
+            _lib.call("hcs_gcn_tile", plan.tile_list.data_ptr() + 4 * t0, t1 - t0, plan.chunk_ptr.data_ptr() + 8 * t0,
+                      plan.gidx.data_ptr(), plan.ent_ptr.data_ptr(), plan.ent.data_ptr(), plan.ent_dtype,
+                      csr.num_rows, ws.window_height, xop.t.data_ptr(), xop.dtype_code, xop.rows, dim, xop.ld, zp,
+                      self.ldz, self.mt.data_ptr(), d_out, self.out.data_ptr(), d_out, scr.data_ptr(),
+                      scr.numel() * 4, s)
+        if s1 > s0:
+            _lib.call("hcs_gcn_scalar", csr.row_ptr.data_ptr(), csr.col_idx.data_ptr(), plan.scalar_vals.data_ptr(),
+                      plan.scalar_vals_code, csr.num_rows, ws.window_height, plan.scalar_list.data_ptr() + 4 * s0,
+                      s1 - s0, xop.t.data_ptr(), xop.dtype_code, xop.rows, dim, xop.ld, zp, self.ldz,
+                      self.m.data_ptr(), d_out, self.out.data_ptr(), d_out, s)
+
+    def result(self):
+        return self.out, (self.z[:, :self.dim] if (self.z is not None and self.want_z) else None)
+
+
+@_lib.nvtx("hcs.gcn_fused")
 def fused_aggregate_update(windows, assignment, x, m: torch.Tensor, precision: str, want_z: bool):
     """Returns (out [n, d_out] fp32, z [n, dim] fp32 or None) on the device."""
-    ws = windows
-    dev = ws.csr.device
-    plan = get_plan(ws, assignment, precision)
-    xop, _ = stage_operand(x, precision, dev, tf32_round=(precision == "tf32" and plan.n_tile > 0))
-    m = m.to(device=dev, dtype=torch.float32).contiguous()
-    dim, d_out = xop.dim, int(m.shape[1])
-    if int(m.shape[0]) != dim:
-        raise ValueError(f"X has {dim} features, weight expects {int(m.shape[0])}")
-    n = ws.num_rows
-    has_scalar = plan.scalar_list.numel() > 0
-    fused = ((not plan.n_tile or (d_out <= FUSED_TILE_MAX_OUT and (precision == "tf32" or dim <= FUSED_MAX_DIM)))
-             and (not has_scalar or (dim <= FUSED_MAX_DIM and d_out <= FUSED_MAX_DIM)))
-    if not fused:
-        # outside the fused kernels' on-chip budget: SpMM kernels, then the dense update kernel
-        z, ldz = _alloc_z(n, dim, dev)
-        plan.run(xop, z, ldz)
-        zz = z[:, :dim]
-        return dense_matmul(zz, m), (zz if want_z else None)
-    z, ldz = _alloc_z(n, dim, dev) if want_z else (None, 0)
-    out = torch.empty((n, d_out), dtype=torch.float32, device=dev)
-    csr = ws.csr
-    s = _lib.stream()
-    zp = z.data_ptr() if z is not None else None
-    if plan.n_tile:
-        mt = m
-        if precision == "tf32":  # the tile epilogue's B operand: M rounded to tf32 (RNA)
-            mt = torch.empty_like(m)
-            _lib.call("hcs_convert", m.data_ptr(), mt.data_ptr(), m.numel(), _lib.DTYPE_F32, s)
-        scr = plan.scratch(s)
-        _lib.call("hcs_gcn_tile", plan.tile_list.data_ptr(), plan.n_tile, plan.chunk_ptr.data_ptr(),
-                  plan.gidx.data_ptr(), plan.ent_ptr.data_ptr(), plan.ent.data_ptr(), plan.ent_dtype, csr.num_rows,
-                  ws.window_height, xop.t.data_ptr(), xop.dtype_code, xop.rows, dim, xop.ld, zp, ldz, mt.data_ptr(),
-                  d_out, out.data_ptr(), d_out, scr.data_ptr(), scr.numel() * 4, s)
-    if plan.scalar_list.numel():
-        _lib.call("hcs_gcn_scalar", csr.row_ptr.data_ptr(), csr.col_idx.data_ptr(), plan.scalar_vals.data_ptr(),
-                  plan.scalar_vals_code, csr.num_rows, ws.window_height, plan.scalar_list.data_ptr(),
-                  plan.scalar_list.numel(), xop.t.data_ptr(), xop.dtype_code, xop.rows, dim, xop.ld, zp, ldz,
-                  m.data_ptr(), d_out, out.data_ptr(), d_out, s)
-    return out, (z[:, :dim] if z is not None else None)
+    layer = FusedLayer(windows, assignment, x, m, precision, want_z)
+    layer.run()
+    return layer.result()
 
 
 def gcn_forward_fused(windows, assignment, x, w, precision):

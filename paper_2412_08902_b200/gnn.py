@@ -71,6 +71,7 @@ def _adjacency(g):
     return g.adjacency if isinstance(g, Graph) else g
 
 
+@_lib.nvtx("hcs.normalize_adj")
 def normalize_adj(g, kind: str = "gcn") -> DeviceCsr:
     """gnn.py:68-95 on the device.  Structure: A (+ I merged by a sorted key union);
     values: float64 kernels with the reference's operation order (csrc/normalize.cu),

@@ -103,6 +103,7 @@ def sort_by_min_neighbor(g) -> np.ndarray:
     return sort_by_min_neighbor_device(_adj(g)).cpu().numpy()
 
 
+@_lib.nvtx("hcs.loa")
 def build_windows_optimized(g, vw: int = 128, group_size: int = WINDOW_HEIGHT, check_counters: bool = False,
                             audit=None) -> WindowGrouping:
     """layout.py:186-263 on the GPU (K8).  Byte-identical grouping to the reference."""

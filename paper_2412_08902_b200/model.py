@@ -6,14 +6,15 @@ The reference has a single GCN layer with no activation, loss or optimizer
     ReLU
     fwd L2 (fused: out2 = (A H) W2, z2 = A H)      K6
     softmax cross-entropy on seeded random labels
-    bwd L2: grad_W2 = z2^T G2 (cuBLAS); grad_H = (A^T G2) W2^T (fused K7)
+    bwd L2: grad_W2 = z2^T G2 (K7 split-K kernel); grad_H = (A^T G2) W2^T (fused K7)
     ReLU backward
     bwd L1: grad_W1 = z1^T G1 (no grad_X for the input features)
     SGD update
 The layer is a torch.autograd.Function whose forward/backward call the fused
-kernels, so the loop body is plain PyTorch.  Multi-GPU (row-window shards):
-each rank computes its rows; the layer output rows are all-gathered between
-layers and grad_W is all-reduced.
+kernels, so the loop body is plain PyTorch.  Multi-GPU (row-window shards,
+ShardedGcnLayer): each rank computes its rows in parts whose all-gathers overlap
+the next part's kernels, and grad_W is all-reduced under the grad_X aggregation
+(SURVEY §5, §8e).
 """
 
 from __future__ import annotations
@@ -22,38 +23,30 @@ import numpy as np
 import torch
 
 from .executors import Assignment
-from .fused import fused_aggregate_update, grad_weight
+from .fused import FusedLayer, fused_aggregate_update, grad_weight
 from .windows import WindowSet
 
 
 class GcnAggregateUpdate(torch.autograd.Function):
-    """y = (A x) W with A given by row windows; saves z = A x for grad_W."""
+    """y = (A x) W with A given by row windows (one GPU); saves z = A x for grad_W."""
 
     @staticmethod
     def forward(ctx, x, w, windows, windows_t, assignment, precision, shard):
         out, z = fused_aggregate_update(windows, assignment, x.detach(), w.detach(), precision, want_z=True)
         ctx.save_for_backward(z, w)
-        ctx.windows_t, ctx.assignment, ctx.precision, ctx.shard = windows_t, assignment, precision, shard
+        ctx.windows_t, ctx.assignment, ctx.precision = windows_t, assignment, precision
         return out
 
     @staticmethod
     def backward(ctx, g):
-        # g: gradient of this rank's output rows (all rows on one GPU)
         z, w = ctx.saved_tensors
         g = g.contiguous()
-        shard = ctx.shard
         gw = grad_weight(z, g)
-        if shard is not None:
-            shard.all_reduce(gw)  # grad_W = sum over ranks of z_r^T G_r
         gx = None
         if ctx.needs_input_grad[0]:
             # grad_X = (A^T G) W^T over the backward windows (A^T's; the forward windows when A is
-            # symmetric); sharded: (A^T G)[rows_r] needs every rank's G rows
-            g_full = g if shard is None else shard.all_gather_rows(g)
-            gx, _ = fused_aggregate_update(ctx.windows_t, ctx.assignment, g_full, w.t(), ctx.precision,
-                                           want_z=False)
-            if shard is not None:
-                gx = shard.embed_rows(gx)  # the input was all-gathered: only our rows flow back
+            # symmetric)
+            gx, _ = fused_aggregate_update(ctx.windows_t, ctx.assignment, g, w.t(), ctx.precision, want_z=False)
         return gx, gw, None, None, None, None, None
 
 
@@ -82,10 +75,78 @@ def gcn_layer(x, w, windows, windows_t=None, assignment=None, precision="bf16", 
         assignment = Assignment(windows.codes)
     if windows_t is None:
         windows_t = backward_windows(windows, shard)
-    out = GcnAggregateUpdate.apply(x, w, windows, windows_t, assignment, precision, shard)
     if shard is not None:
-        out = shard.all_gather_rows_autograd(out)
-    return out
+        return ShardedGcnLayer.apply(x, w, windows, windows_t, assignment, precision, shard, EXCHANGE_PARTS)
+    return GcnAggregateUpdate.apply(x, w, windows, windows_t, assignment, precision, None)
+
+
+class ShardedGcnLayer(torch.autograd.Function):
+    """One row-window-sharded GCN layer: y_full = all_gather_r((A_r x) W).
+
+    Forward: the rank's windows run in EXCHANGE_PARTS nnz-balanced parts; right after part k's
+    kernels its output rows start an async all-gather (NCCL runs it on its own stream), so the
+    exchange of part k overlaps the aggregation of part k+1 and only the last part's transfer is
+    exposed.  Backward: the all-gather of G's rows (needed because A^T G reads every column) is
+    issued first and grad_W = z_r^T G_r is computed while it flies; grad_W's all-reduce then
+    overlaps the grad_X aggregation."""
+
+    @staticmethod
+    def forward(ctx, x, w, windows, windows_t, assignment, precision, shard, parts):
+        layer = FusedLayer(windows, assignment, x.detach(), w.detach(), precision, want_z=True)
+        spans = shard.part_spans(parts)
+        mine = layer.parts([lo for lo, _ in spans[shard.rank]] + [spans[shard.rank][-1][1]])
+        n_loc = shard.row1 - shard.row0
+        wh = shard.wh
+
+        def rows_of(r, k):
+            r0, r1 = shard.rank_rows(r)
+            lo, hi = spans[r][k]
+            return min(lo * wh, r1 - r0), min(hi * wh, r1 - r0)
+
+        pending = []
+        for k, part in enumerate(mine):
+            layer.run(part)
+            a, b = rows_of(shard.rank, k)
+            counts = [rows_of(r, k)[1] - rows_of(r, k)[0] for r in range(shard.world)]
+            pending.append((k, counts) + shard.start_gather(layer.out[a:b], counts))
+        full = torch.empty((shard.n_rows, layer.d_out), dtype=layer.out.dtype, device=layer.out.device)
+        for k, counts, work, recv, maxr in pending:
+            work.wait()
+            for r in range(shard.world):
+                a, b = rows_of(r, k)
+                if b > a:
+                    g0 = shard.rank_rows(r)[0]
+                    full[g0 + a:g0 + b] = recv[r * maxr: r * maxr + (b - a)]
+        out, z = layer.result()
+        assert out.shape[0] == n_loc
+        ctx.save_for_backward(z, w)
+        ctx.windows_t, ctx.assignment, ctx.precision, ctx.shard = windows_t, assignment, precision, shard
+        return full
+
+    @staticmethod
+    def backward(ctx, g_full):
+        import torch.distributed as dist
+
+        z, w = ctx.saved_tensors
+        shard = ctx.shard
+        g_loc = g_full[shard.row0:shard.row1].contiguous()
+        counts = [shard.rank_rows(r)[1] - shard.rank_rows(r)[0] for r in range(shard.world)]
+        gather = shard.start_gather(g_loc, counts) if ctx.needs_input_grad[0] else None
+        gw = grad_weight(z, g_loc)  # overlaps the all-gather of G
+        red = dist.all_reduce(gw, op=dist.ReduceOp.SUM, group=shard.group, async_op=True)
+        gx = None
+        if gather is not None:
+            work, recv, maxr = gather
+            work.wait()
+            g_all = torch.cat([recv[r * maxr: r * maxr + counts[r]] for r in range(shard.world)], 0)
+            gx_loc, _ = fused_aggregate_update(ctx.windows_t, ctx.assignment, g_all, w.t(), ctx.precision,
+                                               want_z=False)  # overlaps grad_W's all-reduce
+            gx = shard.embed_rows(gx_loc)  # the input was replicated / gathered: our rows flow back
+        red.wait()
+        return gx, gw, None, None, None, None, None, None
+
+
+EXCHANGE_PARTS = 4  # row-window parts per sharded layer (exchange of part k under compute of k+1)
 
 
 class Gcn2:

@@ -12,10 +12,30 @@ The collective is torch.distributed (NCCL on GPUs, gloo in CPU tests).
 
 from __future__ import annotations
 
+import os
+from datetime import timedelta
+
 import numpy as np
 import torch
 
 from .matrices import DeviceCsr
+
+NCCL_TIMEOUT_S = float(os.environ.get("HCS_NCCL_TIMEOUT_S", "600"))
+
+
+def init_process_group(backend: str = "nccl", device: torch.device | None = None, timeout_s: float | None = None):
+    """Join the job's process group (one process per GPU; RANK/WORLD_SIZE/MASTER_* from the
+    launcher).  NCCL failure handling: TORCH_NCCL_ASYNC_ERROR_HANDLING=1 makes a failed or timed
+    out collective abort the communicator and raise in every rank (instead of a silent hang),
+    and every collective gets a deadline of HCS_NCCL_TIMEOUT_S seconds (default 600)."""
+    import torch.distributed as dist
+
+    if backend == "nccl":
+        os.environ.setdefault("TORCH_NCCL_ASYNC_ERROR_HANDLING", "1")
+    kw = {"timeout": timedelta(seconds=timeout_s or NCCL_TIMEOUT_S)}
+    if backend == "nccl" and device is not None:
+        kw["device_id"] = device
+    dist.init_process_group(backend, **kw)
 
 
 def shard_window_ranges(row_ptr, n_rows: int, world: int, wh: int = 16) -> list[tuple[int, int]]:
@@ -83,7 +103,7 @@ class Shard:
     the collectives the sharded GCN needs: all-gather of output rows between
     layers (ragged, padded to the largest shard) and all-reduce(sum) of grad_W."""
 
-    def __init__(self, ranges, rank: int, n_rows: int, wh: int = 16, group=None):
+    def __init__(self, ranges, rank: int, n_rows: int, wh: int = 16, group=None, window_starts=None):
         self.ranges = ranges
         self.rank = rank
         self.world = len(ranges)
@@ -92,10 +112,54 @@ class Shard:
         self.group = group
         self.row0 = min(ranges[rank][0] * wh, n_rows)
         self.row1 = min(ranges[rank][1] * wh, n_rows)
+        # entry offset at every global window start (nnz-balanced exchange parts); None -> by count
+        self.window_starts = None if window_starts is None else np.asarray(window_starts, dtype=np.int64)
+        self._spans: dict = {}
 
     @classmethod
     def from_operator(cls, a: DeviceCsr, world: int, rank: int, wh: int = 16, group=None) -> "Shard":
-        return cls(shard_window_ranges(a.row_ptr, a.num_rows, world, wh), rank, a.num_rows, wh, group)
+        rp = a.row_ptr.cpu().numpy() if isinstance(a.row_ptr, torch.Tensor) else np.asarray(a.row_ptr)
+        W = -(-a.num_rows // wh)
+        starts = rp[np.minimum(np.arange(W + 1) * wh, a.num_rows)]
+        return cls(shard_window_ranges(rp, a.num_rows, world, wh), rank, a.num_rows, wh, group, starts)
+
+    def part_spans(self, parts: int) -> list[list[tuple[int, int]]]:
+        """Every rank's `parts` exchange parts as LOCAL window bounds [(lw0, lw1)] (contiguous,
+        ~equal nnz when the window starts are known); identical on every rank, so each rank knows
+        where every peer's part lands without a count exchange."""
+        if parts not in self._spans:
+            out = []
+            for a, b in self.ranges:
+                if self.window_starts is not None and b > a:
+                    st = self.window_starts[a:b + 1]
+                    tg = st[0] + (np.arange(1, parts) * (st[-1] - st[0])) // parts
+                    cuts = [0] + [int(v) for v in np.searchsorted(st, tg, side="left")] + [b - a]
+                else:
+                    cuts = [((b - a) * k) // parts for k in range(parts + 1)]
+                cuts = np.maximum.accumulate(np.minimum(cuts, b - a))
+                out.append([(int(cuts[k]), int(cuts[k + 1])) for k in range(parts)])
+            self._spans[parts] = out
+        return self._spans[parts]
+
+    def rank_rows(self, r: int) -> tuple[int, int]:
+        a, b = self.ranges[r]
+        return min(a * self.wh, self.n_rows), min(b * self.wh, self.n_rows)
+
+    def start_gather(self, local_rows: torch.Tensor, counts: list[int]):
+        """Async all-gather of this rank's `local_rows` (counts[r] rows on rank r, padded to the
+        largest); returns (work, recv, maxr) for finish_gather."""
+        import torch.distributed as dist
+
+        maxr = max(max(counts), 1)
+        d = local_rows.shape[1]
+        send = torch.zeros((maxr, d), dtype=local_rows.dtype, device=local_rows.device)
+        send[: local_rows.shape[0]] = local_rows
+        recv = torch.empty((self.world * maxr, d), dtype=local_rows.dtype, device=local_rows.device)
+        if dist.get_backend(self.group) == "nccl":
+            work = dist.all_gather_into_tensor(recv, send, group=self.group, async_op=True)
+        else:
+            work = dist.all_gather(list(recv.chunk(self.world)), send, group=self.group, async_op=True)
+        return work, recv, maxr
 
     def local_operator(self, a: DeviceCsr) -> DeviceCsr:
         """This rank's rows of A.  A row slice is not symmetric itself; `global_symmetric` records

@@ -187,6 +187,7 @@ def _selector_doubles(model) -> tuple:
             float(model.feature_scales[0]), float(model.feature_scales[1]))
 
 
+@_lib.nvtx("hcs.partition")
 def partition(csr, window_height: int = WINDOW_HEIGHT, model=None) -> WindowSet:
     """GPU K1: windows.py:81-106 partition (+ features + selector decisions).
 

@@ -74,12 +74,34 @@ def _dense_fused(windows, assignment, x, m, precision, want_z):
     return z @ m.to(torch.float64), (z if want_z else None)
 
 
+class _DenseLayer:
+    """Stand-in for fused.FusedLayer (same part interface) over a _DenseWindows."""
+
+    def __init__(self, windows, assignment, x, m, precision, want_z):
+        self.a, self.x, self.m = windows.a, x.to(torch.float64), m.to(torch.float64)
+        self.d_out = int(m.shape[1])
+        self.out = torch.full((self.a.shape[0], self.d_out), float("nan"), dtype=torch.float64)
+        self.z = torch.full((self.a.shape[0], self.x.shape[1]), float("nan"), dtype=torch.float64)
+
+    def parts(self, bounds):
+        return [(bounds[i], bounds[i + 1]) for i in range(len(bounds) - 1)]
+
+    def run(self, part):
+        r0, r1 = min(16 * part[0], self.a.shape[0]), min(16 * part[1], self.a.shape[0])
+        self.z[r0:r1] = self.a[r0:r1] @ self.x
+        self.out[r0:r1] = self.z[r0:r1] @ self.m
+
+    def result(self):
+        return self.out, self.z
+
+
 def _worker(rank, world, port, a_np, x_np, labels_np, w1_np, w2_np, out_q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         gcn_model.fused_aggregate_update = _dense_fused
+        gcn_model.FusedLayer = _DenseLayer
         gcn_model.grad_weight = lambda z, g: z.t() @ g.to(z.dtype)  # dense stand-in for the K7 kernel
         a = torch.from_numpy(a_np)
         n = a.shape[0]
