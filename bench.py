@@ -515,8 +515,8 @@ def run_ours(args):
                                         "k_tile_warp launch from an ncu --set full capture of this config "
                                         "(profiles/ncu_traffic.json); DRAM counters cannot be read inside "
                                         "an un-profiled run") if traffic is not None else None,
-                     "kernel": ("whole step (CUDA graph: k_tile_warp + fix-up + K3)" if use_graph else
-                                "k_tile_warp (+ k_tile_warp_fixup)") if plan.n_tile else "k_spmm_scalar_w",
+                     "kernel": ("whole step (CUDA graph: k_tile_warp + K3)" if use_graph else
+                                "k_tile_warp") if plan.n_tile else "k_spmm_scalar_w",
                      "kernel_ms": tile_ms, "algorithmic_bytes": tile_bytes,
                      "l2_gather_GBps": gather_bytes / (tile_ms * 1e-3) / 1e9 if tile_ms > 0 else None,
                      # the bound that applies to the tile path: every condensed column

@@ -104,11 +104,13 @@ int hcs_set_scalar_variant(int variant);
  * executors.py:111-141 tile_window for every window of a tile plan, on warp-independent
  * workers: each warp owns a balanced range of (window, feature slice, 64-column chunk) work
  * with its own cp.async ring and mma.sync (bf16 m16n8k16, or tf32 m16n8k8 for an fp32 plan),
- * fp32 register accumulators; windows cut by a warp boundary are summed in warp order by a
- * fix-up launch, so results are deterministic.  (Round 1's warp-specialised tcgen05 / mma.sync
- * pipeline engines were removed in round 2: DESIGN.md section 4.)
- * workspace: >= hcs_tile_scratch_floats() floats (split-window partial sums); one workspace
- * must not be shared by launches that can run concurrently. */
+ * fp32 register accumulators; windows cut by a warp boundary are summed in warp order by the
+ * last of their warps to finish (completion counters in the workspace), so results are
+ * deterministic and one product is one launch.  (Round 1's warp-specialised tcgen05 / mma.sync
+ * pipeline engines and its fix-up launch were removed in round 2: DESIGN.md section 4.)
+ * workspace: >= hcs_tile_scratch_floats() floats: split-window completion counters followed by
+ * partial sums.  It must be ZEROED before its first use (the kernels leave the counters zero
+ * again), and one workspace must not be shared by launches that can run concurrently. */
 int hcs_tile_scratch_floats(int64_t* floats);
 /* engine 2 row-slice width in 16-B vectors: 0 auto (8 for dim > 32, else 4), 4 or 8 */
 int hcs_set_tile_slice(int vectors);

@@ -384,7 +384,119 @@ __global__ void __launch_bounds__(kScalarWarps * 32, FUSED ? 1 : HCS_SCALAR_MINB
   }
 }
 
-static int g_scalar_variant = 0;  // 0 auto (warp-per-window), 1 block-per-window kernel, 2 warp kernel with 16-B vectors
+// K3, small window lists (C1-sized graphs, where one product is a few microseconds and latency
+// bound).  The warp-per-window kernel walks a window's rows in dependent rounds: 22.6 us for C1's
+// 169 scalar windows at N = 128.  Here one warp per ROW: the row's (col, value) pairs are read 32
+// at a time (one coalesced load per lane, the next batch prefetched), broadcast by shuffles, and
+// the warp's G = 32/L lane groups gather the X rows of entries g, g+G, ... of the batch with all
+// of a group's loads in flight; a fixed shuffle tree sums the groups (deterministic).  C1 scalar
+// windows: 10.3 us (tools/exp_c1.py; a variant that also cut hub rows into pieces spread over the
+// block's warps, summed in shared memory, was slower: 12.3 us -- the barrier and the extra
+// prologue cost more than the hub row's serial batches).
+template <typename XT, typename VT, int VB, int U>
+__global__ void __launch_bounds__(256, 1) k_spmm_scalar_rows(const int64_t* __restrict__ row_ptr,
+                                                          const int32_t* __restrict__ col, const VT* __restrict__ val,
+                                                          int64_t n_rows, int wh, const int32_t* __restrict__ win_list,
+                                                          int64_t n_list, const XT* __restrict__ x, int dim,
+                                                          int64_t ldx, float* __restrict__ z, int64_t ldz) {
+  constexpr int E = VB / (int)sizeof(XT);
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int64_t wi = gw / wh;
+  if (wi >= n_list) return;
+  const int64_t rs = (int64_t)__ldg(win_list + wi) * wh + (gw - wi * wh);
+  if (rs >= n_rows) return;
+  const uint64_t keep = policy_evict_last();
+  const uint64_t strm = stream_policy();
+  const int64_t kb = __ldg(row_ptr + rs), ke = __ldg(row_ptr + rs + 1);
+  const int nvec_total = (dim + E - 1) / E;
+  const int64_t ldxb = ldx * (int64_t)sizeof(XT);
+  for (int fs = 0; fs < nvec_total; fs += 32) {
+    const int L = min(32, nvec_total - fs);
+    const int G = 32 / L;
+    const int g = lane / L, v = lane - g * L;
+    const int f0 = (fs + v) * E;
+    const char* xb = reinterpret_cast<const char*>(x + f0);
+    float acc[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) acc[i] = 0.f;
+    int cn = 0;
+    float an = 0.f;
+    if (kb + lane < ke) {
+      cn = ld_stream_s32(col + kb + lane, strm);
+      an = load_val(val + kb + lane, strm);
+    }
+    for (int64_t k0 = kb; k0 < ke; k0 += 32) {
+      const int nb = (int)(ke - k0 < 32 ? ke - k0 : 32);
+      const int c = cn;
+      const float a = an;
+      if (k0 + 32 + lane < ke) {  // next batch's pairs under this batch's gathers
+        cn = ld_stream_s32(col + k0 + 32 + lane, strm);
+        an = load_val(val + k0 + 32 + lane, strm);
+      }
+      for (int j0 = 0; j0 < nb; j0 += G * U) {
+        XRaw<VB> xv[U];
+        float av[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int j = j0 + g + u * G;
+          const int cj = __shfl_sync(0xffffffffu, c, j & 31);
+          av[u] = __shfl_sync(0xffffffffu, a, j & 31);
+          xv[u].zero();
+          if (g < G && j < nb) {
+            xv[u].load(xb + (int64_t)cj * ldxb, keep);
+          } else {
+            av[u] = 0.f;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) fma_raw<XT, VB>(acc, xv[u].w, av[u]);
+      }
+    }
+    for (int sft = 1; sft < G; sft <<= 1) {  // fixed-order tree over the G lane groups
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const float o = __shfl_down_sync(0xffffffffu, acc[i], sft * L);
+        if ((g % (2 * sft)) == 0 && g + sft < G) acc[i] += o;
+      }
+    }
+    if (g == 0) {
+      float* zr = z + rs * ldz + f0;
+      if (f0 + E <= dim) {
+#pragma unroll
+        for (int i = 0; i < E; i += 4)
+          reinterpret_cast<float4*>(zr)[i / 4] = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i)
+          if (f0 + i < dim) zr[i] = acc[i];
+      }
+    }
+  }
+}
+
+template <typename XT, typename VT>
+static int launch_scalar_rows(const int64_t* row_ptr, const int32_t* col, const VT* val, int64_t n_rows, int wh,
+                              const int32_t* win_list, int64_t n_list, const XT* x, int dim, int64_t ldx, float* z,
+                              int64_t ldz, bool v32, cudaStream_t st) {
+  const unsigned grid = (unsigned)((n_list * wh + 7) / 8);
+  if (v32)
+    k_spmm_scalar_rows<XT, VT, 32, 8><<<grid, 256, 0, st>>>(row_ptr, col, val, n_rows, wh, win_list, n_list, x, dim,
+                                                            ldx, z, ldz);
+  else
+    k_spmm_scalar_rows<XT, VT, 16, 8><<<grid, 256, 0, st>>>(row_ptr, col, val, n_rows, wh, win_list, n_list, x, dim,
+                                                            ldx, z, ldz);
+  return HCS_OK;
+}
+
+// window lists up to this length use the row kernel in auto mode (one warp per row; small graphs)
+#ifndef HCS_SCALAR_ROWS_MAX
+#define HCS_SCALAR_ROWS_MAX 1024
+#endif
+
+// 0 auto (rows kernel for short lists, else warp-per-window), 1 block-per-window kernel, 2 warp kernel with
+// 16-B vectors, 3 rows kernel, 4 warp-per-window kernel
+static int g_scalar_variant = 0;
 
 template <bool FUSED, typename XT, typename VT>
 static int launch_scalar_w(const int64_t* row_ptr, const int32_t* col, const VT* val, int64_t n_rows, int wh,
@@ -405,7 +517,7 @@ static int launch_scalar_w(const int64_t* row_ptr, const int32_t* col, const VT*
 // 32-byte X vectors when every row slice is 32-byte aligned and padded
 static bool scalar_v32(const void* x, int x_dtype, int64_t ldx, int dim) {
   const int xs = x_dtype == HCS_DTYPE_BF16 ? 2 : 4, e32 = 32 / xs;
-  return g_scalar_variant == 0 && ((uintptr_t)x & 31) == 0 && (ldx * xs) % 32 == 0 &&
+  return (g_scalar_variant == 0 || g_scalar_variant >= 3) && ((uintptr_t)x & 31) == 0 && (ldx * xs) % 32 == 0 &&
          ldx >= ((dim + e32 - 1) / e32) * e32;
 }
 
@@ -413,9 +525,10 @@ static bool scalar_v32(const void* x, int x_dtype, int64_t ldx, int dim) {
 
 using namespace hcs;
 
-// Scalar-path kernel choice (experiments): 0 auto, 1 block-per-window, 2 warp-per-window with 16-B vectors.
+// Scalar-path kernel choice (experiments): 0 auto, 1 block-per-window, 2 warp-per-window with 16-B vectors,
+// 3 warp-per-row (the small-list kernel), 4 warp-per-window whatever the list length.
 extern "C" int hcs_set_scalar_variant(int variant) {
-  HCS_REQUIRE(variant >= 0 && variant <= 2, HCS_EINVAL, "scalar variant must be 0, 1 or 2 (got %d)", variant);
+  HCS_REQUIRE(variant >= 0 && variant <= 4, HCS_EINVAL, "scalar variant must be 0..4 (got %d)", variant);
   g_scalar_variant = variant;
   return HCS_OK;
 }
@@ -435,6 +548,22 @@ extern "C" int hcs_spmm_scalar(const int64_t* row_ptr, const int32_t* col_idx, c
   HCS_REQUIRE(((uintptr_t)x & 15) == 0 && ((uintptr_t)z & 15) == 0, HCS_EINVAL, "x/z must be 16-byte aligned");
   if (n_list == 0) return HCS_OK;
   cudaStream_t st = as_stream(stream);
+  if (g_scalar_variant == 3 || (g_scalar_variant == 0 && n_list <= HCS_SCALAR_ROWS_MAX)) {
+    const bool v32 = scalar_v32(x, x_dtype, ldx, dim);
+    if (x_dtype == HCS_DTYPE_BF16 && values_dtype == HCS_DTYPE_BF16)
+      HCS_TRY(launch_scalar_rows(row_ptr, col_idx, (const __nv_bfloat16*)values, n_rows, wh, win_list, n_list,
+                                 (const __nv_bfloat16*)x, dim, ldx, z, ldz, v32, st));
+    else if (x_dtype == HCS_DTYPE_BF16 && values_dtype == HCS_DTYPE_F32)
+      HCS_TRY(launch_scalar_rows(row_ptr, col_idx, (const float*)values, n_rows, wh, win_list, n_list,
+                                 (const __nv_bfloat16*)x, dim, ldx, z, ldz, v32, st));
+    else if (x_dtype == HCS_DTYPE_F32 && values_dtype == HCS_DTYPE_F32)
+      HCS_TRY(launch_scalar_rows(row_ptr, col_idx, (const float*)values, n_rows, wh, win_list, n_list,
+                                 (const float*)x, dim, ldx, z, ldz, v32, st));
+    else
+      return set_error(HCS_EINVAL, "unsupported dtype combination x=%d values=%d", x_dtype, values_dtype);
+    HCS_LAUNCH_CHECK("k_spmm_scalar_rows");
+    return HCS_OK;
+  }
   if (g_scalar_variant != 1 && wh <= 31) {
     const bool v32 = scalar_v32(x, x_dtype, ldx, dim);
     if (x_dtype == HCS_DTYPE_BF16 && values_dtype == HCS_DTYPE_BF16)

@@ -15,8 +15,8 @@
 //           group walk one balanced range of (window, chunk) positions, one slice each, so
 //           a chunk's plan is read once and an X row's slices are fetched together;
 //           ranges may cut a unit, whose partial sums then go to two scratch slots per
-//           warp and are added in range order by k_tile_warp_fixup (deterministic, no
-//           float atomics);
+//           warp; the last warp of the unit to finish adds them in range order
+//           (deterministic, no float atomics; split_arrive below);
 //   chunk = gather 64 X-row slices (cp.async 16 B, L2 evict_last, 3-stage ring per warp,
 //           XOR-swizzled for conflict-free ldmatrix.trans), build the 16 x 64 bf16 slab
 //           from the packed entries (prefetched into registers one chunk ahead; the slab is
@@ -132,6 +132,88 @@ __device__ __forceinline__ void warp_range(int64_t total, int64_t nwarps, int64_
   b = (total * (gw + 1)) / nwarps;
 }
 
+// ---------------------------------------------------------------- split units, in-kernel
+// A unit (or, for the fused out partials, a window) cut by warp-range boundaries is finished
+// by the LAST of its warps to arrive: every participant writes its partial slot, fences and
+// adds the number of positions it covered to the unit's counter (indexed by the opening
+// warp); the one that completes the count sums the slots in range order (opener's tail slot
+// 1, then each later warp's head slot 0) -- the same order whichever warp arrives last, so
+// results are deterministic -- writes Z and resets the counter to zero for the next launch.
+// Replaces round 1's fix-up launch (O(nwarps) scan per warp; 10 us on a 2 K-node graph).
+
+// workspace layout: [z counters | out counters] (kCntWords u32 each) then the partial slots
+constexpr int kMaxWarpsPerCta = 16;
+inline int64_t tile_cnt_words() { return ((int64_t)num_sms() * kMaxWarpsPerCta + 31) / 32 * 32; }
+
+// group of a balanced split of `total` positions over `ng` ranges that owns position v
+// (largest g with floor(total * g / ng) <= v; see warp_range)
+__device__ __forceinline__ int64_t range_owner(int64_t total, int64_t ng, int64_t v) {
+  return ((v + 1) * ng - 1) / total;
+}
+
+// all lanes: after writing this warp's slot for the split unit [us, ue); (a, b) = our range.
+// Returns true in the warp that must reduce (the last to arrive).
+__device__ __forceinline__ bool split_arrive(unsigned* cnt, int64_t us, int64_t ue, int64_t a, int64_t b, int lane) {
+  __syncwarp();
+  int last = 0;
+  if (lane == 0) {
+    const unsigned mine = (unsigned)((b < ue ? b : ue) - (a > us ? a : us));
+    __threadfence();
+    const unsigned old = atomicAdd(cnt, mine);
+    if (old + mine == (unsigned)(ue - us)) {
+      last = 1;
+      *cnt = 0u;
+    }
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (last) __threadfence();
+  return last != 0;
+}
+
+// acc = sum of the split unit's partial slots in range order. Slots of warp w: slots + (2w + s) *
+// SLOT floats (s = 1: the unit it opened, s = 0: the unit it continued); warp of group k = k * FSm + fw.
+template <int NT, int SLOT>
+__device__ __forceinline__ void split_reduce(const float* __restrict__ slots, int64_t total, int64_t ng, int64_t g_o,
+                                             int FSm, int fw, int64_t ue, float (&acc)[NT][4], int lane) {
+  const float* s = slots + ((g_o * FSm + fw) * 2 + 1) * (int64_t)SLOT;
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[nt][q] = __ldcg(s + (nt * 4 + q) * 32 + lane);
+  // range bounds floor(total * k / ng) stepped incrementally (no 64-bit division in the loop)
+  const int64_t tq = total / ng, tr = total - tq * ng;
+  int64_t bk = (total * (g_o + 1)) / ng, br = total * (g_o + 1) - bk * ng;
+  for (int64_t k = g_o + 1; k < ng; ++k) {
+    const int64_t ak = bk;
+    bk += tq;
+    br += tr;
+    if (br >= ng) {
+      ++bk;
+      br -= ng;
+    }
+    if (ak >= bk) continue;
+    const float* sk = slots + ((k * FSm + fw) * 2 + 0) * (int64_t)SLOT;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[nt][q] += __ldcg(sk + (nt * 4 + q) * 32 + lane);
+    if (ue <= bk) break;
+  }
+}
+
+// the out counters follow the z counters (grid = num_sms() for every tile launch)
+__device__ __forceinline__ int64_t tile_cnt_words_dev() {
+  return ((int64_t)gridDim.x * kMaxWarpsPerCta + 31) / 32 * 32;
+}
+
+template <int NT>
+__device__ __forceinline__ void write_slot(float* __restrict__ slot, const float (&acc)[NT][4], int lane) {
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) __stcg(slot + (nt * 4 + q) * 32 + lane, acc[nt][q]);
+}
+
 template <int SWV>
 __device__ __forceinline__ void store_slice(float* __restrict__ z, int64_t ldz, int64_t rs, int rows, int dim, int f,
                                             const float (&acc)[SWV][4], int lane) {
@@ -154,14 +236,78 @@ __device__ __forceinline__ void store_slice(float* __restrict__ z, int64_t ldz, 
   }
 }
 
+constexpr int kFusedOutMax = 64;        // d_out of the warp kernel's fused epilogue
+constexpr int kFusedLdw = 128 + 8;      // bf16 per M^T row (d_in <= 128)
+constexpr int kOutSlot = 16 * kFusedOutMax;
+
+// fused epilogue: a window's 16 x d_out out rows (accumulator layout of m16n8 tiles)
+template <int NO>
+__device__ __forceinline__ void store_out(float* __restrict__ out, int64_t ldo, int64_t rs, int rows, int d_out,
+                                          const float (&oacc)[NO][4], int lane) {
+  const int r0 = lane >> 2, cc = (lane & 3) * 2;
+#pragma unroll
+  for (int n8 = 0; n8 < NO; ++n8)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = r0 + 8 * (q >> 1), col = n8 * 8 + cc + (q & 1);
+      if (r < rows && col < d_out) out[(rs + r) * ldo + col] = oacc[n8][q];
+    }
+}
+
+// Split-unit finish for Z: arrive on the unit's counter; the last warp sums the slots and stores.
+// Everything that locates the unit in the balanced split is recomputed here from kernel
+// parameters (rare path), so none of it stays live across the gather/MMA loop (the 32-feature
+// kernel runs at its 128-register cap).  unit = (window chunk base, slice f) of a sequence of
+// FSr = (paired ? 1 : FS) slices per window; warp of group k = k * FSm + fw (FSm = paired ? FS : 1).
+template <int SWV, int SLOT>
+__device__ __forceinline__ void finish_split_z(const int64_t* __restrict__ chunk_ptr, int64_t T, int FS, int paired,
+                                               int warps_per_cta, unsigned* __restrict__ cnt,
+                                               const float* __restrict__ slots, float* __restrict__ z, int64_t ldz,
+                                               int64_t base, int f, int nj, int64_t rs, int rows, int dim) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t)blockIdx.x * warps_per_cta + (threadIdx.x >> 5);
+  const int64_t nwarps = (int64_t)gridDim.x * warps_per_cta;
+  const int FSr = paired ? 1 : FS, FSm = paired ? FS : 1;
+  const int fw = paired ? (int)(gw % FS) : 0;
+  const int64_t ng = nwarps / FSm, gi = gw / FSm;
+  const int64_t c0 = __ldg(chunk_ptr);
+  const int64_t total = (int64_t)FSr * (__ldg(chunk_ptr + T) - c0);
+  int64_t a, b;
+  warp_range(total, ng, gi, a, b);
+  const int64_t us = (int64_t)FSr * (base - c0) + (int64_t)f * nj;
+  const int64_t g_o = range_owner(total, ng, us);
+  if (!split_arrive(cnt + g_o * FSm + fw, us, us + nj, a, b, lane)) return;
+  float acc[SWV][4];
+  split_reduce<SWV, SLOT>(slots, total, ng, g_o, FSm, fw, us + nj, acc, lane);
+  store_slice<SWV>(z, ldz, rs, rows, dim, f + fw, acc, lane);
+}
+
+// the same for a window's fused out rows (non-paired sequence; window = positions
+// [FS (base - c0), + FS nj); its counters follow the z counters)
+__device__ __forceinline__ void finish_split_out(const int64_t* __restrict__ chunk_ptr, int64_t T, int FS,
+                                                 int warps_per_cta, unsigned* __restrict__ cnt,
+                                                 const float* __restrict__ oslots, float* __restrict__ out,
+                                                 int64_t ldo, int64_t base, int nj, int64_t rs, int rows, int d_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (int64_t)blockIdx.x * warps_per_cta + (threadIdx.x >> 5);
+  const int64_t ng = (int64_t)gridDim.x * warps_per_cta;
+  const int64_t c0 = __ldg(chunk_ptr);
+  const int64_t total = (int64_t)FS * (__ldg(chunk_ptr + T) - c0);
+  int64_t a, b;
+  warp_range(total, ng, gw, a, b);
+  const int64_t ws = (int64_t)FS * (base - c0), we = ws + (int64_t)FS * nj;
+  const int64_t g_o = range_owner(total, ng, ws);
+  if (!split_arrive(cnt + tile_cnt_words_dev() + g_o, ws, we, a, b, lane)) return;
+  float oacc[kFusedOutMax / 8][4];
+  split_reduce<kFusedOutMax / 8, kOutSlot>(oslots, total, ng, g_o, 1, 0, we, oacc, lane);
+  store_out(out, ldo, rs, rows, d_out, oacc, lane);
+}
+
 // Fused GCN epilogue (K6/K7) of the warp kernel: after each (window, slice) unit the
 // warp multiplies its 16 x 64 aggregated slice (bf16 A fragments taken straight from the
 // accumulators) by the matching 64 x d_out block of M (bf16 M^T resident in shared
 // memory) into an out accumulator; a window's out rows are written when its last slice
-// is done, or summed in warp order by k_tile_warp_fixup_out when a warp boundary cuts it.
-constexpr int kFusedOutMax = 64;        // d_out of the warp kernel's fused epilogue
-constexpr int kFusedLdw = 128 + 8;      // bf16 per M^T row (d_in <= 128)
-constexpr int kOutSlot = 16 * kFusedOutMax;
+// is done, or summed in warp order by the last of its warps to finish when a warp boundary cuts it.
 
 // NPR = 16-feature groups of a slice that hold features (compile time, so the unrolled
 // ldmatrix/mma schedule is kept): SWV/2, or 3 for a single 33..48-feature slice (the 41-wide
@@ -173,7 +319,7 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
                 const uint32_t* __restrict__ ent, int64_t n_rows, int wh, const __nv_bfloat16* __restrict__ x,
                 int64_t ldx, int dim, int FS, float* __restrict__ z, int64_t ldz, float* __restrict__ scratch,
                 const float* __restrict__ mw, int d_out, float* __restrict__ out, int64_t ldo,
-                float* __restrict__ oscratch, int paired) {
+                float* __restrict__ oscratch, int paired, unsigned* __restrict__ cnt) {
   using C = WarpCfg<SWV>;
   constexpr int kWarpTileWarps = C::kWarps, kWarpStageBytes = C::kStageBytes, kWarpSmemPerWarp = C::kPerWarp;
   constexpr int NI = C::kIssue;
@@ -378,20 +524,19 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
 #pragma unroll
       for (int q = 0; q < 4; ++q) sts128_zero(slab + (lane + 32 * q) * 16);
     }
-    // end of our part of the unit: Z (whole unit) or a scratch slot (split unit)
+    // end of our part of the unit: Z (whole unit) or a scratch slot (split unit; the last of
+    // its warps to arrive sums the slots in range order, below)
     const bool unit_done = P0.j + 1 == P0.nj;
     if (unit_done || P0.rem == 1) {
       const int64_t rs = (int64_t)__ldg(tile_list + P0.t) * wh;
       const int rows = (int)(n_rows - rs < wh ? n_rows - rs : wh);
+      bool zsplit = false;
       if (z != nullptr) {
         if (!in_head && unit_done) {
           store_slice<SWV>(z, ldz, rs, rows, dim, P0.f + fw, acc, lane);
         } else {
-          float* slot = scratch + (gw * 2 + (in_head ? 0 : 1)) * C::kSlot;
-#pragma unroll
-          for (int nt = 0; nt < SWV; ++nt)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) slot[(nt * 4 + q) * 32 + lane] = acc[nt][q];
+          write_slot<SWV>(scratch + (gw * 2 + (in_head ? 0 : 1)) * C::kSlot, acc, lane);
+          zsplit = true;  // finished after the fused epilogue has used acc
         }
       }
       in_head = false;
@@ -419,25 +564,19 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
         const bool win_done = unit_done && P0.f == FS - 1;
         if (win_done || P0.rem == 1) {
           if (win_done && !win_head) {
-            const int r0 = lane >> 2, cc = (lane & 3) * 2;
-#pragma unroll
-            for (int n8 = 0; n8 < kFusedOutMax / 8; ++n8)
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const int r = r0 + 8 * (q >> 1), col = n8 * 8 + cc + (q & 1);
-                if (r < rows && col < d_out) out[(rs + r) * ldo + col] = oacc[n8][q];
-              }
+            store_out(out, ldo, rs, rows, d_out, oacc, lane);
           } else {
-            float* slot = oscratch + (gw * 2 + (win_head ? 0 : 1)) * kOutSlot;
-#pragma unroll
-            for (int n8 = 0; n8 < kFusedOutMax / 8; ++n8)
-#pragma unroll
-              for (int q = 0; q < 4; ++q) slot[(n8 * 4 + q) * 32 + lane] = oacc[n8][q];
+            write_slot(oscratch + (gw * 2 + (win_head ? 0 : 1)) * kOutSlot, oacc, lane);
+            finish_split_out(chunk_ptr, T, FS, kWarpTileWarps, cnt, oscratch, out, ldo, P0.base, P0.nj, rs, rows,
+                             d_out);
           }
 #pragma unroll
           for (int i = 0; i < kFusedOutMax / 8; ++i) oacc[i][0] = oacc[i][1] = oacc[i][2] = oacc[i][3] = 0.f;
         }
       }
+      if (zsplit)
+        finish_split_z<SWV, C::kSlot>(chunk_ptr, T, FS, paired, kWarpTileWarps, cnt, scratch, z, ldz, P0.base, P0.f,
+                                      P0.nj, rs, rows, dim);
 #pragma unroll
       for (int i = 0; i < SWV; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
     }
@@ -479,54 +618,6 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
   cp_async_wait<0>();
 }
 
-// Sums the partial slots of units cut by warp-range boundaries, in warp order.
-template <int SWV>
-__global__ void k_tile_warp_fixup(const int32_t* __restrict__ tile_list, int64_t T,
-                                  const int64_t* __restrict__ chunk_ptr, int64_t n_rows, int wh, int dim, int FS,
-                                  float* __restrict__ z, int64_t ldz, const float* __restrict__ scratch,
-                                  int64_t nwarps, int paired) {
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (gw >= nwarps) return;
-  // same warp -> range mapping as k_tile_warp (paired: group gw / FS, slice gw % FS)
-  const int FSr = paired ? 1 : FS;
-  const int fw = paired ? (int)(gw % FS) : 0;
-  const int64_t ngroups = paired ? nwarps / FS : nwarps;
-  const int64_t gi = paired ? gw / FS : gw;
-  if (gi >= ngroups) return;
-  const int64_t c0 = chunk_ptr[0];
-  const int64_t total = (int64_t)FSr * (chunk_ptr[T] - c0);
-  int64_t a, b;
-  warp_range(total, ngroups, gi, a, b);
-  if (a >= b) return;
-  const ChunkPos last = locate(chunk_ptr, T, FSr, b - 1);
-  const int64_t ustart = (int64_t)FSr * (last.base - c0) + (int64_t)last.f * last.nj;
-  const int64_t uend = ustart + last.nj;
-  if (!(uend > b && ustart >= a)) return;  // not the warp that opens a split unit
-  constexpr int kSlot = WarpCfg<SWV>::kSlot;
-  float acc[SWV][4];
-  const float* s = scratch + (gw * 2 + 1) * kSlot;
-#pragma unroll
-  for (int nt = 0; nt < SWV; ++nt)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[nt][q] = s[(nt * 4 + q) * 32 + lane];
-  for (int64_t k = gi + 1; k < ngroups; ++k) {  // later ranges of the same slice, in order
-    int64_t ak, bk;
-    warp_range(total, ngroups, k, ak, bk);
-    if (ak >= bk) continue;
-    const int64_t wk = paired ? k * FS + fw : k;
-    const float* sk = scratch + (wk * 2 + 0) * kSlot;
-#pragma unroll
-    for (int nt = 0; nt < SWV; ++nt)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[nt][q] += sk[(nt * 4 + q) * 32 + lane];
-    if (uend <= bk) break;
-  }
-  const int64_t rs = (int64_t)tile_list[last.t] * wh;
-  const int rows = (int)(n_rows - rs < wh ? n_rows - rs : wh);
-  store_slice<SWV>(z, ldz, rs, rows, dim, last.f + fw, acc, lane);
-}
-
 // ---------------------------------------------------------------- tf32 variant
 // Same schedule and fix-up; fp32 X rows (32-feature slices of 128 B), 16 x 64 fp32 slab,
 // mma.sync m16n8k8 tf32 (X and values RNA-rounded to tf32 by the caller / plan).
@@ -544,7 +635,7 @@ __device__ __forceinline__ int swz_tf(int k, int v) { return v ^ ((2 * k) & 6); 
 // aggregated slice (tf32 A fragments taken from the accumulators, features permuted within each
 // 8-block so no shuffle is needed) by the slice's 32 x d_out block of M (tf32-rounded, read from
 // global / L1: the kernel's shared memory is full) into an out accumulator; window partials cut by
-// a warp boundary go to oscratch and are summed in warp order by k_tile_warp_fixup_out.
+// a warp boundary go to oscratch and are summed in warp order by the last of its warps.
 template <bool FUSED>
 __global__ void __launch_bounds__(kTfWarps * 32, 1)
     k_tile_warp_tf32(const int32_t* __restrict__ tile_list, int64_t T, const int64_t* __restrict__ chunk_ptr,
@@ -552,7 +643,7 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
                      const uint2* __restrict__ ent, int64_t n_rows, int wh, const float* __restrict__ x, int64_t ldx,
                      int dim, int FS, float* __restrict__ z, int64_t ldz, float* __restrict__ scratch,
                      const float* __restrict__ mw, int d_out, float* __restrict__ out, int64_t ldo,
-                     float* __restrict__ oscratch) {
+                     float* __restrict__ oscratch, unsigned* __restrict__ cnt) {
   constexpr int NI = 16;
   extern __shared__ uint8_t tsmem_raw[];
   uint8_t* tsmem = (uint8_t*)(((uintptr_t)tsmem_raw + 127) & ~(uintptr_t)127);
@@ -711,15 +802,13 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
     if (unit_done || p0.fi + 1 == b) {
       const int64_t rs = (int64_t)__ldg(tile_list + p0.t) * wh;
       const int rows = (int)(n_rows - rs < wh ? n_rows - rs : wh);
+      bool zsplit = false;
       if (z != nullptr) {
         if (!in_head && unit_done) {
           store_slice<4>(z, ldz, rs, rows, dim, p0.f, acc, lane);
         } else {
-          float* slot = scratch + (gw * 2 + (in_head ? 0 : 1)) * WarpCfg<4>::kSlot;
-#pragma unroll
-          for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) slot[(nt * 4 + q) * 32 + lane] = acc[nt][q];
+          write_slot<4>(scratch + (gw * 2 + (in_head ? 0 : 1)) * WarpCfg<4>::kSlot, acc, lane);
+          zsplit = true;
         }
       }
       in_head = false;
@@ -749,24 +838,18 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
         const bool win_done = unit_done && p0.f == FS - 1;
         if (win_done || p0.fi + 1 == b) {
           if (win_done && !win_head) {
-#pragma unroll
-            for (int n8 = 0; n8 < NO; ++n8)
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                const int r = g8 + 8 * (q >> 1), col = n8 * 8 + 2 * t4 + (q & 1);
-                if (r < rows && col < d_out) out[(rs + r) * ldo + col] = oacc[n8][q];
-              }
+            store_out(out, ldo, rs, rows, d_out, oacc, lane);
           } else {
-            float* slot = oscratch + (gw * 2 + (win_head ? 0 : 1)) * kOutSlot;
-#pragma unroll
-            for (int n8 = 0; n8 < NO; ++n8)
-#pragma unroll
-              for (int q = 0; q < 4; ++q) slot[(n8 * 4 + q) * 32 + lane] = oacc[n8][q];
+            write_slot<NO>(oscratch + (gw * 2 + (win_head ? 0 : 1)) * kOutSlot, oacc, lane);
+            finish_split_out(chunk_ptr, T, FS, kTfWarps, cnt, oscratch, out, ldo, p0.base, p0.nj, rs, rows, d_out);
           }
 #pragma unroll
           for (int i = 0; i < NO; ++i) oacc[i][0] = oacc[i][1] = oacc[i][2] = oacc[i][3] = 0.f;
         }
       }
+      if (zsplit)
+        finish_split_z<4, WarpCfg<4>::kSlot>(chunk_ptr, T, FS, 0, kTfWarps, cnt, scratch, z, ldz, p0.base, p0.f,
+                                             p0.nj, rs, rows, dim);
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
     }
@@ -785,11 +868,6 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
   cp_async_wait<0>();
 }
 
-__global__ void k_tile_warp_fixup_out(const int32_t* __restrict__ tile_list, int64_t T,
-                                      const int64_t* __restrict__ chunk_ptr, int64_t n_rows, int wh, int FS,
-                                      int d_out, float* __restrict__ out, int64_t ldo,
-                                      const float* __restrict__ oscratch, int64_t nwarps);
-
 // tf32 SpMM (m == nullptr) or fused GCN layer (m = tf32-rounded M [dim x d_out], d_out <= 64; z may
 // be nullptr when no z_cache is wanted).
 int spmm_tile_warp_tf32(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
@@ -800,73 +878,18 @@ int spmm_tile_warp_tf32(const int32_t* tile_list, int64_t n_tile, const int64_t*
   const int grid = num_sms();
   const int64_t nwarps = (int64_t)grid * kTfWarps;
   const bool fused = m != nullptr;
-  const int64_t need = nwarps * 2 * (WarpCfg<4>::kSlot + (fused ? kOutSlot : 0));
+  const int64_t cw = 2 * tile_cnt_words();
+  const int64_t need = cw + nwarps * 2 * (WarpCfg<4>::kSlot + (fused ? kOutSlot : 0));
   HCS_REQUIRE(scratch != nullptr && scratch_floats >= need, HCS_EINVAL, "tile scratch too small");
-  float* oscratch = scratch + nwarps * 2 * WarpCfg<4>::kSlot;
+  unsigned* cnt = reinterpret_cast<unsigned*>(scratch);
+  float* slots = scratch + cw;
+  float* oscratch = slots + nwarps * 2 * WarpCfg<4>::kSlot;
   auto kern = fused ? k_tile_warp_tf32<true> : k_tile_warp_tf32<false>;
   HCS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kTfSmem));
   kern<<<grid, kTfWarps * 32, kTfSmem, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim,
-                                             FS, z, ldz, scratch, m, d_out, out, ldo, oscratch);
+                                             FS, z, ldz, slots, m, d_out, out, ldo, oscratch, cnt);
   HCS_LAUNCH_CHECK("k_tile_warp_tf32");
-  const int fix_threads = 256;
-  const int fix_blocks = (int)((nwarps * 32 + fix_threads - 1) / fix_threads);
-  if (z != nullptr) {
-    k_tile_warp_fixup<4><<<fix_blocks, fix_threads, 0, st>>>(tile_list, n_tile, chunk_ptr, n_rows, wh, dim, FS, z,
-                                                              ldz, scratch, nwarps, 0);
-    HCS_LAUNCH_CHECK("k_tile_warp_fixup");
-  }
-  if (fused) {
-    k_tile_warp_fixup_out<<<fix_blocks, fix_threads, 0, st>>>(tile_list, n_tile, chunk_ptr, n_rows, wh, FS, d_out,
-                                                               out, ldo, oscratch, nwarps);
-    HCS_LAUNCH_CHECK("k_tile_warp_fixup_out");
-  }
   return HCS_OK;
-}
-
-// Sums the fused-epilogue out partials of windows cut by warp-range boundaries, in warp order.
-__global__ void k_tile_warp_fixup_out(const int32_t* __restrict__ tile_list, int64_t T,
-                                      const int64_t* __restrict__ chunk_ptr, int64_t n_rows, int wh, int FS,
-                                      int d_out, float* __restrict__ out, int64_t ldo,
-                                      const float* __restrict__ oscratch, int64_t nwarps) {
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (gw >= nwarps) return;
-  const int64_t c0 = chunk_ptr[0];
-  const int64_t total = (int64_t)FS * (chunk_ptr[T] - c0);
-  int64_t a, b;
-  warp_range(total, nwarps, gw, a, b);
-  if (a >= b) return;
-  const ChunkPos last = locate(chunk_ptr, T, FS, b - 1);
-  const int64_t wstart = (int64_t)FS * (last.base - c0), wend = wstart + (int64_t)FS * last.nj;
-  if (!(wend > b && wstart >= a)) return;
-  constexpr int NO = kFusedOutMax / 8;
-  float acc[NO][4];
-  const float* s = oscratch + (gw * 2 + 1) * kOutSlot;
-#pragma unroll
-  for (int n8 = 0; n8 < NO; ++n8)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[n8][q] = s[(n8 * 4 + q) * 32 + lane];
-  for (int64_t k = gw + 1; k < nwarps; ++k) {
-    int64_t ak, bk;
-    warp_range(total, nwarps, k, ak, bk);
-    if (ak >= bk) continue;
-    const float* sk = oscratch + (k * 2 + 0) * kOutSlot;
-#pragma unroll
-    for (int n8 = 0; n8 < NO; ++n8)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[n8][q] += sk[(n8 * 4 + q) * 32 + lane];
-    if (wend <= bk) break;
-  }
-  const int64_t rs = (int64_t)tile_list[last.t] * wh;
-  const int rows = (int)(n_rows - rs < wh ? n_rows - rs : wh);
-  const int r0 = lane >> 2, cc = (lane & 3) * 2;
-#pragma unroll
-  for (int n8 = 0; n8 < NO; ++n8)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int r = r0 + 8 * (q >> 1), col = n8 * 8 + cc + (q & 1);
-      if (r < rows && col < d_out) out[(rs + r) * ldo + col] = acc[n8][q];
-    }
 }
 
 static int g_warp_swv = 0;     // 0 auto, 4 or 8 (16-B vectors per row slice)
@@ -890,10 +913,13 @@ static int launch_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* 
   const int FS = (dim + C::kFeat - 1) / C::kFeat;
   const int grid = num_sms();
   const int64_t nwarps = (int64_t)grid * C::kWarps;
-  const int64_t need = nwarps * 2 * C::kSlot + (FUSED ? nwarps * 2 * kOutSlot : 0);
+  const int64_t cw = 2 * tile_cnt_words();
+  const int64_t need = cw + nwarps * 2 * C::kSlot + (FUSED ? nwarps * 2 * kOutSlot : 0);
   HCS_REQUIRE(scratch != nullptr && scratch_floats >= need, HCS_EINVAL, "tile scratch too small (%lld floats, need %lld)",
               (long long)scratch_floats, (long long)need);
-  float* oscratch = scratch + nwarps * 2 * C::kSlot;
+  unsigned* cnt = reinterpret_cast<unsigned*>(scratch);
+  float* slots = scratch + cw;
+  float* oscratch = slots + nwarps * 2 * C::kSlot;
   const int smem = C::kSmem + (FUSED ? kFusedOutMax * kFusedLdw * 2 : 0);
   const bool want = g_warp_paired == 1 || (g_warp_paired == 2 && x_rows * ldx * 2 > kPairMinXBytes);
   const int paired = (!FUSED && FS > 1 && want && C::kWarps % FS == 0) ? 1 : 0;
@@ -905,20 +931,8 @@ static int launch_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* 
                   : k_tile_warp<SWV, FUSED>;
   HCS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   kern<<<grid, C::kWarps * 32, smem, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim,
-                                            FS, z, ldz, scratch, mw, d_out, out, ldo, oscratch, paired);
+                                            FS, z, ldz, slots, mw, d_out, out, ldo, oscratch, paired, cnt);
   HCS_LAUNCH_CHECK("k_tile_warp");
-  const int fix_threads = 256;
-  const int fix_blocks = (int)((nwarps * 32 + fix_threads - 1) / fix_threads);
-  if (z != nullptr) {
-    k_tile_warp_fixup<SWV><<<fix_blocks, fix_threads, 0, st>>>(tile_list, n_tile, chunk_ptr, n_rows, wh, dim, FS, z,
-                                                                ldz, scratch, nwarps, paired);
-    HCS_LAUNCH_CHECK("k_tile_warp_fixup");
-  }
-  if (FUSED) {
-    k_tile_warp_fixup_out<<<fix_blocks, fix_threads, 0, st>>>(tile_list, n_tile, chunk_ptr, n_rows, wh, FS, d_out,
-                                                               out, ldo, oscratch, nwarps);
-    HCS_LAUNCH_CHECK("k_tile_warp_fixup_out");
-  }
   return HCS_OK;
 }
 
@@ -948,7 +962,9 @@ int spmm_tile_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chun
 }
 
 int64_t tile_warp_scratch_floats() {
-  return std::max<int64_t>(
+  static_assert(WarpCfg<4>::kWarps <= kMaxWarpsPerCta && WarpCfg<8>::kWarps <= kMaxWarpsPerCta &&
+                    kTfWarps <= kMaxWarpsPerCta, "split counters");
+  return 2 * tile_cnt_words() + std::max<int64_t>(
       std::max<int64_t>((int64_t)num_sms() * WarpCfg<4>::kWarps * 2 * WarpCfg<4>::kSlot,
                         (int64_t)num_sms() * WarpCfg<8>::kWarps * 2 * (WarpCfg<8>::kSlot + kOutSlot)),
       (int64_t)num_sms() * WarpCfg<16>::kWarps * 2 * WarpCfg<16>::kSlot);

@@ -253,11 +253,12 @@ class HybridPlan:
         return self._cache_d
 
     def new_scratch(self) -> torch.Tensor:
-        """A fresh partial-sum buffer for the tile kernel's split windows (include/hcspmm.h: a
+        """A fresh workspace for the tile kernel's split windows: completion counters (zero
+        when first used; the kernels leave them zero) and partial-sum slots (include/hcspmm.h: a
         workspace must not be shared by launches that may run concurrently)."""
         n = _lib.ctypes.c_int64(0)
         _lib.check(_lib.lib().hcs_tile_scratch_floats(_lib.ctypes.byref(n)))
-        return torch.empty(max(int(n.value), 1), dtype=torch.float32, device=self.tile_list.device)
+        return torch.zeros(max(int(n.value), 1), dtype=torch.float32, device=self.tile_list.device)
 
     def scratch(self, stream: int | None = None) -> torch.Tensor:
         """Partial-sum slots of the tile kernel, one buffer per CUDA stream: launches on one
@@ -271,8 +272,9 @@ class HybridPlan:
         return buf
 
     def launches_per_run(self, dim: int) -> int:
-        """Kernels of one run(): engine 2 = tile kernel + fix-up, plus the scalar kernel."""
-        return (2 if self.n_tile else 0) + (1 if self.scalar_list.numel() else 0)
+        """Kernels of one run(): the tile kernel (split windows finished in-kernel) plus the
+        scalar kernel."""
+        return (1 if self.n_tile else 0) + (1 if self.scalar_list.numel() else 0)
 
     def parts(self, k: int) -> list[tuple[int, int, int, int, int, int]]:
         """k contiguous window ranges of ~equal nnz: (w0, w1, tile t0, t1, scalar s0, s1) each."""
@@ -310,6 +312,14 @@ class HybridPlan:
         s = _lib.stream() if stream is None else stream
         t0, t1 = (0, self.n_tile) if part is None else part[2:4]
         s0, s1 = (0, int(self.scalar_list.numel())) if part is None else part[4:6]
+        # small hybrid plans are latency-bound: K3 runs on a side stream next to K4 (forked and
+        # joined on the current stream, so a CUDA-graph capture gets two parallel branches)
+        fork = (stream is None and tile_events is None and t1 > t0 and s1 > s0
+                and len(self.windows) <= CONCURRENT_MAX_WINDOWS)
+        if fork:
+            cur = torch.cuda.current_stream(csr.device)
+            side = _side_stream(csr.device)
+            side.wait_stream(cur)
         if tile_events is not None:
             tile_events[0].record()
         if t1 > t0:
@@ -325,7 +335,20 @@ class HybridPlan:
             _lib.call("hcs_spmm_scalar", csr.row_ptr.data_ptr(), csr.col_idx.data_ptr(), self.scalar_vals.data_ptr(),
                       self.scalar_vals_code, csr.num_rows, self.windows.window_height,
                       self.scalar_list.data_ptr() + 4 * s0, s1 - s0, xop.t.data_ptr(), xop.dtype_code, xop.rows,
-                      xop.dim, xop.ld, z.data_ptr(), ldz, s)
+                      xop.dim, xop.ld, z.data_ptr(), ldz, side.cuda_stream if fork else s)
+        if fork:
+            cur.wait_stream(side)
+
+
+CONCURRENT_MAX_WINDOWS = 8192
+_SIDE_STREAMS: dict = {}
+
+
+def _side_stream(dev) -> torch.cuda.Stream:
+    st = _SIDE_STREAMS.get(dev)
+    if st is None:
+        st = _SIDE_STREAMS[dev] = torch.cuda.Stream(device=dev)
+    return st
 
 
 def get_plan(windows, assignment: Assignment, precision: str) -> HybridPlan:
@@ -605,13 +628,15 @@ def spmm_auto(csr, x, assignment_for, precision: str = "bf16", threads: int = 1)
     return spmm_hybrid(windows, assignment_for(windows), x, precision=precision, threads=threads)
 
 
-_SCALAR_VARIANTS = {"auto": 0, "block": 1, "warp16": 2}
+_SCALAR_VARIANTS = {"auto": 0, "block": 1, "warp16": 2, "rows": 3, "warp": 4}
 
 
 def set_scalar_variant(variant: str = "auto") -> None:
-    """Select the CUDA-core (K3) kernel: "auto" (warp per window, col/val staged in shared
-    memory, 32-byte X vectors when the operand allows), "block" (block per window, one warp
-    per row with a fixed shuffle tree), "warp16" (warp per window, 16-byte vectors)."""
+    """Select the CUDA-core (K3) kernel: "auto" ("rows" for lists of <= 1,024 windows, else
+    "warp"), "warp" (warp per window, col/val staged in shared memory, 32-byte X vectors when the
+    operand allows), "rows" (warp per row, pairs broadcast by shuffles; small graphs), "block"
+    (block per window, one warp per row with a fixed shuffle tree), "warp16" (warp per window,
+    16-byte vectors)."""
     if variant not in _SCALAR_VARIANTS:
         raise ValueError(f"variant must be one of {sorted(_SCALAR_VARIANTS)}, got {variant!r}")
     _lib.call("hcs_set_scalar_variant", _SCALAR_VARIANTS[variant])

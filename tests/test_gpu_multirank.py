@@ -71,17 +71,39 @@ def _worker(rank, world, port, q):
                 t.copy_(h)
 
         csh = _CpuShard(sh.ranges, rank, n)
+        from paper_2412_08902_b200.model import gcn_layer
+
+        with torch.no_grad():  # this run's own layer-1 activation mask (see the test)
+            mask = (gcn_layer(xf, m.w1.detach(), ws, shard=csh) > 0).cpu().numpy()
         loss = m.epoch(xf, labels, ws, shard=csh)
-        q.put((rank, full, float(loss.detach()), m.w1.grad.cpu().numpy(), m.w2.grad.cpu().numpy()))
+        q.put((rank, full, float(loss.detach()), m.w1.grad.cpu().numpy(), m.w2.grad.cpu().numpy(), mask))
     finally:
         dist.destroy_process_group()
+
+
+def _fp64_grads(a_ref, x, labels, w1, w2, mask):
+    """Dense float64 reference of the 2-layer epoch's weight gradients under a given layer-1
+    activation mask (test_gpu_gnn.test_two_layer_training_gradients: bf16 operands move
+    pre-activations near 0 across the ReLU kink, which alone changes grad_W1 by a few %, so each
+    run is compared under its own mask -- the arithmetic is measured, not the mask flips)."""
+    n = a_ref.num_rows
+    rows = np.repeat(np.arange(n), np.diff(a_ref.row_ptr))
+    ad = torch.zeros((n, n), dtype=torch.float64)
+    ad[torch.from_numpy(rows), torch.from_numpy(a_ref.col_idx)] = torch.from_numpy(a_ref.values)
+    ad = ad.cuda()
+    rw1, rw2 = w1.double().requires_grad_(True), w2.double().requires_grad_(True)
+    mk = torch.from_numpy(mask).double().cuda()
+    logits = ad @ ((ad @ x.double() @ rw1) * mk) @ rw2
+    loss = torch.nn.functional.cross_entropy(logits, labels)
+    loss.backward()
+    return float(loss.detach()), rw1.grad.cpu().numpy(), rw2.grad.cpu().numpy()
 
 
 def test_two_ranks_match_one(cuda_ok):
     import torch.multiprocessing as mp
 
     import paper_2412_08902_b200 as hc
-    from paper_2412_08902_b200.model import Gcn2
+    from paper_2412_08902_b200.model import Gcn2, gcn_layer
 
     a_ref = _graph()
     n = a_ref.num_rows
@@ -92,6 +114,9 @@ def test_two_ranks_match_one(cuda_ok):
     xf = torch.from_numpy(np.random.default_rng(2).uniform(-1, 1, (n, 128))).float().cuda()
     labels = torch.from_numpy(np.random.default_rng(3).integers(0, 41, n)).cuda()
     m = Gcn2(128, 64, 41, seed=0)
+    w1, w2 = m.w1.detach().clone(), m.w2.detach().clone()
+    with torch.no_grad():
+        mask1 = (gcn_layer(xf, w1, ws) > 0).cpu().numpy()
     loss1 = float(m.epoch(xf, labels, ws).detach())
     g1, g2 = m.w1.grad.cpu().numpy(), m.w2.grad.cpu().numpy()
     ctx = mp.get_context("spawn")
@@ -104,12 +129,18 @@ def test_two_ranks_match_one(cuda_ok):
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
-    for rank, full, loss, w1g, w2g in res:
+
+    def rel(a, b):
+        return float(np.abs(a - b).max() / np.abs(b).max())
+
+    lr1, r1, r2 = _fp64_grads(a_ref, xf, labels, w1, w2, mask1)
+    assert rel(g1, r1) <= 1e-2 and rel(g2, r2) <= 1e-2, (rel(g1, r1), rel(g2, r2))
+    for rank, full, loss, w1g, w2g, mask in res:
         # the same windows and kernels; only warp-range cut points differ -> fp32 reassociation
         assert np.abs(full - z1).max() <= 1e-5 * np.abs(z1).max()
         assert abs(loss - loss1) <= 1e-5 * abs(loss1)
-        # gradients: the bf16 re-rounding of slightly different fp32 partial sums (layer outputs,
-        # aggregated slices) differs between the runs; grad_W2 passes one bf16 aggregation,
-        # grad_W1 three -- the per-op 1e-2 budget of the reference comparison (test_gpu_gnn.py)
-        assert np.abs(w2g - g2).max() <= 1e-2 * np.abs(g2).max()
-        assert np.abs(w1g - g1).max() <= 3e-2 * np.abs(g1).max()
+        # the sharded epoch's gradients are as accurate as the single-GPU epoch's (same 1e-2
+        # budget against float64 as test_gpu_gnn), each under its own activation mask
+        assert (mask != mask1).mean() < 1e-3
+        _, s1, s2 = _fp64_grads(a_ref, xf, labels, w1, w2, mask)
+        assert rel(w1g, s1) <= 1e-2 and rel(w2g, s2) <= 1e-2, (rank, rel(w1g, s1), rel(w2g, s2))

@@ -299,7 +299,7 @@ def test_async_requests_match_sync(cuda_ok, big):
         hc.spmm_hybrid_async(ws, asg, torch.zeros(n, 8, device="cuda"))
 
 
-@pytest.mark.parametrize("variant", ["auto", "block", "warp16"])
+@pytest.mark.parametrize("variant", ["auto", "warp", "rows", "block", "warp16"])
 @pytest.mark.parametrize("precision", ["bf16", "tf32"])
 def test_scalar_variants(cuda_ok, variant, precision):
     """Every K3 kernel variant == the exact product within the precision's tolerance, on
@@ -310,10 +310,13 @@ def test_scalar_variants(cuda_ok, variant, precision):
 
     tol = BF16_TOL if precision == "bf16" else 1e-3
     rng = np.random.default_rng(7)
-    # rows 0..159: 1-8 nnz; rows 160..239: 40-90 nnz (windows over the cap); 245 rows total
+    # rows 0..159: 1-8 nnz; rows 160..239: 40-90 nnz (windows over the cap); 245 rows total;
+    # a few hub rows of 250-400 nnz (several 32-entry batches in the rows kernel)
     rows, cols = [], []
     for r in range(245):
         k = int(rng.integers(1, 9)) if r < 160 else int(rng.integers(40, 90))
+        if r % 41 == 3:
+            k = int(rng.integers(250, 400))
         if r % 37 == 5:
             k = 0  # empty rows
         cs = rng.choice(900, size=k, replace=False)
