@@ -326,12 +326,8 @@ def run_ours(args):
 
         def step(i=None):
             if world == 1:
-                if graph is not None:
-                    if i is not None:
-                        tev[i][0].record()
+                if graph is not None:  # (no per-step events: each is a node that costs a launch slot)
                     graph.replay()
-                    if i is not None:
-                        tev[i][1].record()
                     return
                 plan.run(xop, z, ldz, tile_events=tev[i] if i is not None else None)
                 return
@@ -366,7 +362,10 @@ def run_ours(args):
             dist.barrier()
         ms = s_ev.elapsed_time(e_ev) / steps
         # per-kernel time only on one GPU (with N ranks the step is split into parts)
-        tile_ms = statistics.mean(a.elapsed_time(b) for a, b in tev) if (plan.n_tile and world == 1) else 0.0
+        if graph is not None:
+            tile_ms = ms  # the whole step is one graph launch
+        else:
+            tile_ms = statistics.mean(a.elapsed_time(b) for a, b in tev) if (plan.n_tile and world == 1) else 0.0
         if world > 1:
             # the same shard's SpMM alone (no exchange), so the line reports both "SpMM only" and
             # "SpMM + all-gather", max over ranks

@@ -449,3 +449,4 @@ def test_spmm_graph_replay(cuda_ok, precision):
         assert torch.equal(g.replay(), 2 * z1)
     with pytest.raises(ValueError, match="CUDA tensor"):
         hc.SpmmGraph(ws, asg, x.cpu())
+
