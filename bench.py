@@ -191,6 +191,10 @@ def dist_setup(args):
             torch.cuda.set_device(0)
             init_process_group("gloo")
         else:
+            # the communicator set-up (ranks, devices, NVLink/NVLS transport) in the log, also when the
+            # driver launches the ranks with torchrun itself; NCCL reads these at communicator init
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             torch.cuda.set_device(local)
             init_process_group("nccl", device=torch.device("cuda", local))
     else:
@@ -353,11 +357,13 @@ def run_ours(args):
         sampler = ClockSampler(local)
         with sampler:
             s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            profile_range(True)
             s_ev.record()
             for i in range(steps):
                 step(i)
             e_ev.record()
             torch.cuda.synchronize()
+            profile_range(False)
         if world > 1:
             dist.barrier()
         ms = s_ev.elapsed_time(e_ev) / steps
@@ -427,7 +433,7 @@ def run_ours(args):
                 reps.append((time.perf_counter() - t1) / k)
             e2e_s = statistics.median(reps)
             # the drop-in call: a rowwin caller passes a float64 DenseMatrix (pageable numpy) and
-            # gets numpy back; every byte of X crosses PCIe as float64 and is converted on the GPU
+            # gets numpy back (conversion to the compute dtype is part of the timed call)
             x64 = hc.DenseMatrix(x.double().cpu().numpy())
             for _ in range(2):
                 hc.spmm_hybrid(ws, asg, x64, precision=args.precision)
@@ -438,6 +444,18 @@ def run_ours(args):
                 del r
             torch.cuda.synchronize()
             dropin_s = (time.perf_counter() - t1) / kd
+            from paper_2412_08902_b200 import executors as _ex
+
+            if n * dim >= _ex.HOST_STAGE_MIN_ELEMS:  # csrc/host_stage.cu: converted on the host, then H2D
+                es = 2 if args.precision == "bf16" else 4
+                sl = (32 if dim <= 32 else 64) if es == 2 else 32  # stage_operand's row padding
+                ldp = -(-dim // sl) * sl if dim % sl else dim
+                dropin_h2d = int(n * ldp * es)
+                dropin_staging = (f"float64 rows converted to {args.precision} by host threads into pinned "
+                                  f"{_ex.HOST_STAGE_BLOCK_BYTES >> 20} MB blocks, each block's H2D overlapping the "
+                                  "next block's conversion (inside the timed region)")
+            else:
+                dropin_h2d, dropin_staging = int(n * dim * 8), "float64 H2D, converted on the device"
             del x64
             e2e = {"value": 2.0 * nnz * dim / e2e_s / 1e9, "unit": "GFLOP/s",
                    "h2d_bytes_per_step": int(xh.numel() * xh.element_size()),
@@ -452,9 +470,10 @@ def run_ours(args):
                    "sync_api": "paper_2412_08902_b200.spmm_hybrid(windows, assignment, pinned host bf16 X) -> host fp32 Z",
                    "dropin": {"value": 2.0 * nnz * dim / dropin_s / 1e9, "unit": "GFLOP/s",
                               "ms_per_step": dropin_s * 1e3,
-                              "h2d_bytes_per_step": int(n * dim * 8), "d2h_bytes_per_step": out_bytes,
+                              "h2d_bytes_per_step": dropin_h2d, "d2h_bytes_per_step": out_bytes,
                               "api": ("paper_2412_08902_b200.spmm_hybrid(windows, assignment, DenseMatrix(float64 "
-                                      "numpy X, pageable)) -> numpy float32 Z: the rowwin caller's drop-in call")}}
+                                      "numpy X, pageable)) -> numpy float32 Z: the rowwin caller's drop-in call"),
+                              "staging": dropin_staging}}
         return ms, tile_ms, sampler.summary(), e2e
 
     dim = args.dim
@@ -512,7 +531,7 @@ def run_ours(args):
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "traffic_source": ("committed constant: dram__bytes_read.sum + dram__bytes_write.sum of one "
                                         "k_tile_warp launch from an ncu --set full capture of this config "
-                                        "(profiles/ncu_traffic.json); DRAM counters cannot be read inside "
+                                        "(profiles/ncu_traffic.json <- profiles/r02_ncu_full_tile_c2_d128.txt); DRAM counters cannot be read inside "
                                         "an un-profiled run") if traffic is not None else None,
                      "kernel": ("whole step (CUDA graph: k_tile_warp + K3)" if use_graph else
                                 "k_tile_warp") if plan.n_tile else "k_spmm_scalar_w",
@@ -599,6 +618,36 @@ def cpu_baseline(a, dim, budget):
 
 
 # ----------------------------------------------------------------------------- C3: 2-layer GCN epoch
+def profile_range(start: bool) -> None:
+    """HCS_PROFILE_TIMED=1: cudaProfilerStart/Stop around the timed region, so
+    `ncu --profile-from-start off` lists exactly the timed kernels."""
+    if os.environ.get("HCS_PROFILE_TIMED") == "1":
+        (torch.cuda.cudart().cudaProfilerStart if start else torch.cuda.cudart().cudaProfilerStop)()
+
+
+def epoch_kernels(fn) -> dict | None:
+    """The kernels one more step launches (CUPTI via torch.profiler, outside the timed region):
+    launch count, our own (hcs::) launches, and any library GEMM (cuBLAS / CUTLASS) by name."""
+    try:
+        from torch.profiler import ProfilerActivity, profile
+
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            fn()
+            torch.cuda.synchronize()
+        names = [e.name for e in prof.events() if e.device_type.name == "CUDA" and "memcpy" not in e.name.lower()
+                 and "memset" not in e.name.lower()]
+    except Exception as exc:  # CUPTI unavailable: say so instead of guessing
+        return {"error": f"{type(exc).__name__}: {exc}"[:200]}
+    gemm = sorted({n[:80] for n in names if any(k in n.lower() for k in ("gemm", "cublas", "cutlass", "xmma"))})
+    own = [n for n in names if "hcs::" in n]
+    short = {}
+    for n in names:
+        k = n.split("(")[0][:60]
+        short[k] = short.get(k, 0) + 1
+    return {"launches": len(names), "hcs_launches": len(own), "library_gemm": gemm, "by_kernel": short}
+
+
 def run_c3(args):
     """BASELINE configs[2]: 2-layer GCN (128 -> 64 -> 41) training on the Reddit-shaped graph
     with the fused SpMM+GEMM kernels, forward + backward + SGD per step."""
@@ -632,12 +681,15 @@ def run_c3(args):
     sampler = ClockSampler(local)
     with sampler:
         s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        profile_range(True)
         s_ev.record()
         for _ in range(steps):
             loss = model.epoch(x, labels, ws, shard=shard)
         e_ev.record()
         torch.cuda.synchronize()
+        profile_range(False)
     ms = s_ev.elapsed_time(e_ev) / steps
+    kernels = epoch_kernels(lambda: model.epoch(x, labels, ws, shard=shard)) if rank == 0 else None
     if world > 1:
         t = torch.tensor([ms], device=dev if dist.get_backend() == "nccl" else "cpu", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -653,7 +705,8 @@ def run_c3(args):
                       "n": n, "nnz": nnz, "parallelism": f"row-window shards x{world}" if world > 1 else "single GPU",
                       "loss_last": float(loss.detach())},
            "spmm_gflops": spmm_flops / (ms * 1e-3) / 1e9, "gemm_gflop_per_epoch": gemm_flops / 1e9,
-           "gpu_launches": None, "clocks": sampler.summary()}
+           "gpu_launches": (kernels["launches"] * steps) if kernels else None,
+           "kernels_per_epoch": kernels, "clocks": sampler.summary()}
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:

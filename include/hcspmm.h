@@ -75,6 +75,13 @@ int hcs_tile_plan_workspace_bytes(int64_t nnz_tile, int64_t nchunks, size_t* byt
 int hcs_io_count(const char* path, int64_t offset, int kind, int nthreads, int64_t* count, int* irregular);
 int hcs_io_parse(const char* path, int64_t offset, int kind, int expected, int64_t count, int nthreads, int64_t* a,
                  int64_t* b, double* v, int* irregular);
+/* matrices.py:126-149 DenseMatrix (float64, row-major) staged for the device: rows [0, rows) of a
+ * host float64 matrix converted by `threads` host threads (<= 0: all) into host memory `dst`
+ * (typically pinned) as bf16 (out_dtype HCS_DTYPE_BF16; torch's double -> float -> bfloat16
+ * rounding, bit for bit) or fp32 (HCS_DTYPE_F32), leading dimension ld_dst >= dim, padding
+ * columns zeroed.  The drop-in spmm_hybrid(DenseMatrix) call pipelines it with the H2D copy. */
+int hcs_host_convert_f64(const double* src, int64_t rows, int64_t dim, int64_t ld_src, void* dst, int64_t ld_dst,
+                         int out_dtype, int threads);
 
 /* plan builder: 0 (default) = per-window stable bucketing by chunk, 1 = global radix sort on
  * (chunk, row, column); both produce identical plans */

@@ -62,6 +62,7 @@ _SIGS = {
     "hcs_loa": (ctypes.c_int, [P, P, I64, I32, I32, P, P, P, P, P, SZ, P]),
     "hcs_convert": (ctypes.c_int, [P, P, I64, ctypes.c_int, P]),
     "hcs_normalize_values": (ctypes.c_int, [ctypes.c_int, P, P, P, I64, P, P, P, P]),
+    "hcs_host_convert_f64": (ctypes.c_int, [P, I64, I64, I64, P, I64, ctypes.c_int, ctypes.c_int]),
     "hcs_io_count": (ctypes.c_int, [ctypes.c_char_p, I64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(I64),
                                     ctypes.POINTER(ctypes.c_int)]),
     "hcs_io_parse": (ctypes.c_int, [ctypes.c_char_p, I64, ctypes.c_int, ctypes.c_int, I64, ctypes.c_int, P, P, P,

@@ -524,6 +524,7 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
 #pragma unroll
       for (int q = 0; q < 4; ++q) sts128_zero(slab + (lane + 32 * q) * 16);
     }
+    __syncwarp();  // the next chunk's scatter may hit a slot another lane clears here (racecheck)
     // end of our part of the unit: Z (whole unit) or a scratch slot (split unit; the last of
     // its warps to arrive sums the slots in range order, below)
     const bool unit_done = P0.j + 1 == P0.nj;

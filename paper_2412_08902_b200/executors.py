@@ -174,6 +174,12 @@ def stage_operand(x, precision: str, device, tf32_round: bool = False) -> tuple[
         # 128 B for fp32) so every gathered row slice starts on a cache-line boundary (C3's
         # 41-wide gradient: 96-B rows straddle lines; the fused backward took 1.52 ms)
         ld = _round_up(dim, slice_elems)
+    if (was_host and t.dtype == torch.float64 and rows * dim >= HOST_STAGE_MIN_ELEMS and dim
+            and t.stride(1) == 1):
+        # the drop-in operand (a reference DenseMatrix: float64, pageable): converted on the host
+        # cores straight into pinned blocks of the compute dtype, each block's H2D copy overlapping
+        # the conversion of the next (csrc/host_stage.cu)
+        return DeviceOperand(_stage_host_f64(t, rows, dim, ld, want, device, tf32_round), dim, ld, code), was_host
     if was_host and t.dtype == want and ld == dim and t.is_contiguous() and not tf32_round:
         # host operand already in the compute dtype: one (async when pinned) H2D copy
         buf = torch.empty((rows, ld), dtype=want, device=device)
@@ -194,6 +200,64 @@ def stage_operand(x, precision: str, device, tf32_round: bool = False) -> tuple[
         else:
             buf[:, :dim] = src.to(want)
     return DeviceOperand(buf, dim, ld, code), was_host
+
+
+HOST_STAGE_MIN_ELEMS = 1 << 20   # float64 host operands from 8 MB take the pipelined staging path
+HOST_STAGE_BLOCK_BYTES = 8 << 20  # bytes (compute dtype) per staged block
+_STAGE_RINGS: dict = {}
+
+
+class _StageRing:
+    """Two pinned staging blocks per device, reused across calls; `busy[i]` is the event of the
+    last H2D copy out of block i (it must complete before the block is rewritten)."""
+
+    def __init__(self, nbytes: int):
+        self.blocks = [torch.empty(nbytes, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        self.busy = [None, None]
+
+
+def _stage_host_f64(t: torch.Tensor, rows: int, dim: int, ld: int, want, device, tf32_round: bool) -> torch.Tensor:
+    import os
+
+    elem = 2 if want == torch.bfloat16 else 4
+    out_code = _lib.DTYPE_BF16 if want == torch.bfloat16 else _lib.DTYPE_F32
+    block_rows = max(1, HOST_STAGE_BLOCK_BYTES // (ld * elem))
+    nbytes = block_rows * ld * elem
+    ring = _STAGE_RINGS.get(device)
+    if ring is None or ring.blocks[0].numel() < nbytes:
+        if ring is not None:
+            for ev in ring.busy:
+                if ev is not None:
+                    ev.synchronize()
+        ring = _STAGE_RINGS[device] = _StageRing(nbytes)
+    h2d = _H2D_STREAMS.get(device)
+    if h2d is None:
+        h2d = _H2D_STREAMS[device] = torch.cuda.Stream(device=device)
+    cur = torch.cuda.current_stream(device)
+    buf = torch.empty((rows, ld), dtype=want, device=device)
+    h2d.wait_stream(cur)  # buf's memory may still be in use by earlier work on this stream
+    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    src = t.data_ptr()
+    ld_src = t.stride(0)
+    for i, r0 in enumerate(range(0, rows, block_rows)):
+        r1 = min(rows, r0 + block_rows)
+        slot = i & 1
+        if ring.busy[slot] is not None:
+            ring.busy[slot].synchronize()
+        blk = ring.blocks[slot][: (r1 - r0) * ld * elem].view(want).view(r1 - r0, ld)
+        _lib.call("hcs_host_convert_f64", src + r0 * ld_src * 8, r1 - r0, dim, ld_src, blk.data_ptr(), ld, out_code,
+                  threads)
+        with torch.cuda.stream(h2d):
+            buf[r0:r1].copy_(blk, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(h2d)
+        ring.busy[slot] = ev
+    cur.wait_stream(h2d)
+    if tf32_round:  # tf32 tensor-core inputs: RNA-rounded on the device
+        rnd = torch.empty_like(buf)
+        _lib.call("hcs_convert", buf.data_ptr(), rnd.data_ptr(), buf.numel(), 0, _lib.stream())
+        return rnd
+    return buf
 
 
 # --------------------------------------------------------------------------- hybrid plan

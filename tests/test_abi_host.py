@@ -127,3 +127,35 @@ def test_sparse_csr_validate_and_from_coo():
     bad = hc.SparseCsr(2, 3, np.array([0, 2, 2]), np.array([2, 1]), np.ones(2))
     with pytest.raises(ValueError, match="strictly ascending"):
         bad.validate()
+
+
+def test_host_convert_f64_matches_torch_casts():
+    """hcs_host_convert_f64 (the drop-in DenseMatrix staging, csrc/host_stage.cu) == torch's
+    double -> bfloat16 cast bit for bit (infinities, overflow, subnormals, RNE ties, signed
+    zeros; NaN stays NaN), == astype(float32) for fp32, and zeroes the padding columns; any
+    thread count gives the same bytes."""
+    import numpy as np
+    import torch
+
+    from paper_2412_08902_b200 import _lib
+
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal((777, 77)) * np.exp(rng.uniform(-60, 60, (777, 77)))
+    a[0, :6] = [np.nan, np.inf, -np.inf, 0.0, -0.0, 1e39]
+    a[1, :4] = [1e-40, -1e-42, 3.4e38, -1e300]
+    a[2, :3] = [1 + 2 ** -8, 1 + 3 * 2 ** -8, -(1 + 2 ** -8)]  # exact bf16 ties
+    ref = torch.from_numpy(a).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    for ld, threads in ((77, 1), (80, 3), (96, 0)):
+        out = np.full((777, ld), 0xAAAA, dtype=np.uint16)
+        _lib.call("hcs_host_convert_f64", a.ctypes.data, 777, 77, 77, out.ctypes.data, ld, _lib.DTYPE_BF16, threads)
+        nan = np.isnan(a)
+        assert np.array_equal(out[:, :77][~nan], ref[~nan])
+        assert ((out[:, :77][nan] & 0x7F80) == 0x7F80).all() and (out[:, :77][nan] & 0x7F).all()
+        assert (out[:, 77:] == 0).all()
+        o32 = np.full((777, ld), 7.0, dtype=np.float32)
+        _lib.call("hcs_host_convert_f64", a.ctypes.data, 777, 77, 77, o32.ctypes.data, ld, _lib.DTYPE_F32, threads)
+        with np.errstate(over="ignore"):
+            assert np.array_equal(o32[:, :77], a.astype(np.float32), equal_nan=True)
+        assert (o32[:, 77:] == 0).all()
+    with pytest.raises(ValueError, match="leading dimensions"):
+        _lib.call("hcs_host_convert_f64", a.ctypes.data, 777, 77, 70, out.ctypes.data, 96, _lib.DTYPE_BF16, 1)

@@ -236,3 +236,39 @@ def test_loa_full_reddit_community_invariants(cuda_ok):
     assert g2.adjacency.nnz == adj.nnz
     ci = lambda a: float(a.nnz) / float(hc.partition(a).ncols().sum())  # noqa: E731
     assert ci(g2.adjacency) > 1.2 * ci(adj)
+
+
+@pytest.mark.parametrize("precision", ["bf16", "tf32"])
+def test_c1_bench_graph_full_parity(cuda_ok, precision):
+    """The C1 bench graph itself (graphgen.cora_shaped, the product's on-device generator that
+    bench.py times): every window, condensation, fp64 density bits and selector code == the
+    oracle; the hybrid SpMM of the whole graph == the oracle's f32 hybrid executor (reference
+    executors.py:160-188) within the precision's tolerance at dims 32 and 128; the CUDA-graph
+    replay bench.py times (SpmmGraph, K3 forked beside K4) == spmm_hybrid bit for bit."""
+    from paper_2412_08902_b200.executors import SpmmGraph
+
+    torch.cuda.set_device(0)
+    adj = graphgen.cora_shaped(seed=0)
+    adj.symmetric = True
+    a = normalize_adj(adj, "gcn")
+    ws = hc.partition(a)
+    rp = a.row_ptr.cpu().numpy()
+    wcp = ws.win_col_ptr.cpu().numpy()
+    _check_window_range("c1", a, ws, 0, len(ws), rp, wcp, ws.density.cpu().numpy(), ws.codes.cpu().numpy())
+    ref_ws = orc.partition(orc.Csr(a.num_rows, a.num_cols, rp, a.col_idx.cpu().numpy().astype(np.int64),
+                                   _host_values(a)))
+    asg = hc.classify_windows(hc.default_model(), ws)
+    for dim in (32, 128):
+        x = orc.random_dense(a.num_rows, dim, seed=1)
+        z = hc.spmm_hybrid(ws, asg, hc.DenseMatrix(x), precision=precision).z.data
+        want = orc.spmm_hybrid(ref_ws, asg.codes, x, precision="f32")
+        err = orc.max_rel_err(np.asarray(z), want)
+        _record("c1_bench_graph_spmm_vs_reference_f32", dim=dim, precision=precision, max_rel_err=err,
+                tol=TOL[precision])
+        assert err <= TOL[precision], (dim, precision, err)
+        xd = torch.from_numpy(x).to(torch.bfloat16 if precision == "bf16" else torch.float32).cuda()
+        g = SpmmGraph(ws, asg, xd, precision=precision)
+        zg = g.replay().clone()
+        torch.cuda.synchronize()
+        zd = hc.spmm_hybrid(ws, asg, xd, precision=precision).z.data
+        assert torch.equal(zg, zd)

@@ -251,6 +251,22 @@ def test_host_pipelined_path(cuda_ok):
     assert np.abs(host.z.data - d).max() <= 1e-5 * np.abs(d).max()
     assert orc.max_rel_err(host.z.data, orc.spmm_exact(a, x)) <= BF16_TOL
     assert host.stats == dev.stats
+    # the float64 operand (4.5 M elements) took the pipelined host staging path (host threads
+    # convert blocks into pinned bf16 while the previous block uploads): the staged operand is
+    # torch's own cast bit for bit, for bf16 and for the tf32 path's fp32 + RNA rounding
+    assert x.size >= ex.HOST_STAGE_MIN_ELEMS
+    for prec, want in (("bf16", torch.bfloat16), ("tf32", torch.float32)):
+        op, was_host = ex.stage_operand(hc.DenseMatrix(x), prec, xt.device, tf32_round=prec == "tf32")
+        assert was_host
+        ref = torch.from_numpy(x).to(want).cuda()
+        if prec == "tf32":
+            rnd = torch.empty_like(ref)
+            from paper_2412_08902_b200 import _lib
+
+            _lib.call("hcs_convert", ref.data_ptr(), rnd.data_ptr(), ref.numel(), 0, _lib.stream())
+            ref = rnd
+        assert torch.equal(op.t[:, : x.shape[1]], ref)
+        assert not op.t[:, x.shape[1]:].any()
 
 
 @pytest.mark.parametrize("big", [False, True])
