@@ -10,8 +10,11 @@
 // conversion of the same array produces (tests/test_abi_host.py; NaN payloads aside).
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
 #include <cstdint>
 #include <cstring>
+#include <functional>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -50,6 +53,75 @@ void convert_rows(const double* src, int64_t ld_src, int64_t r0, int64_t r1, int
   }
 }
 
+// Persistent worker threads: a staged operand is converted in several blocks per call, and
+// starting threads per block cost more than the conversion of a small block (16 threads x 8 blocks
+// of a C2 operand: ~2 ms of thread start-up, tools/exp_dropin.py).  run(n, fn) calls fn(0..n-1),
+// fn(0) on the caller; calls are serialised.
+class Pool {
+ public:
+  void run(int n, const std::function<void(int)>& fn) {
+    std::lock_guard<std::mutex> serial(call_mu_);
+    {
+      std::unique_lock<std::mutex> lk(mu_);
+      while ((int)workers_.size() < n - 1) {
+        const int id = (int)workers_.size() + 1;
+        workers_.emplace_back([this, id] { loop(id); });
+      }
+      job_ = &fn;
+      active_ = n;
+      pending_ = n - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    fn(0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [this] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+
+ private:
+  void loop(int id) {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int)>* job;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (stop_) return;
+        if (id >= active_) continue;
+        job = job_;
+      }
+      (*job)(id);
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (--pending_ == 0) done_.notify_one();
+      }
+    }
+  }
+  std::mutex call_mu_, mu_;
+  std::condition_variable cv_, done_;
+  std::vector<std::thread> workers_;
+  const std::function<void(int)>* job_ = nullptr;
+  uint64_t gen_ = 0;
+  int active_ = 0, pending_ = 0;
+  bool stop_ = false;
+};
+
+Pool& pool() {
+  static Pool* p = new Pool();  // never destroyed: workers may outlive static destruction order
+  return *p;
+}
+
 }  // namespace
 
 // Converts rows [0, rows) of a row-major float64 host matrix (leading dimension ld_src) into dst
@@ -71,13 +143,8 @@ extern "C" int hcs_host_convert_f64(const double* src, int64_t rows, int64_t dim
     convert_rows(src, ld_src, 0, rows, dim, dst, ld_dst, out_dtype);
     return HCS_OK;
   }
-  std::vector<std::thread> pool;
-  pool.reserve(nt - 1);
-  for (int t = 1; t < nt; ++t) {
-    const int64_t r0 = rows * t / nt, r1 = rows * (t + 1) / nt;
-    pool.emplace_back(convert_rows, src, ld_src, r0, r1, dim, dst, ld_dst, out_dtype);
-  }
-  convert_rows(src, ld_src, 0, rows / nt, dim, dst, ld_dst, out_dtype);
-  for (auto& th : pool) th.join();
+  pool().run(nt, [&](int t) {
+    convert_rows(src, ld_src, rows * t / nt, rows * (t + 1) / nt, dim, dst, ld_dst, out_dtype);
+  });
   return HCS_OK;
 }

@@ -203,7 +203,8 @@ def stage_operand(x, precision: str, device, tf32_round: bool = False) -> tuple[
 
 
 HOST_STAGE_MIN_ELEMS = 1 << 20   # float64 host operands from 8 MB take the pipelined staging path
-HOST_STAGE_BLOCK_BYTES = 8 << 20  # bytes (compute dtype) per staged block
+HOST_STAGE_BLOCK_BYTES = 16 << 20  # bytes (compute dtype) per staged block
+HOST_STAGE_THREADS = None         # None: every CPU this process may run on
 _STAGE_RINGS: dict = {}
 
 
@@ -236,7 +237,8 @@ def _stage_host_f64(t: torch.Tensor, rows: int, dim: int, ld: int, want, device,
     cur = torch.cuda.current_stream(device)
     buf = torch.empty((rows, ld), dtype=want, device=device)
     h2d.wait_stream(cur)  # buf's memory may still be in use by earlier work on this stream
-    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    threads = HOST_STAGE_THREADS or (len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity")
+                                     else (os.cpu_count() or 1))
     src = t.data_ptr()
     ld_src = t.stride(0)
     for i, r0 in enumerate(range(0, rows, block_rows)):
