@@ -282,20 +282,21 @@ __device__ __forceinline__ void finish_split_z(const int64_t* __restrict__ chunk
   store_slice<SWV>(z, ldz, rs, rows, dim, f + fw, acc, lane);
 }
 
-// the same for a window's fused out rows (non-paired sequence; window = positions
-// [FS (base - c0), + FS nj); its counters follow the z counters)
+// the same for a window's fused out rows (window = positions [FSr (base - c0), + FSr nj) of the
+// group sequence; one out partial per group, slot 2g + s; counters follow the z counters)
 __device__ __forceinline__ void finish_split_out(const int64_t* __restrict__ chunk_ptr, int64_t T, int FS,
-                                                 int warps_per_cta, unsigned* __restrict__ cnt,
+                                                 int paired, int warps_per_cta, unsigned* __restrict__ cnt,
                                                  const float* __restrict__ oslots, float* __restrict__ out,
                                                  int64_t ldo, int64_t base, int nj, int64_t rs, int rows, int d_out) {
   const int lane = threadIdx.x & 31;
+  const int FSr = paired ? 1 : FS, FSm = paired ? FS : 1;
   const int64_t gw = (int64_t)blockIdx.x * warps_per_cta + (threadIdx.x >> 5);
-  const int64_t ng = (int64_t)gridDim.x * warps_per_cta;
+  const int64_t ng = (int64_t)gridDim.x * warps_per_cta / FSm;
   const int64_t c0 = __ldg(chunk_ptr);
-  const int64_t total = (int64_t)FS * (__ldg(chunk_ptr + T) - c0);
+  const int64_t total = (int64_t)FSr * (__ldg(chunk_ptr + T) - c0);
   int64_t a, b;
-  warp_range(total, ng, gw, a, b);
-  const int64_t ws = (int64_t)FS * (base - c0), we = ws + (int64_t)FS * nj;
+  warp_range(total, ng, gw / FSm, a, b);
+  const int64_t ws = (int64_t)FSr * (base - c0), we = ws + (int64_t)FSr * nj;
   const int64_t g_o = range_owner(total, ng, ws);
   if (!split_arrive(cnt + tile_cnt_words_dev() + g_o, ws, we, a, b, lane)) return;
   float oacc[kFusedOutMax / 8][4];
@@ -524,7 +525,9 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
 #pragma unroll
       for (int q = 0; q < 4; ++q) sts128_zero(slab + (lane + 32 * q) * 16);
     }
+#ifndef HCS_EXP_NO_UNDO_SYNC
     __syncwarp();  // the next chunk's scatter may hit a slot another lane clears here (racecheck)
+#endif
     // end of our part of the unit: Z (whole unit) or a scratch slot (split unit; the last of
     // its warps to arrive sums the slots in range order, below)
     const bool unit_done = P0.j + 1 == P0.nj;
@@ -552,7 +555,7 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
           af[1] = pack_bf16(acc[2 * j][2], acc[2 * j][3]);
           af[2] = pack_bf16(acc[2 * j + 1][0], acc[2 * j + 1][1]);
           af[3] = pack_bf16(acc[2 * j + 1][2], acc[2 * j + 1][3]);
-          const int kb = P0.f * C::kFeat + 16 * j;
+          const int kb = (P0.f + fw) * C::kFeat + 16 * j;
 #pragma unroll
           for (int n8 = 0; n8 < kFusedOutMax / 8; ++n8) {
             if (n8 * 8 < d_out) {
@@ -561,15 +564,39 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
             }
           }
         }
-        const bool win_head = (int64_t)FS * (P0.base - c0) < a;  // window began in an earlier warp's range
-        const bool win_done = unit_done && P0.f == FS - 1;
+        const bool win_head = (int64_t)FSr * (P0.base - c0) < a;  // window began in an earlier range
+        const bool win_done = unit_done && P0.f == FSr - 1;
         if (win_done || P0.rem == 1) {
-          if (win_done && !win_head) {
-            store_out(out, ldo, rs, rows, d_out, oacc, lane);
-          } else {
-            write_slot(oscratch + (gw * 2 + (win_head ? 0 : 1)) * kOutSlot, oacc, lane);
-            finish_split_out(chunk_ptr, T, FS, kWarpTileWarps, cnt, oscratch, out, ldo, P0.base, P0.nj, rs, rows,
-                             d_out);
+          if (paired) {
+            // the pair's slice partials: warp f = 1 hands its 16 x 64 out partial to warp f = 0
+            // through its own ring slot of the chunk just computed (free until the next step's
+            // issue), then out = partial(slice 0) + partial(slice 1)
+            const uint32_t xs = smem_u32(wsmem + (warp | 1) * kWarpSmemPerWarp) + s0 * kWarpStageBytes;
+            const int bar = 1 + (warp >> 1);
+            if (fw == 1) {
+#pragma unroll
+              for (int n8 = 0; n8 < kFusedOutMax / 8; ++n8)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) sts32f(xs + ((n8 * 4 + q) * 32 + lane) * 4, oacc[n8][q]);
+            }
+            named_bar_sync(bar, 64);
+            if (fw == 0) {
+#pragma unroll
+              for (int n8 = 0; n8 < kFusedOutMax / 8; ++n8)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) oacc[n8][q] += lds32f(xs + ((n8 * 4 + q) * 32 + lane) * 4);
+            }
+            named_bar_sync(bar, 64);
+          }
+          if (fw == 0) {
+            if (win_done && !win_head) {
+              store_out(out, ldo, rs, rows, d_out, oacc, lane);
+            } else {
+              const int64_t gi = paired ? gw / FS : gw;
+              write_slot(oscratch + (gi * 2 + (win_head ? 0 : 1)) * kOutSlot, oacc, lane);
+              finish_split_out(chunk_ptr, T, FS, paired, kWarpTileWarps, cnt, oscratch, out, ldo, P0.base, P0.nj,
+                               rs, rows, d_out);
+            }
           }
 #pragma unroll
           for (int i = 0; i < kFusedOutMax / 8; ++i) oacc[i][0] = oacc[i][1] = oacc[i][2] = oacc[i][3] = 0.f;
@@ -842,7 +869,7 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
             store_out(out, ldo, rs, rows, d_out, oacc, lane);
           } else {
             write_slot<NO>(oscratch + (gw * 2 + (win_head ? 0 : 1)) * kOutSlot, oacc, lane);
-            finish_split_out(chunk_ptr, T, FS, kTfWarps, cnt, oscratch, out, ldo, p0.base, p0.nj, rs, rows, d_out);
+            finish_split_out(chunk_ptr, T, FS, 0, kTfWarps, cnt, oscratch, out, ldo, p0.base, p0.nj, rs, rows, d_out);
           }
 #pragma unroll
           for (int i = 0; i < NO; ++i) oacc[i][0] = oacc[i][1] = oacc[i][2] = oacc[i][3] = 0.f;
@@ -923,7 +950,9 @@ static int launch_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* 
   float* oscratch = slots + nwarps * 2 * C::kSlot;
   const int smem = C::kSmem + (FUSED ? kFusedOutMax * kFusedLdw * 2 : 0);
   const bool want = g_warp_paired == 1 || (g_warp_paired == 2 && x_rows * ldx * 2 > kPairMinXBytes);
-  const int paired = (!FUSED && FS > 1 && want && C::kWarps % FS == 0) ? 1 : 0;
+  // the fused epilogue pairs 2 slices (out partials summed through shared memory, one named barrier
+  // pair per window end); the plain SpMM any FS dividing the CTA's warps
+  const int paired = (FS > 1 && want && C::kWarps % FS == 0 && (!FUSED || FS == 2)) ? 1 : 0;
   // one slice of 33..48 features: the fused (GCN) kernel skips the empty 16-feature group
   // (C3 5.92 -> 5.71 ms); the plain SpMM is faster with the full unrolled schedule now that
   // every lane copies whole padded rows (N = 40/41/48: 1.29 -> 1.21 ms; tools/exp_c3_npr3.sh)

@@ -384,7 +384,7 @@ class HybridPlan:
                 and len(self.windows) <= CONCURRENT_MAX_WINDOWS)
         if fork:
             cur = torch.cuda.current_stream(csr.device)
-            side = _side_stream(csr.device)
+            side = _side_stream(csr.device, cur)
             side.wait_stream(cur)
         if tile_events is not None:
             tile_events[0].record()
@@ -410,10 +410,13 @@ CONCURRENT_MAX_WINDOWS = 8192
 _SIDE_STREAMS: dict = {}
 
 
-def _side_stream(dev) -> torch.cuda.Stream:
-    st = _SIDE_STREAMS.get(dev)
+def _side_stream(dev, cur: torch.cuda.Stream) -> torch.cuda.Stream:
+    """One side stream per (device, caller stream): products issued from different streams or
+    threads (or one of them being captured into a CUDA graph) never share a side stream."""
+    key = (dev, cur.cuda_stream)
+    st = _SIDE_STREAMS.get(key)
     if st is None:
-        st = _SIDE_STREAMS[dev] = torch.cuda.Stream(device=dev)
+        st = _SIDE_STREAMS[key] = torch.cuda.Stream(device=dev)
     return st
 
 
