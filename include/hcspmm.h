@@ -107,6 +107,18 @@ int hcs_spmm_scalar(const int64_t* row_ptr, const int32_t* col_idx, const void* 
  * Window heights > 31 always use variant 1.  Every variant is deterministic. */
 int hcs_set_scalar_variant(int variant);
 
+/* K3 for small plans (executors.HybridPlan, <= 1,024 scalar windows): one warp per piece of <= 32
+ * entries of a row of the listed windows, so a hub row is spread over many warps.  Pieces of a row
+ * are consecutive: p_first = the row's first piece, p_count = its pieces, p_k = [k0, k1) entry
+ * range per piece (2 int64), p_row = output row.  A row of one piece is stored directly; the last
+ * piece of a longer row to finish sums the partials (slots: npieces x ld_slot floats) in piece
+ * order.  cnt: npieces uint32, zero before first use and left zero; one (slots, cnt) workspace
+ * must not be shared by concurrent launches. */
+int hcs_spmm_scalar_pieces(const int32_t* col_idx, const void* values, int values_dtype, const int32_t* p_row,
+                           const int64_t* p_k, const int32_t* p_first, const int32_t* p_count, int64_t npieces,
+                           const void* x, int x_dtype, int32_t dim, int64_t ldx, float* z, int64_t ldz, float* slots,
+                           int64_t ld_slot, unsigned* cnt, void* stream);
+
 /* ---------------------------------------------------------------- K4
  * executors.py:111-141 tile_window for every window of a tile plan, on warp-independent
  * workers: each warp owns a balanced range of (window, feature slice, 64-column chunk) work

@@ -43,6 +43,8 @@ _SIGS = {
                                      ctypes.c_int, I64, P, SZ, P]),
     "hcs_spmm_scalar": (ctypes.c_int, [P, P, P, ctypes.c_int, I64, I32, P, I64, P, ctypes.c_int, I64, I32, I64, P,
                                        I64, P]),
+    "hcs_spmm_scalar_pieces": (ctypes.c_int, [P, P, ctypes.c_int, P, P, P, P, I64, P, ctypes.c_int, I32, I64, P,
+                                              I64, P, I64, P, P]),
     "hcs_spmm_tile": (ctypes.c_int, [P, I64, P, P, P, P, ctypes.c_int, I64, I32, P, ctypes.c_int, I64, I32, I64, P,
                                      I64, P, SZ, P]),
     "hcs_tile_scratch_floats": (ctypes.c_int, [ctypes.POINTER(I64)]),

@@ -475,6 +475,128 @@ __global__ void __launch_bounds__(256, 1) k_spmm_scalar_rows(const int64_t* __re
   }
 }
 
+// K3, small plans with hub rows: the rows kernel above leaves a hub row's 32-entry batches on one
+// warp (C1: a degree-168 row is ~6 dependent gather rounds of the 10 us launch).  Here the plan
+// cuts every row into pieces of <= 32 entries (HybridPlan.scalar_pieces) and one warp takes one
+// piece: a row of one piece is stored directly; the pieces of a longer row write partials, add 1
+// to the row's completion counter, and the last one to arrive sums the partials in piece order
+// (deterministic), stores the row and resets the counter (the split_arrive scheme of K4).
+template <typename XT, typename VT, int VB>
+__global__ void __launch_bounds__(256, 1) k_spmm_scalar_pieces(const int32_t* __restrict__ col,
+                                                            const VT* __restrict__ val,
+                                                            const int32_t* __restrict__ p_row,
+                                                            const int64_t* __restrict__ p_k,
+                                                            const int32_t* __restrict__ p_first,
+                                                            const int32_t* __restrict__ p_count, int64_t npieces,
+                                                            const XT* __restrict__ x, int dim, int64_t ldx,
+                                                            float* __restrict__ z, int64_t ldz,
+                                                            float* __restrict__ slots, int64_t ld_slot,
+                                                            unsigned* __restrict__ cnt) {
+  constexpr int E = VB / (int)sizeof(XT);
+  const int lane = threadIdx.x & 31;
+  const int64_t pc = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (pc >= npieces) return;
+  const int64_t rs = __ldg(p_row + pc);
+  const int64_t kb = __ldg(p_k + 2 * pc), ke = __ldg(p_k + 2 * pc + 1);
+  const int first = __ldg(p_first + pc), count = __ldg(p_count + pc);
+  const uint64_t keep = policy_evict_last();
+  const uint64_t strm = stream_policy();
+  int c = 0;
+  float a = 0.f;
+  const int nb = (int)(ke - kb);  // <= 32
+  if (lane < nb) {
+    c = ld_stream_s32(col + kb + lane, strm);
+    a = load_val(val + kb + lane, strm);
+  }
+  const int nvec_total = (dim + E - 1) / E;
+  const int64_t ldxb = ldx * (int64_t)sizeof(XT);
+  for (int fs = 0; fs < nvec_total; fs += 32) {
+    const int L = min(32, nvec_total - fs);
+    const int G = 32 / L;
+    const int g = lane / L, v = lane - g * L;
+    const int f0 = (fs + v) * E;
+    const char* xb = reinterpret_cast<const char*>(x + f0);
+    float acc[E];
+#pragma unroll
+    for (int i = 0; i < E; ++i) acc[i] = 0.f;
+    for (int j0 = 0; j0 < nb; j0 += G * 8) {
+      XRaw<VB> xv[8];
+      float av[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = j0 + g + u * G;
+        const int cj = __shfl_sync(0xffffffffu, c, j & 31);
+        av[u] = __shfl_sync(0xffffffffu, a, j & 31);
+        xv[u].zero();
+        if (g < G && j < nb) {
+          xv[u].load(xb + (int64_t)cj * ldxb, keep);
+        } else {
+          av[u] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) fma_raw<XT, VB>(acc, xv[u].w, av[u]);
+    }
+    for (int sft = 1; sft < G; sft <<= 1) {
+#pragma unroll
+      for (int i = 0; i < E; ++i) {
+        const float o = __shfl_down_sync(0xffffffffu, acc[i], sft * L);
+        if ((g % (2 * sft)) == 0 && g + sft < G) acc[i] += o;
+      }
+    }
+    if (g == 0) {
+      float* dst = count == 1 ? z + rs * ldz + f0 : slots + pc * ld_slot + f0;
+      if (f0 + E <= dim) {
+#pragma unroll
+        for (int i = 0; i < E; i += 4) {
+          if (count == 1)
+            reinterpret_cast<float4*>(dst)[i / 4] = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+          else
+            __stcg(reinterpret_cast<float4*>(dst) + i / 4, make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]));
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < E; ++i)
+          if (f0 + i < dim) {
+            if (count == 1) dst[i] = acc[i]; else __stcg(dst + i, acc[i]);
+          }
+      }
+    }
+  }
+  if (count == 1) return;
+  // a row of several pieces: the last piece to finish sums the partials in piece order
+  __syncwarp();
+  int last = 0;
+  if (lane == 0) {
+    __threadfence();
+    const unsigned old = atomicAdd(cnt + first, 1u);
+    if (old + 1u == (unsigned)count) {
+      last = 1;
+      cnt[first] = 0u;
+    }
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return;
+  __threadfence();
+  for (int f = lane * 4; f < dim; f += 128) {
+    float4 sum = __ldcg(reinterpret_cast<const float4*>(slots + (int64_t)first * ld_slot + f));
+    for (int q = 1; q < count; ++q) {
+      const float4 t = __ldcg(reinterpret_cast<const float4*>(slots + (int64_t)(first + q) * ld_slot + f));
+      sum.x += t.x;
+      sum.y += t.y;
+      sum.z += t.z;
+      sum.w += t.w;
+    }
+    float* zr = z + rs * ldz + f;
+    if (f + 4 <= dim) {
+      *reinterpret_cast<float4*>(zr) = sum;
+    } else {
+      const float sv[4] = {sum.x, sum.y, sum.z, sum.w};
+      for (int i = 0; i < 4 && f + i < dim; ++i) zr[i] = sv[i];
+    }
+  }
+}
+
 template <typename XT, typename VT>
 static int launch_scalar_rows(const int64_t* row_ptr, const int32_t* col, const VT* val, int64_t n_rows, int wh,
                               const int32_t* win_list, int64_t n_list, const XT* x, int dim, int64_t ldx, float* z,
@@ -650,5 +772,50 @@ extern "C" int hcs_gcn_scalar(const int64_t* row_ptr, const int32_t* col_idx, co
     return set_error(HCS_EINVAL, "unsupported dtype combination x=%d values=%d", x_dtype, values_dtype);
   HCS_LAUNCH_CHECK("k_spmm_scalar<fused>");
   (void)x_rows;
+  return HCS_OK;
+}
+
+// K3 for small plans, hub rows split: one warp per piece of <= 32 entries of a row (see
+// k_spmm_scalar_pieces).  Pieces of one row are consecutive: p_first[i] = the row's first piece,
+// p_count[i] = its number of pieces; p_k = [k0, k1) entry ranges (2 int64 per piece).
+// slots: npieces x ld_slot floats (ld_slot >= dim, multiple of 4, 16-B aligned); cnt: npieces
+// uint32 completion counters, zero before the first launch (left zero).
+extern "C" int hcs_spmm_scalar_pieces(const int32_t* col_idx, const void* values, int values_dtype,
+                                      const int32_t* p_row, const int64_t* p_k, const int32_t* p_first,
+                                      const int32_t* p_count, int64_t npieces, const void* x, int x_dtype,
+                                      int32_t dim, int64_t ldx, float* z, int64_t ldz, float* slots, int64_t ld_slot,
+                                      unsigned* cnt, void* stream) {
+  HCS_REQUIRE(dim > 0 && npieces >= 0, HCS_EINVAL, "dim must be positive");
+  HCS_REQUIRE(ld_slot >= dim && ld_slot % 4 == 0 && ((uintptr_t)slots & 15) == 0, HCS_EINVAL,
+              "slots: ld_slot must cover dim, be a multiple of 4 and 16-byte aligned");
+  HCS_REQUIRE(((uintptr_t)x & 15) == 0 && ((uintptr_t)z & 15) == 0 && ldz % 4 == 0 && ldz >= dim, HCS_EINVAL,
+              "x/z must be 16-byte aligned, ldz a multiple of 4 covering dim");
+  if (npieces == 0) return HCS_OK;
+  cudaStream_t st = as_stream(stream);
+  const unsigned grid = (unsigned)((npieces + 7) / 8);
+  const bool v32 = ((uintptr_t)x & 31) == 0 && (ldx * (x_dtype == HCS_DTYPE_BF16 ? 2 : 4)) % 32 == 0 &&
+                   ldx >= ((dim + (x_dtype == HCS_DTYPE_BF16 ? 15 : 7)) / (x_dtype == HCS_DTYPE_BF16 ? 16 : 8)) *
+                              (x_dtype == HCS_DTYPE_BF16 ? 16 : 8);
+#define HCS_PIECES(XT, VT)                                                                                        \
+  do {                                                                                                          \
+    if (v32)                                                                                                    \
+      k_spmm_scalar_pieces<XT, VT, 32><<<grid, 256, 0, st>>>(col_idx, (const VT*)values, p_row, p_k, p_first,  \
+                                                             p_count, npieces, (const XT*)x, dim, ldx, z, ldz,  \
+                                                             slots, ld_slot, cnt);                              \
+    else                                                                                                        \
+      k_spmm_scalar_pieces<XT, VT, 16><<<grid, 256, 0, st>>>(col_idx, (const VT*)values, p_row, p_k, p_first,  \
+                                                             p_count, npieces, (const XT*)x, dim, ldx, z, ldz,  \
+                                                             slots, ld_slot, cnt);                              \
+  } while (0)
+  if (x_dtype == HCS_DTYPE_BF16 && values_dtype == HCS_DTYPE_BF16)
+    HCS_PIECES(__nv_bfloat16, __nv_bfloat16);
+  else if (x_dtype == HCS_DTYPE_BF16 && values_dtype == HCS_DTYPE_F32)
+    HCS_PIECES(__nv_bfloat16, float);
+  else if (x_dtype == HCS_DTYPE_F32 && values_dtype == HCS_DTYPE_F32)
+    HCS_PIECES(float, float);
+  else
+    return set_error(HCS_EINVAL, "unsupported dtype combination x=%d values=%d", x_dtype, values_dtype);
+#undef HCS_PIECES
+  HCS_LAUNCH_CHECK("k_spmm_scalar_pieces");
   return HCS_OK;
 }

@@ -337,6 +337,17 @@ class HybridPlan:
             buf = bufs[key] = self.new_scratch()
         return buf
 
+    def scalar_pieces(self):
+        """Small plans: the SCALAR windows' rows cut into <= 32-entry pieces (build_scalar_pieces)."""
+        if "pieces" not in self._cache:
+            self._cache["pieces"] = build_scalar_pieces(self.windows.csr, self.scalar_list,
+                                                        self.windows.window_height)
+        return self._cache["pieces"]
+
+    def _run_scalar_pieces(self, xop, z, ldz, s0: int, s1: int, stream: int) -> None:
+        run_scalar_pieces(self.windows.csr, self.scalar_vals, self.scalar_vals_code, self.scalar_pieces(), self._cache,
+                          xop, z, ldz, s0, s1, stream)
+
     def launches_per_run(self, dim: int) -> int:
         """Kernels of one run(): the tile kernel (split windows finished in-kernel) plus the
         scalar kernel."""
@@ -382,9 +393,14 @@ class HybridPlan:
         # joined on the current stream, so a CUDA-graph capture gets two parallel branches)
         fork = (stream is None and tile_events is None and t1 > t0 and s1 > s0
                 and len(self.windows) <= CONCURRENT_MAX_WINDOWS)
+        pieces = s1 > s0 and int(self.scalar_list.numel()) <= SCALAR_PIECES_MAX_WINDOWS and _scalar_variant_auto()
         if fork:
             cur = torch.cuda.current_stream(csr.device)
             side = _side_stream(csr.device, cur)
+        ss = side.cuda_stream if fork else s
+        if pieces:  # first use allocates and zero-fills on the current stream: before the fork point
+            pieces_workspace(self._cache, self.scalar_pieces(), ss, xop.dim, csr.device)
+        if fork:
             side.wait_stream(cur)
         if tile_events is not None:
             tile_events[0].record()
@@ -398,15 +414,19 @@ class HybridPlan:
         if tile_events is not None:
             tile_events[1].record()
         if s1 > s0:
-            _lib.call("hcs_spmm_scalar", csr.row_ptr.data_ptr(), csr.col_idx.data_ptr(), self.scalar_vals.data_ptr(),
-                      self.scalar_vals_code, csr.num_rows, self.windows.window_height,
-                      self.scalar_list.data_ptr() + 4 * s0, s1 - s0, xop.t.data_ptr(), xop.dtype_code, xop.rows,
-                      xop.dim, xop.ld, z.data_ptr(), ldz, side.cuda_stream if fork else s)
+            if pieces:
+                self._run_scalar_pieces(xop, z, ldz, s0, s1, ss)
+            else:
+                _lib.call("hcs_spmm_scalar", csr.row_ptr.data_ptr(), csr.col_idx.data_ptr(),
+                          self.scalar_vals.data_ptr(), self.scalar_vals_code, csr.num_rows, self.windows.window_height,
+                          self.scalar_list.data_ptr() + 4 * s0, s1 - s0, xop.t.data_ptr(), xop.dtype_code,
+                          xop.rows, xop.dim, xop.ld, z.data_ptr(), ldz, ss)
         if fork:
             cur.wait_stream(side)
 
 
 CONCURRENT_MAX_WINDOWS = 8192
+SCALAR_PIECES_MAX_WINDOWS = 1024  # scalar lists up to this length run hcs_spmm_scalar_pieces
 _SIDE_STREAMS: dict = {}
 
 
@@ -418,6 +438,60 @@ def _side_stream(dev, cur: torch.cuda.Stream) -> torch.cuda.Stream:
     if st is None:
         st = _SIDE_STREAMS[key] = torch.cuda.Stream(device=dev)
     return st
+
+
+def build_scalar_pieces(csr, win_list: torch.Tensor, wh: int):
+    """Every row of the listed windows cut into pieces of <= 32 entries, in list order, for
+    hcs_spmm_scalar_pieces (one warp per piece; a hub row's pieces are summed in piece order by the
+    last to finish).  Returns (p_row i32, p_k i64 [P, 2], p_first i32, p_count i32, window -> first
+    piece as host int64 [len + 1])."""
+    dev = csr.device
+    sl = win_list.to(torch.int64)
+    rows = sl[:, None] * wh + torch.arange(wh, device=dev)[None, :]
+    valid = rows < csr.num_rows
+    nrow_w = valid.sum(1)
+    rows = rows[valid]
+    k0, k1 = csr.row_ptr[rows], csr.row_ptr[rows + 1]
+    npc = torch.clamp((k1 - k0 + 31) // 32, min=1)
+    first = torch.cumsum(npc, 0) - npc
+    r_of = torch.repeat_interleave(torch.arange(rows.numel(), device=dev), npc)
+    q = torch.arange(r_of.numel(), device=dev) - first[r_of]
+    pk0 = k0[r_of] + 32 * q
+    pk = torch.stack([pk0, torch.minimum(pk0 + 32, k1[r_of])], 1).contiguous()
+    row_first = torch.zeros(nrow_w.numel() + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(nrow_w, 0, out=row_first[1:])
+    pc_ptr = torch.zeros(rows.numel() + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(npc, 0, out=pc_ptr[1:])
+    return (rows[r_of].to(torch.int32), pk, first[r_of].to(torch.int32), npc[r_of].to(torch.int32),
+            pc_ptr[row_first].cpu().numpy())
+
+
+def pieces_workspace(cache: dict, pieces, stream: int, dim: int, device):
+    """The (slots, counters) workspace of hcs_spmm_scalar_pieces for launches on `stream`, cached
+    per (stream, row width).  A new one is allocated and its counters zero-filled on the CURRENT
+    torch stream: a caller launching on another stream must order that stream after this call
+    (HybridPlan.run creates it before its fork point); the kernel leaves the counters zero."""
+    ld_slot = _round_up(dim, 4)
+    wkey = ("pieces_ws", stream, ld_slot)
+    ws = cache.get(wkey)
+    if ws is None:
+        P = max(int(pieces[0].numel()), 1)
+        ws = cache[wkey] = (torch.empty((P, ld_slot), dtype=torch.float32, device=device),
+                            torch.zeros(P, dtype=torch.int32, device=device), ld_slot)
+    return ws
+
+
+def run_scalar_pieces(csr, vals, vals_code, pieces, cache: dict, xop, z, ldz, s0: int, s1: int, stream: int) -> None:
+    """Launch hcs_spmm_scalar_pieces for windows [s0, s1) of the piece list (see pieces_workspace)."""
+    p_row, p_k, p_first, p_count, win_piece = pieces
+    q0, q1 = int(win_piece[s0]), int(win_piece[s1])
+    if q1 <= q0:
+        return
+    slots, cnt, ld_slot = pieces_workspace(cache, pieces, stream, xop.dim, z.device)
+    _lib.call("hcs_spmm_scalar_pieces", csr.col_idx.data_ptr(), vals.data_ptr(), vals_code,
+              p_row.data_ptr() + 4 * q0, p_k.data_ptr() + 16 * q0, p_first.data_ptr() + 4 * q0,
+              p_count.data_ptr() + 4 * q0, q1 - q0, xop.t.data_ptr(), xop.dtype_code, xop.dim, xop.ld, z.data_ptr(),
+              ldz, slots.data_ptr(), ld_slot, cnt.data_ptr(), stream)
 
 
 def get_plan(windows, assignment: Assignment, precision: str) -> HybridPlan:
@@ -678,7 +752,10 @@ def spmm_scalar(csr, x, precision: str = "bf16", window_height: int = 16) -> Spm
     W = -(-d.num_rows // window_height)
     wl = torch.arange(W, dtype=torch.int32, device=dev)
     vals, vcode = (d.values_bf16(), _lib.DTYPE_BF16) if precision == "bf16" else (d.values, _lib.DTYPE_F32)
-    if W:
+    if W and W <= SCALAR_PIECES_MAX_WINDOWS and _scalar_variant_auto():  # the hybrid plan's small-list kernel
+        run_scalar_pieces(d, vals, vcode, build_scalar_pieces(d, wl, window_height), {}, xop, z, ldz, 0, W,
+                          _lib.stream())
+    elif W:
         _lib.call("hcs_spmm_scalar", d.row_ptr.data_ptr(), d.col_idx.data_ptr(), vals.data_ptr(), vcode, d.num_rows,
                   window_height, wl.data_ptr(), W, xop.t.data_ptr(), xop.dtype_code, xop.rows, xop.dim, xop.ld,
                   z.data_ptr(), ldz, _lib.stream())
@@ -698,14 +775,21 @@ def spmm_auto(csr, x, assignment_for, precision: str = "bf16", threads: int = 1)
 
 
 _SCALAR_VARIANTS = {"auto": 0, "block": 1, "warp16": 2, "rows": 3, "warp": 4}
+_SCALAR_VARIANT = ["auto"]
+
+
+def _scalar_variant_auto() -> bool:
+    return _SCALAR_VARIANT[0] == "auto"
 
 
 def set_scalar_variant(variant: str = "auto") -> None:
-    """Select the CUDA-core (K3) kernel: "auto" ("rows" for lists of <= 1,024 windows, else
-    "warp"), "warp" (warp per window, col/val staged in shared memory, 32-byte X vectors when the
+    """Select the CUDA-core (K3) kernel: "auto" (inside a hybrid plan: the piece kernel, one warp
+    per <= 32-entry piece of a row, for lists of <= 1,024 windows; through hcs_spmm_scalar
+    directly: "rows" for lists of <= 1,024 windows, else "warp"), "warp" (warp per window, col/val staged in shared memory, 32-byte X vectors when the
     operand allows), "rows" (warp per row, pairs broadcast by shuffles; small graphs), "block"
     (block per window, one warp per row with a fixed shuffle tree), "warp16" (warp per window,
     16-byte vectors)."""
     if variant not in _SCALAR_VARIANTS:
         raise ValueError(f"variant must be one of {sorted(_SCALAR_VARIANTS)}, got {variant!r}")
     _lib.call("hcs_set_scalar_variant", _SCALAR_VARIANTS[variant])
+    _SCALAR_VARIANT[0] = variant

@@ -292,12 +292,20 @@ def test_async_requests_match_sync(cuda_ok, big):
             return np.abs(gz - wz).max() <= 1e-5 * np.abs(wz).max()
         return np.array_equal(gz, wz)
 
+    rows_tile = np.repeat(asg.codes, ws.window_height)[:n] == 1
+
+    def diag(gz, wz):
+        bad = np.nonzero(np.abs(gz - wz).max(1))[0]
+        rl = np.diff(a.row_ptr)[bad]
+        return (f"{bad.size} rows differ ({int(rows_tile[bad].sum())} on tile windows), first {bad[:8].tolist()}, "
+                f"row lengths {rl[:8].tolist()}, max diff {float(np.abs(gz - wz).max())}")
+
     for x, g in zip(ins, got):
         want = hc.spmm_hybrid(ws, asg, x)
         assert type(g.z.data) is type(want.z.data)
         gz = g.z.data if isinstance(g.z.data, np.ndarray) else g.z.data.numpy()
         wz = want.z.data if isinstance(want.z.data, np.ndarray) else want.z.data.numpy()
-        assert same(gz, wz)
+        assert same(gz, wz), diag(gz, wz)
         assert g.stats == want.stats
     assert orc.max_rel_err(got[0].z.data, orc.spmm_exact(a, xs[0])) <= BF16_TOL
     # caller-owned pinned result buffers (a ring of two, three requests)
@@ -462,7 +470,11 @@ def test_spmm_graph_replay(cuda_ok, precision):
     assert torch.equal(z1, ref)
     if precision == "bf16":  # operand used in place: replay sees the new X
         x.mul_(2)
-        assert torch.equal(g.replay(), 2 * z1)
+        z2 = g.replay()
+        bad = torch.nonzero((z2 - 2 * z1).abs().amax(1)).flatten().cpu().numpy()
+        rows_tile = np.repeat(asg.codes, ws.window_height)[:a.num_rows] == 1
+        assert torch.equal(z2, 2 * z1), (f"{bad.size} rows differ ({int(rows_tile[bad].sum())} tile), first "
+                                         f"{bad[:8].tolist()}, row lengths {np.diff(a.row_ptr)[bad[:8]].tolist()}")
     with pytest.raises(ValueError, match="CUDA tensor"):
         hc.SpmmGraph(ws, asg, x.cpu())
 
