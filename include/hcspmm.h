@@ -141,17 +141,10 @@ int hcs_set_tile_npr3(int on);
  * 0 = one warp per contiguous range of (window, slice, chunk); 2 = 1 only when X exceeds 96 MB.
  * All deterministic. */
 int hcs_set_tile_pairing(int on);
-/* chunk_desc (optional, NULL = none): one 16-byte descriptor per chunk of the plan, indexed by the
- * plan-wide chunk number -- {int64 first entry, int32 tile_list index of the chunk's window (plan-
- * wide), int32 entries << 2 | (first chunk of its window) << 1 | (last chunk)} (executors.HybridPlan
- * .chunk_desc).  With descriptors, bf16 plans whose every work position is one chunk (paired
- * feature slices, or one slice) run the chunk-walking kernel; results are bitwise identical. */
 int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
                   const int64_t* ent_ptr, const void* ent, int ent_dtype, int64_t n_rows, int32_t wh, const void* x,
                   int x_dtype, int64_t x_rows, int32_t dim, int64_t ldx, float* z, int64_t ldz, void* workspace,
-                  size_t ws_bytes, const void* chunk_desc, void* stream);
-/* chunk-descriptor kernel on (1, default) / off (0): experiment switch */
-int hcs_set_tile_chunk_kernel(int on);
+                  size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------- K6 / K7
  * gnn.py:121-159 forward (fused mode) and gnn.py:162-205 backward (fused mode):
@@ -167,8 +160,7 @@ int hcs_set_tile_chunk_kernel(int on);
 int hcs_gcn_tile(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
                  const int64_t* ent_ptr, const void* ent, int ent_dtype, int64_t n_rows, int32_t wh, const void* x,
                  int x_dtype, int64_t x_rows, int32_t dim, int64_t ldx, float* z, int64_t ldz, const float* m,
-                 int32_t d_out, float* out, int64_t ldo, void* workspace, size_t ws_bytes, const void* chunk_desc,
-                 void* stream);
+                 int32_t d_out, float* out, int64_t ldo, void* workspace, size_t ws_bytes, void* stream);
 int hcs_gcn_scalar(const int64_t* row_ptr, const int32_t* col_idx, const void* values, int values_dtype,
                    int64_t n_rows, int32_t wh, const int32_t* win_list, int64_t n_list, const void* x, int x_dtype,
                    int64_t x_rows, int32_t dim, int64_t ldx, float* z, int64_t ldz, const float* m, int32_t d_out,

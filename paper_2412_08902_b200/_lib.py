@@ -46,8 +46,7 @@ _SIGS = {
     "hcs_spmm_scalar_pieces": (ctypes.c_int, [P, P, ctypes.c_int, P, P, P, P, I64, P, ctypes.c_int, I32, I64, P,
                                               I64, P, I64, P, P]),
     "hcs_spmm_tile": (ctypes.c_int, [P, I64, P, P, P, P, ctypes.c_int, I64, I32, P, ctypes.c_int, I64, I32, I64, P,
-                                     I64, P, SZ, P, P]),
-    "hcs_set_tile_chunk_kernel": (ctypes.c_int, [ctypes.c_int]),
+                                     I64, P, SZ, P]),
     "hcs_tile_scratch_floats": (ctypes.c_int, [ctypes.POINTER(I64)]),
     "hcs_set_tile_slice": (ctypes.c_int, [ctypes.c_int]),
     "hcs_set_tile_npr3": (ctypes.c_int, [ctypes.c_int]),
@@ -55,7 +54,7 @@ _SIGS = {
     "hcs_set_tile_pairing": (ctypes.c_int, [ctypes.c_int]),
     "hcs_set_tile_plan_builder": (ctypes.c_int, [ctypes.c_int]),
     "hcs_gcn_tile": (ctypes.c_int, [P, I64, P, P, P, P, ctypes.c_int, I64, I32, P, ctypes.c_int, I64, I32, I64, P,
-                                     I64, P, I32, P, I64, P, SZ, P, P]),
+                                     I64, P, I32, P, I64, P, SZ, P]),
     "hcs_gcn_scalar": (ctypes.c_int, [P, P, P, ctypes.c_int, I64, I32, P, I64, P, ctypes.c_int, I64, I32, I64, P,
                                        I64, P, I32, P, I64, P]),
     "hcs_grad_w_workspace_bytes": (ctypes.c_int, [I64, I32, I32, ctypes.POINTER(SZ)]),

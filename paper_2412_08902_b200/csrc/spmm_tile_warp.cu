@@ -420,18 +420,7 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
       const uint32_t vb = feat < ldx ? vb_full : 0u;
       const char* src = xb + (int64_t)feat * 2;
       const uint32_t dst = stage0 + slot * kWarpStageBytes;
-#if defined(HCS_EXP_GATHER_MODE) && HCS_EXP_GATHER_MODE == 1  // ablation: no X gathers at all
-      if (true) {
-      } else if (false) {
-#elif defined(HCS_EXP_GATHER_MODE) && HCS_EXP_GATHER_MODE == 2  // ablation: same LSU work, 256 rows of X
-      if (true) {
-#pragma unroll
-        for (int it = 0; it < NI; ++it)
-          cp_async16(dst + dofs[it], src + (uint64_t)((uint32_t)g[it] & 255u) * ldxb, vb, keep);
-      } else if (false) {
-#else
       if (p.j + 1 < p.nj) {  // full chunk: every slot holds a column
-#endif
 #pragma unroll
         for (int it = 0; it < NI; ++it) cp_async16(dst + dofs[it], src + (uint64_t)(uint32_t)g[it] * ldxb, vb, keep);
       } else {  // the window's last chunk: pad slots (-1) are zero-filled
@@ -508,7 +497,6 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
     }
     cp_async_wait<2>();  // P0's gathers landed (P1, P2 may still be in flight)
     __syncwarp();
-#ifndef HCS_EXP_NO_MMA  // ablation experiments only (tools/exp_libs): wrong results when defined
     {
       const uint32_t st = stage0 + s0 * kWarpStageBytes;
 #pragma unroll
@@ -521,17 +509,11 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
         for (int pr = 0; pr < NPR; ++pr) {
           uint32_t bb[4];
           ldsm_x4_trans(bb, st + C::off(k, 2 * pr + bfc));
-#ifndef HCS_EXP_NO_HMMA
           hmma_16816(acc[2 * pr], af, bb[0], bb[1]);
           hmma_16816(acc[2 * pr + 1], af, bb[2], bb[3]);
-#else
-          acc[2 * pr][0] += __uint_as_float(bb[0] ^ bb[1] ^ af[0]);
-          acc[2 * pr + 1][0] += __uint_as_float(bb[2] ^ bb[3] ^ af[1]);
-#endif
         }
       }
     }
-#endif
     __syncwarp();
     // clear the slab for the next chunk: undo this chunk's scatter (all entries in registers),
     // or zero it fully when the chunk overflowed the register-held entries
@@ -660,293 +642,6 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
     if (step(Q1, Q2, Q3, Q0, G1, G0, E1, E0, EPb, EPc, EPd)) break;
     if (step(Q2, Q3, Q0, Q1, G0, G1, E0, E1, EPc, EPd, EPa)) break;
     if (step(Q3, Q0, Q1, Q2, G1, G0, E1, E0, EPd, EPa, EPb)) break;
-  }
-  cp_async_wait<0>();
-}
-
-// ---------------------------------------------------------------- chunk-descriptor variant
-// The same per-warp pipeline, walked by CHUNK INDEX.  Ablation of k_tile_warp at C2 / N = 128
-// (tools/exp_libs builds, profiles/r02_tile_ablation.txt): with no X gathers and no MMAs the kernel
-// still took 1.44 of its 2.44 ms -- the per-chunk skeleton (position bookkeeping over (window, slice,
-// chunk) triples, entry-pointer pairs, chunk_ptr walks) issued by only 2 warps per scheduler is
-// the larger half.  When every position is one chunk (paired slices, or one slice: the default for
-// bf16), the plan provides one 16-byte descriptor per chunk (HybridPlan.chunk_desc):
-//     {int64 first entry, int32 tile-list index of the window, int32 ne << 2 | first << 1 | last}
-// so a step is: descriptor + 64 gather indices of chunk c+3, entries of c+1, gathers of c+2 --
-// chunk c, c+1, ... are consecutive integers and there is no position state to advance.
-__device__ __forceinline__ int4 ld_desc(const int4* p, uint64_t pol) {
-  int4 v;
-  asm volatile("ld.global.nc.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p), "l"(pol));
-  return v;
-}
-
-template <int SWV, bool FUSED, int NPR = SWV / 2>
-__global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
-    k_tile_chunk(const int32_t* __restrict__ tile_list, int64_t T, const int64_t* __restrict__ chunk_ptr,
-                 const int4* __restrict__ desc, const int32_t* __restrict__ gidx, const uint32_t* __restrict__ ent,
-                 int64_t n_rows, int wh, const __nv_bfloat16* __restrict__ x, int64_t ldx, int dim, int FS,
-                 float* __restrict__ z, int64_t ldz, float* __restrict__ scratch, const float* __restrict__ mw,
-                 int d_out, float* __restrict__ out, int64_t ldo, float* __restrict__ oscratch, int paired,
-                 unsigned* __restrict__ cnt) {
-  using C = WarpCfg<SWV>;
-  constexpr int kWarpTileWarps = C::kWarps, kWarpStageBytes = C::kStageBytes, kWarpSmemPerWarp = C::kPerWarp;
-  constexpr int NI = C::kIssue;
-  extern __shared__ uint8_t wsmem_raw[];
-  uint8_t* wsmem = (uint8_t*)(((uintptr_t)wsmem_raw + 127) & ~(uintptr_t)127);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t nwarps = (int64_t)gridDim.x * kWarpTileWarps;
-  const int64_t gw = (int64_t)blockIdx.x * kWarpTileWarps + warp;
-  const int64_t c0 = chunk_ptr[0];
-  const int fw = paired ? (int)(gw % FS) : 0;
-  const int64_t ngroups = paired ? nwarps / FS : nwarps;
-  const int64_t total = chunk_ptr[T] - c0;
-  int64_t a = 0, b = 0;
-  if (!paired || gw < ngroups * FS) warp_range(total, ngroups, paired ? gw / FS : gw, a, b);
-  if (FUSED) {
-    __nv_bfloat16* wt = reinterpret_cast<__nv_bfloat16*>(wsmem + C::kOffW);
-    for (int i = threadIdx.x; i < kFusedOutMax * kFusedLdw; i += blockDim.x) {
-      const int n = i / kFusedLdw, k = i - n * kFusedLdw;
-      wt[i] = __float2bfloat16_rn((n < d_out && k < dim) ? mw[(int64_t)k * d_out + n] : 0.f);
-    }
-    __syncthreads();
-  }
-  if (a >= b) return;
-  const int64_t cb = c0 + b;  // chunks [c0 + a, cb) are ours
-  const uint32_t stage0 = smem_u32(wsmem + warp * kWarpSmemPerWarp);
-  const uint32_t slab = stage0 + kWarpTileStages * kWarpStageBytes;
-  const uint64_t keep = policy_evict_last();
-  const uint64_t once = policy_evict_first();
-  const int gv = lane % SWV, rg = lane / SWV;
-  uint32_t dofs[NI];
-#pragma unroll
-  for (int it = 0; it < NI; ++it) dofs[it] = C::off(rg * NI + it, gv);
-  const int featv = gv * 8;
-  const char* xb = reinterpret_cast<const char*>(x);
-  const uint32_t ldxb = (uint32_t)(ldx * 2);
-  const int ar = lane & 15, akc = lane >> 4;
-  const int bk = (lane & 7) + ((lane >> 3) & 1) * 8, bfc = lane >> 4;
-  // descriptors carry the window's plan-wide tile index; this launch's views start at window t_base
-  const int t_base = __ldg(&desc[c0].z);
-
-  auto load_desc = [&](int64_t c) -> int4 { return c < cb ? ld_desc(desc + c, once) : make_int4(0, 0, 0, 0); };
-  auto load_gidx = [&](int64_t c, int (&g)[NI]) {
-    if (c < cb) {
-      const int4* gp = reinterpret_cast<const int4*>(gidx + c * 64 + rg * NI);
-#pragma unroll
-      for (int q = 0; q < NI / 4; ++q) {
-        int4 v;
-        asm volatile("ld.global.nc.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
-                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                     : "l"(gp + q), "l"(once));
-        g[4 * q] = v.x;
-        g[4 * q + 1] = v.y;
-        g[4 * q + 2] = v.z;
-        g[4 * q + 3] = v.w;
-      }
-    }
-  };
-  auto issue = [&](int64_t c, const int4& d, const int (&g)[NI], int slot) {
-    if (c < cb && (NPR == SWV / 2 || gv < 2 * NPR)) {
-      const int feat = fw * C::kFeat + featv;
-      const uint32_t vb = feat < ldx ? 16u : 0u;
-      const char* src = xb + (int64_t)feat * 2;
-      const uint32_t dst = stage0 + slot * kWarpStageBytes;
-      if (!(d.w & 1)) {  // not the window's last chunk: every slot holds a column
-#pragma unroll
-        for (int it = 0; it < NI; ++it) cp_async16(dst + dofs[it], src + (uint64_t)(uint32_t)g[it] * ldxb, vb, keep);
-      } else {  // the window's last chunk: pad slots (-1) are zero-filled
-#pragma unroll
-        for (int it = 0; it < NI; ++it) {
-          const int gi = g[it];
-          cp_async16(dst + dofs[it], src + (uint64_t)(uint32_t)max(gi, 0) * ldxb, gi >= 0 ? vb : 0u, keep);
-        }
-      }
-    }
-    cp_async_commit();
-  };
-  auto load_ent = [&](const int4& d, uint32_t (&e)[kWarpEntRegs]) {
-    const int64_t e0 = (int64_t)(uint32_t)d.x | ((int64_t)d.y << 32);
-    const int ne = d.w >> 2;
-#pragma unroll
-    for (int q = 0; q < kWarpEntRegs; ++q) {
-      const int i = lane + 32 * q;
-      e[q] = i < ne ? ld_plan_u32(ent + e0 + i, once) : 0u;
-    }
-    const int ov = 32 * kWarpEntRegs + 32 * lane;
-    if (ov < ne) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(ent + e0 + ov));
-  };
-
-  float acc[SWV][4];
-#pragma unroll
-  for (int i = 0; i < SWV; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
-  float oacc[FUSED ? kFusedOutMax / 8 : 1][4];
-#pragma unroll
-  for (int i = 0; i < (FUSED ? kFusedOutMax / 8 : 1); ++i) oacc[i][0] = oacc[i][1] = oacc[i][2] = oacc[i][3] = 0.f;
-  bool in_head;  // our first window began in an earlier range
-  int s0 = 0;
-
-  // step at chunk c: D[0..4] = descriptors of c..c+4 (desc of c+5 loaded here: 3 steps ahead of its
-  // gather issue, whose full / padded path it selects), Gcur = indices of
-  // c+2 (issued here), Gnext <- indices of c+3, Ecur = entries of c, Enext <- entries of c+1
-  auto step = [&](int64_t c, int4 (&D)[5], int (&Gcur)[NI], int (&Gnext)[NI], uint32_t (&Ecur)[kWarpEntRegs],
-                  uint32_t (&Enext)[kWarpEntRegs]) -> bool {
-    if (c >= cb) return true;
-    const int4 D0 = D[0];
-    const int s2 = s0 >= 1 ? s0 - 1 : s0 + 2;
-    issue(c + 2, D[2], Gcur, s2);
-    load_gidx(c + 3, Gnext);
-    D[0] = D[1];
-    D[1] = D[2];
-    D[2] = D[3];
-    D[3] = D[4];
-    D[4] = load_desc(c + 5);
-    load_ent(D[0], Enext);  // (now the descriptor of c + 1)
-    const int ne = D0.w >> 2;
-    {
-#pragma unroll
-      for (int q = 0; q < kWarpEntRegs; ++q)
-        if (lane + 32 * q < ne) sts16(slab + (Ecur[q] & 0x7FFu), Ecur[q] >> 16);
-      const int64_t e0 = (int64_t)(uint32_t)D0.x | ((int64_t)D0.y << 32);
-      for (int i0 = 32 * kWarpEntRegs; i0 < ne; i0 += 32 * 8) {
-        uint32_t w[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int i = i0 + 32 * u + lane;
-          w[u] = i < ne ? ld_plan_u32(ent + e0 + i, once) : 0u;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (i0 + 32 * u + lane < ne) sts16(slab + (w[u] & 0x7FFu), w[u] >> 16);
-      }
-    }
-    cp_async_wait<2>();
-    __syncwarp();
-    {
-      const uint32_t st = stage0 + s0 * kWarpStageBytes;
-#pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
-        uint32_t af[4];
-        const int kc = 2 * ks + akc;
-        ldsm_x4(af, slab + ar * 128 + (((kc ^ ar) & 7) << 4));
-        const int k = ks * 16 + bk;
-#pragma unroll
-        for (int pr = 0; pr < NPR; ++pr) {
-          uint32_t bb[4];
-          ldsm_x4_trans(bb, st + C::off(k, 2 * pr + bfc));
-          hmma_16816(acc[2 * pr], af, bb[0], bb[1]);
-          hmma_16816(acc[2 * pr + 1], af, bb[2], bb[3]);
-        }
-      }
-    }
-    __syncwarp();
-    if (ne <= 32 * kWarpEntRegs) {
-#pragma unroll
-      for (int q = 0; q < kWarpEntRegs; ++q)
-        if (lane + 32 * q < ne) sts16(slab + (Ecur[q] & 0x7FFu), 0u);
-    } else {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) sts128_zero(slab + (lane + 32 * q) * 16);
-    }
-    __syncwarp();  // the next chunk's scatter may hit a slot another lane clears here
-    const bool unit_done = D0.w & 1;
-    if (unit_done || c + 1 == cb) {
-      const int t = D0.z - t_base;  // window of this launch's views
-      const int64_t rs = (int64_t)__ldg(tile_list + t) * wh;
-      const int rows = (int)(n_rows - rs < wh ? n_rows - rs : wh);
-      bool zsplit = false;
-      if (z != nullptr) {
-        if (!in_head && unit_done) {
-          store_slice<SWV>(z, ldz, rs, rows, dim, fw, acc, lane);
-        } else {
-          write_slot<SWV>(scratch + (gw * 2 + (in_head ? 0 : 1)) * C::kSlot, acc, lane);
-          zsplit = true;
-        }
-      }
-      if (FUSED) {
-        const uint32_t* wt = reinterpret_cast<const uint32_t*>(wsmem + C::kOffW);
-        const int g8 = lane >> 2, t4 = lane & 3;
-#pragma unroll
-        for (int j = 0; j < NPR; ++j) {
-          uint32_t af[4];
-          af[0] = pack_bf16(acc[2 * j][0], acc[2 * j][1]);
-          af[1] = pack_bf16(acc[2 * j][2], acc[2 * j][3]);
-          af[2] = pack_bf16(acc[2 * j + 1][0], acc[2 * j + 1][1]);
-          af[3] = pack_bf16(acc[2 * j + 1][2], acc[2 * j + 1][3]);
-          const int kb = fw * C::kFeat + 16 * j;
-#pragma unroll
-          for (int n8 = 0; n8 < kFusedOutMax / 8; ++n8) {
-            if (n8 * 8 < d_out) {
-              const uint32_t* wrow = wt + ((n8 * 8 + g8) * kFusedLdw + kb) / 2 + t4;
-              hmma_16816(oacc[n8], af, wrow[0], wrow[4]);
-            }
-          }
-        }
-        if (paired) {  // the pair's slice partials through warp f = 1's consumed ring slot
-          const uint32_t xs = smem_u32(wsmem + (warp | 1) * kWarpSmemPerWarp) + s0 * kWarpStageBytes;
-          const int bar = 1 + (warp >> 1);
-          if (fw == 1) {
-#pragma unroll
-            for (int n8 = 0; n8 < kFusedOutMax / 8; ++n8)
-#pragma unroll
-              for (int q = 0; q < 4; ++q) sts32f(xs + ((n8 * 4 + q) * 32 + lane) * 4, oacc[n8][q]);
-          }
-          named_bar_sync(bar, 64);
-          if (fw == 0) {
-#pragma unroll
-            for (int n8 = 0; n8 < kFusedOutMax / 8; ++n8)
-#pragma unroll
-              for (int q = 0; q < 4; ++q) oacc[n8][q] += lds32f(xs + ((n8 * 4 + q) * 32 + lane) * 4);
-          }
-          named_bar_sync(bar, 64);
-        }
-        if (fw == 0) {
-          if (unit_done && !in_head) {
-            store_out(out, ldo, rs, rows, d_out, oacc, lane);
-          } else {
-            const int64_t gi = paired ? gw / FS : gw;
-            write_slot(oscratch + (gi * 2 + (in_head ? 0 : 1)) * kOutSlot, oacc, lane);
-            const int64_t base = __ldg(chunk_ptr + t);
-            finish_split_out(chunk_ptr, T, FS, 1, kWarpTileWarps, cnt, oscratch, out, ldo, base,
-                             (int)(__ldg(chunk_ptr + t + 1) - base), rs, rows, d_out);
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < kFusedOutMax / 8; ++i) oacc[i][0] = oacc[i][1] = oacc[i][2] = oacc[i][3] = 0.f;
-      }
-      in_head = false;
-      if (zsplit) {
-        const int64_t base = __ldg(chunk_ptr + t);
-        finish_split_z<SWV, C::kSlot>(chunk_ptr, T, FS, 1, kWarpTileWarps, cnt, scratch, z, ldz, base, 0,
-                                      (int)(__ldg(chunk_ptr + t + 1) - base), rs, rows, dim);
-      }
-#pragma unroll
-      for (int i = 0; i < SWV; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
-    }
-    s0 = s0 == kWarpTileStages - 1 ? 0 : s0 + 1;
-    return false;
-  };
-
-#pragma unroll
-  for (int q = 0; q < 4; ++q) sts128_zero(slab + (lane + 32 * q) * 16);
-  __syncwarp();
-  const int64_t ca = c0 + a;
-  int4 D[5];
-#pragma unroll
-  for (int i = 0; i < 5; ++i) D[i] = load_desc(ca + i);
-  in_head = !(D[0].w & 2);
-  int G0[NI], G1[NI];
-  load_gidx(ca, G0);
-  load_gidx(ca + 1, G1);
-  issue(ca, D[0], G0, 0);
-  issue(ca + 1, D[1], G1, 1);
-  load_gidx(ca + 2, G0);
-  uint32_t E0[kWarpEntRegs], E1[kWarpEntRegs];
-  load_ent(D[0], E0);
-  for (int64_t c = ca;; c += 2) {
-    if (step(c, D, G0, G1, E0, E1)) break;
-    if (step(c + 1, D, G1, G0, E1, E0)) break;
   }
   cp_async_wait<0>();
 }
@@ -1234,9 +929,6 @@ static int g_warp_swv = 0;     // 0 auto, 4 or 8 (16-B vectors per row slice)
 static int g_warp_paired = 1;
 // 33..48-feature single slice: 1 = skip the empty 16-feature group at compile time (NPR = 3)
 static int g_warp_npr3 = 1;
-// 1 (default): the chunk-descriptor kernel whenever a plan provides descriptors and every position
-// is one chunk; 0: the position-walking kernel (experiment switch, hcs_set_tile_chunk_kernel)
-static int g_warp_chunk = 1;
 constexpr int64_t kPairMinXBytes = 96ll << 20;
 
 template <int SWV, bool FUSED = false>
@@ -1244,7 +936,7 @@ static int launch_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* 
                        const int64_t* ent_ptr, const uint32_t* ent, int64_t n_rows, int wh, const __nv_bfloat16* x,
                        int64_t ldx, int dim, float* z, int64_t ldz, float* scratch, int64_t scratch_floats,
                        cudaStream_t st, const float* mw = nullptr, int d_out = 0, float* out = nullptr,
-                       int64_t ldo = 0, int64_t x_rows = 0, const int4* desc = nullptr) {
+                       int64_t ldo = 0, int64_t x_rows = 0) {
   using C = WarpCfg<SWV>;
   const int FS = (dim + C::kFeat - 1) / C::kFeat;
   const int grid = num_sms();
@@ -1264,16 +956,9 @@ static int launch_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* 
   // one slice of 33..48 features: the fused (GCN) kernel skips the empty 16-feature group
   // (C3 5.92 -> 5.71 ms); the plain SpMM is faster with the full unrolled schedule now that
   // every lane copies whole padded rows (N = 40/41/48: 1.29 -> 1.21 ms; tools/exp_c3_npr3.sh)
-  const bool npr3 = FUSED && g_warp_npr3 && SWV == 8 && FS == 1 && dim <= 48 && dim > 32;
-  if (desc != nullptr && g_warp_chunk && (paired || FS == 1)) {  // every position is one chunk
-    auto kern = npr3 ? k_tile_chunk<SWV, FUSED, (SWV == 8 ? 3 : SWV / 2)> : k_tile_chunk<SWV, FUSED>;
-    HCS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    kern<<<grid, C::kWarps * 32, smem, st>>>(tile_list, n_tile, chunk_ptr, desc, gidx, ent, n_rows, wh, x, ldx, dim,
-                                              FS, z, ldz, slots, mw, d_out, out, ldo, oscratch, paired, cnt);
-    HCS_LAUNCH_CHECK("k_tile_chunk");
-    return HCS_OK;
-  }
-  auto kern = npr3 ? k_tile_warp<SWV, FUSED, (SWV == 8 ? 3 : SWV / 2)> : k_tile_warp<SWV, FUSED>;
+  auto kern = (FUSED && g_warp_npr3 && SWV == 8 && FS == 1 && dim <= 48 && dim > 32)
+                  ? k_tile_warp<SWV, FUSED, (SWV == 8 ? 3 : SWV / 2)>
+                  : k_tile_warp<SWV, FUSED>;
   HCS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   kern<<<grid, C::kWarps * 32, smem, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim,
                                             FS, z, ldz, slots, mw, d_out, out, ldo, oscratch, paired, cnt);
@@ -1285,25 +970,25 @@ static int launch_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* 
 int gcn_tile_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
                   const int64_t* ent_ptr, const uint32_t* ent, int64_t n_rows, int wh, const __nv_bfloat16* x,
                   int64_t ldx, int dim, float* z, int64_t ldz, const float* m, int d_out, float* out, int64_t ldo,
-                  float* scratch, int64_t scratch_floats, cudaStream_t st, const int4* desc) {
+                  float* scratch, int64_t scratch_floats, cudaStream_t st) {
   return launch_warp<8, true>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim, z, ldz,
-                              scratch, scratch_floats, st, m, d_out, out, ldo, 0, desc);
+                              scratch, scratch_floats, st, m, d_out, out, ldo);
 }
 
 int spmm_tile_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
                    const int64_t* ent_ptr, const uint32_t* ent, int64_t n_rows, int wh, const __nv_bfloat16* x,
                    int64_t x_rows, int64_t ldx, int dim, float* z, int64_t ldz, float* scratch, int64_t scratch_floats,
-                   cudaStream_t st, const int4* desc) {
+                   cudaStream_t st) {
   // 64-feature slices halve the per-feature slab work once a window has >= 2 slices of 32
   const int swv = g_warp_swv ? g_warp_swv : (dim > 32 ? 8 : 4);
   if (swv == 16)
     return launch_warp<16>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim, z, ldz, scratch,
-                          scratch_floats, st, nullptr, 0, nullptr, 0, x_rows, desc);
+                          scratch_floats, st, nullptr, 0, nullptr, 0, x_rows);
   if (swv == 8)
     return launch_warp<8>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim, z, ldz, scratch,
-                          scratch_floats, st, nullptr, 0, nullptr, 0, x_rows, desc);
+                          scratch_floats, st, nullptr, 0, nullptr, 0, x_rows);
   return launch_warp<4>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim, z, ldz, scratch,
-                          scratch_floats, st, nullptr, 0, nullptr, 0, x_rows, desc);
+                          scratch_floats, st, nullptr, 0, nullptr, 0, x_rows);
 }
 
 int64_t tile_warp_scratch_floats() {
@@ -1325,11 +1010,9 @@ using namespace hcs;
 extern "C" int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
                              const int64_t* ent_ptr, const void* ent, int ent_dtype, int64_t n_rows, int32_t wh,
                              const void* x, int x_dtype, int64_t x_rows, int32_t dim, int64_t ldx, float* z,
-                             int64_t ldz, void* workspace, size_t ws_bytes, const void* chunk_desc,
-                             void* stream) {
+                             int64_t ldz, void* workspace, size_t ws_bytes, void* stream) {
   HCS_REQUIRE(wh > 0 && wh <= 16, HCS_EINVAL, "tile path supports window heights 1..16 (got %d)", wh);
   HCS_REQUIRE(dim > 0, HCS_EINVAL, "dim must be positive");
-  HCS_REQUIRE(((uintptr_t)chunk_desc & 15) == 0, HCS_EINVAL, "chunk_desc must be 16-byte aligned");
   HCS_REQUIRE(((uintptr_t)x & 15) == 0, HCS_EINVAL, "x must be 16-byte aligned");
   HCS_REQUIRE(x_dtype == ent_dtype, HCS_EINVAL, "x and plan dtypes differ (%d vs %d)", x_dtype, ent_dtype);
   HCS_REQUIRE(((uintptr_t)z & 7) == 0 && ldz % 2 == 0, HCS_EINVAL, "z must be 8-byte aligned with even ldz");
@@ -1345,7 +1028,7 @@ extern "C" int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int
   if (n_tile == 0) return HCS_OK;
   return spmm_tile_warp(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, (const uint32_t*)ent, n_rows, wh,
                         (const __nv_bfloat16*)x, x_rows, ldx, dim, z, ldz, (float*)workspace,
-                        (int64_t)(ws_bytes / sizeof(float)), as_stream(stream), (const int4*)chunk_desc);
+                        (int64_t)(ws_bytes / sizeof(float)), as_stream(stream));
 }
 
 // K6/K7: tile windows with the fused GCN epilogue: out = (A_w X) M per TILE window, plus
@@ -1356,8 +1039,7 @@ extern "C" int hcs_gcn_tile(const int32_t* tile_list, int64_t n_tile, const int6
                             const int64_t* ent_ptr, const void* ent, int ent_dtype, int64_t n_rows, int32_t wh,
                             const void* x, int x_dtype, int64_t x_rows, int32_t dim, int64_t ldx, float* z,
                             int64_t ldz, const float* m, int32_t d_out, float* out, int64_t ldo, void* workspace,
-                            size_t ws_bytes, const void* chunk_desc, void* stream) {
-  HCS_REQUIRE(((uintptr_t)chunk_desc & 15) == 0, HCS_EINVAL, "chunk_desc must be 16-byte aligned");
+                            size_t ws_bytes, void* stream) {
   HCS_REQUIRE(wh > 0 && wh <= 16, HCS_EINVAL, "tile path supports window heights 1..16 (got %d)", wh);
   HCS_REQUIRE(d_out > 0 && d_out <= kFusedOutMax, HCS_EINVAL, "fused GCN tile path needs 1 <= d_out <= %d (got %d)",
               kFusedOutMax, d_out);
@@ -1381,7 +1063,7 @@ extern "C" int hcs_gcn_tile(const int32_t* tile_list, int64_t n_tile, const int6
   if (n_tile == 0) return HCS_OK;
   return gcn_tile_warp(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, (const uint32_t*)ent, n_rows, wh,
                        (const __nv_bfloat16*)x, ldx, dim, z, ldz, m, d_out, out, ldo, (float*)workspace,
-                       (int64_t)(ws_bytes / sizeof(float)), st, (const int4*)chunk_desc);
+                       (int64_t)(ws_bytes / sizeof(float)), st);
 }
 
 // Experiment switch: the fused kernel's NPR = 3 variant for a single 33..48-feature slice (1, default) or the full one (0).
@@ -1411,14 +1093,5 @@ extern "C" int hcs_set_tile_pairing(int on) {
 extern "C" int hcs_tile_scratch_floats(int64_t* floats) {
   HCS_REQUIRE(floats != nullptr, HCS_EINVAL, "floats is NULL");
   *floats = hcs::tile_warp_scratch_floats();
-  return HCS_OK;
-}
-
-// Experiment switch: the chunk-descriptor tile kernel (1, default, when the plan provides
-// descriptors) or the position-walking kernel (0).  Both are deterministic; the cut points are the
-// same, so the results are bitwise identical.
-extern "C" int hcs_set_tile_chunk_kernel(int on) {
-  HCS_REQUIRE(on == 0 || on == 1, HCS_EINVAL, "chunk kernel switch must be 0 or 1 (got %d)", on);
-  hcs::g_warp_chunk = on;
   return HCS_OK;
 }

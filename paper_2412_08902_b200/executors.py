@@ -311,25 +311,6 @@ class HybridPlan:
             self.scalar_vals, self.scalar_vals_code = csr.values_bf16(), _lib.DTYPE_BF16
         else:
             self.scalar_vals, self.scalar_vals_code = csr.values, _lib.DTYPE_F32
-        self.chunk_desc = self._chunk_descriptors() if (self.n_tile and precision == "bf16") else None
-
-    def _chunk_descriptors(self) -> torch.Tensor:
-        """One 16-byte descriptor per chunk for the chunk-walking tile kernel (include/hcspmm.h,
-        hcs_spmm_tile): {int64 first entry, int32 tile-list index of the window, int32
-        entries << 2 | first-chunk-of-window << 1 | last-chunk}."""
-        dev = self.chunk_ptr.device
-        nch = self.nchunks
-        counts = self.chunk_ptr[1:] - self.chunk_ptr[:-1]
-        t_of = torch.repeat_interleave(torch.arange(self.n_tile, device=dev), counts)
-        c = torch.arange(nch, device=dev)
-        first = (c == self.chunk_ptr[t_of]).to(torch.int64)
-        last = (c == self.chunk_ptr[t_of + 1] - 1).to(torch.int64)
-        ne = self.ent_ptr[1:] - self.ent_ptr[:-1]
-        desc = torch.empty((nch, 4), dtype=torch.int32, device=dev)
-        desc[:, 0:2] = self.ent_ptr[:-1].contiguous().view(torch.int32).view(nch, 2)
-        desc[:, 2] = t_of.to(torch.int32)
-        desc[:, 3] = ((ne << 2) | (first << 1) | last).to(torch.int32)
-        return desc
 
     @property
     def _cache(self) -> dict:
@@ -429,8 +410,7 @@ class HybridPlan:
             _lib.call("hcs_spmm_tile", self.tile_list.data_ptr() + 4 * t0, t1 - t0, self.chunk_ptr.data_ptr() + 8 * t0,
                       self.gidx.data_ptr(), self.ent_ptr.data_ptr(), self.ent.data_ptr(), self.ent_dtype,
                       csr.num_rows, self.windows.window_height, xop.t.data_ptr(), xop.dtype_code, xop.rows, xop.dim,
-                      xop.ld, z.data_ptr(), ldz, scratch.data_ptr(), scratch.numel() * 4,
-                      self.chunk_desc.data_ptr() if self.chunk_desc is not None else None, s)
+                      xop.ld, z.data_ptr(), ldz, scratch.data_ptr(), scratch.numel() * 4, s)
         if tile_events is not None:
             tile_events[1].record()
         if s1 > s0:

@@ -127,7 +127,7 @@ class FusedLayer:
                       plan.gidx.data_ptr(), plan.ent_ptr.data_ptr(), plan.ent.data_ptr(), plan.ent_dtype,
                       csr.num_rows, ws.window_height, xop.t.data_ptr(), xop.dtype_code, xop.rows, dim, xop.ld, zp,
                       self.ldz, self.mt.data_ptr(), d_out, self.out.data_ptr(), d_out, scr.data_ptr(),
-                      scr.numel() * 4, plan.chunk_desc.data_ptr() if plan.chunk_desc is not None else None, s)
+                      scr.numel() * 4, s)
         if s1 > s0:
             _lib.call("hcs_gcn_scalar", csr.row_ptr.data_ptr(), csr.col_idx.data_ptr(), plan.scalar_vals.data_ptr(),
                       plan.scalar_vals_code, csr.num_rows, ws.window_height, plan.scalar_list.data_ptr() + 4 * s0,

@@ -479,40 +479,3 @@ def test_spmm_graph_replay(cuda_ok, precision):
         hc.SpmmGraph(ws, asg, x.cpu())
 
 
-
-@pytest.mark.parametrize("dim", [32, 64, 128, 41])
-def test_chunk_kernel_matches_position_kernel(cuda_ok, dim):
-    """The chunk-descriptor tile kernel (default) == the position-walking kernel bit for bit (same
-    balanced ranges and cut points, same arithmetic order): plain products at every slice width,
-    row-range parts (sub-range launches: descriptors carry plan-wide window indices), and the fused
-    GCN epilogue (paired slices at 128 features, the NPR = 3 kernel at 41)."""
-    from paper_2412_08902_b200 import _lib, gnn
-
-    a = plaw8k_csr()
-    ws = hc.partition(to_hc(a))
-    asg = Assignment.uniform(len(ws), Path.TILE)
-    x = torch.from_numpy(orc.random_dense(a.num_cols, dim, 3)).to(torch.bfloat16).cuda()
-    from paper_2412_08902_b200.executors import _alloc_z, get_plan, stage_operand
-
-    plan = get_plan(ws, asg, "bf16")
-    assert plan.chunk_desc is not None
-    xop, _ = stage_operand(x, "bf16", x.device)
-    layer = gnn.GnnLayer.random(dim, 40, seed=1)
-    res = {}
-    try:
-        for on in (1, 0):
-            _lib.call("hcs_set_tile_chunk_kernel", on)
-            z, ldz = _alloc_z(ws.num_rows, dim, x.device)
-            plan.run(xop, z, ldz)
-            zp, _ = _alloc_z(ws.num_rows, dim, x.device)
-            for part in plan.parts(5):
-                plan.run(xop, zp, ldz, part=part)
-            f, zc, _ = gnn.forward(layer, ws, x.float(), mode="fused", assignment=asg, windows=ws)
-            res[on] = (z[:, :dim].clone(), zp[:, :dim].clone(), f.data.clone(), zc.data.clone())
-    finally:
-        _lib.call("hcs_set_tile_chunk_kernel", 1)
-    for u, v in zip(res[1], res[0]):
-        assert torch.equal(u, v)
-    exact = orc.spmm_exact(a, x.float().cpu().numpy())
-    assert orc.max_rel_err(res[1][0].cpu().numpy(), exact) <= BF16_TOL
-    assert orc.max_rel_err(res[1][1].cpu().numpy(), exact) <= BF16_TOL
