@@ -671,7 +671,7 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
                      const uint2* __restrict__ ent, int64_t n_rows, int wh, const float* __restrict__ x, int64_t ldx,
                      int dim, int FS, float* __restrict__ z, int64_t ldz, float* __restrict__ scratch,
                      const float* __restrict__ mw, int d_out, float* __restrict__ out, int64_t ldo,
-                     float* __restrict__ oscratch, unsigned* __restrict__ cnt) {
+                     float* __restrict__ oscratch, unsigned* __restrict__ cnt, int paired) {
   constexpr int NI = 16;
   extern __shared__ uint8_t tsmem_raw[];
   uint8_t* tsmem = (uint8_t*)(((uintptr_t)tsmem_raw + 127) & ~(uintptr_t)127);
@@ -679,9 +679,14 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
   const int64_t nwarps = (int64_t)gridDim.x * kTfWarps;
   const int64_t gw = (int64_t)blockIdx.x * kTfWarps + warp;
   const int64_t c0 = chunk_ptr[0];
-  const int64_t total = (int64_t)FS * (chunk_ptr[T] - c0);
-  int64_t a, b;
-  warp_range(total, nwarps, gw, a, b);
+  // paired slices (plain SpMM, FS dividing the CTA's warps): the FS warps of a group walk one
+  // balanced range of chunks, one 32-feature slice each, so each chunk's plan is read once
+  const int FSr = paired ? 1 : FS;
+  const int fw = paired ? (int)(gw % FS) : 0;
+  const int64_t ngroups = paired ? nwarps / FS : nwarps;
+  const int64_t total = (int64_t)FSr * (chunk_ptr[T] - c0);
+  int64_t a = 0, b = 0;
+  if (!paired || gw < ngroups * FS) warp_range(total, ngroups, paired ? gw / FS : gw, a, b);
   if (a >= b) return;
   const uint32_t stage0 = smem_u32(tsmem + warp * kTfPerWarp);
   const uint32_t slab = stage0 + kWarpTileStages * kTfStage;
@@ -696,13 +701,13 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
   const int g8 = lane >> 2, t4 = lane & 3;
   const int arow = (lane & 7) + ((lane >> 3) & 1) * 8, ach = lane >> 4;
 
-  ChunkPos p0 = locate(chunk_ptr, T, FS, a);
+  ChunkPos p0 = locate(chunk_ptr, T, FSr, a);
   ChunkPos p1 = p0, p2, p3;
-  advance(p1, chunk_ptr, T, FS);
+  advance(p1, chunk_ptr, T, FSr);
   p2 = p1;
-  advance(p2, chunk_ptr, T, FS);
+  advance(p2, chunk_ptr, T, FSr);
   p3 = p2;
-  advance(p3, chunk_ptr, T, FS);
+  advance(p3, chunk_ptr, T, FSr);
   bool in_head = p0.j != 0;
 
   auto load_gidx = [&](const ChunkPos& p, int (&g)[NI]) {
@@ -723,7 +728,7 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
   };
   auto issue = [&](const ChunkPos& p, const int (&g)[NI], int slot) {
     if (p.fi < b) {
-      const int feat = p.f * 32 + gv * 4;
+      const int feat = (p.f + fw) * 32 + gv * 4;
       const uint32_t vb = feat < ldx ? 16u : 0u;  // zero padding read as data (see k_tile_warp)
       const char* src = xb + (int64_t)feat * 4;
       const uint32_t dst = stage0 + slot * kTfStage;
@@ -833,7 +838,7 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
       bool zsplit = false;
       if (z != nullptr) {
         if (!in_head && unit_done) {
-          store_slice<4>(z, ldz, rs, rows, dim, p0.f, acc, lane);
+          store_slice<4>(z, ldz, rs, rows, dim, p0.f + fw, acc, lane);
         } else {
           write_slot<4>(scratch + (gw * 2 + (in_head ? 0 : 1)) * WarpCfg<4>::kSlot, acc, lane);
           zsplit = true;
@@ -876,15 +881,15 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
         }
       }
       if (zsplit)
-        finish_split_z<4, WarpCfg<4>::kSlot>(chunk_ptr, T, FS, 0, kTfWarps, cnt, scratch, z, ldz, p0.base, p0.f,
-                                             p0.nj, rs, rows, dim);
+        finish_split_z<4, WarpCfg<4>::kSlot>(chunk_ptr, T, FS, paired, kTfWarps, cnt, scratch, z, ldz, p0.base,
+                                             p0.f, p0.nj, rs, rows, dim);
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
     }
     p0 = p1;
     p1 = p2;
     p2 = p3;
-    advance(p3, chunk_ptr, T, FS);
+    advance(p3, chunk_ptr, T, FSr);
 #pragma unroll
     for (int q = 0; q < kWarpEntRegs; ++q) e0r[q] = e1r[q];
     ep0a = ep1a;
@@ -895,6 +900,9 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
   }
   cp_async_wait<0>();
 }
+
+// paired 32-feature slices for the tf32 SpMM (1 default; hcs_set_tile_pairing(0) turns it off too)
+static int g_warp_paired_tf32 = 1;
 
 // tf32 SpMM (m == nullptr) or fused GCN layer (m = tf32-rounded M [dim x d_out], d_out <= 64; z may
 // be nullptr when no z_cache is wanted).
@@ -913,9 +921,10 @@ int spmm_tile_warp_tf32(const int32_t* tile_list, int64_t n_tile, const int64_t*
   float* slots = scratch + cw;
   float* oscratch = slots + nwarps * 2 * WarpCfg<4>::kSlot;
   auto kern = fused ? k_tile_warp_tf32<true> : k_tile_warp_tf32<false>;
+  const int paired = (!fused && FS > 1 && kTfWarps % FS == 0 && g_warp_paired_tf32) ? 1 : 0;
   HCS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kTfSmem));
   kern<<<grid, kTfWarps * 32, kTfSmem, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim,
-                                             FS, z, ldz, slots, m, d_out, out, ldo, oscratch, cnt);
+                                             FS, z, ldz, slots, m, d_out, out, ldo, oscratch, cnt, paired);
   HCS_LAUNCH_CHECK("k_tile_warp_tf32");
   return HCS_OK;
 }
@@ -1087,6 +1096,7 @@ extern "C" int hcs_set_tile_slice(int vectors) {
 extern "C" int hcs_set_tile_pairing(int on) {
   HCS_REQUIRE(on >= 0 && on <= 2, HCS_EINVAL, "pairing must be 0, 1 or 2 (got %d)", on);
   hcs::g_warp_paired = on;
+  hcs::g_warp_paired_tf32 = on ? 1 : 0;
   return HCS_OK;
 }
 
