@@ -474,6 +474,37 @@ def run_ours(args):
                               "api": ("paper_2412_08902_b200.spmm_hybrid(windows, assignment, DenseMatrix(float64 "
                                       "numpy X, pageable)) -> numpy float32 Z: the rowwin caller's drop-in call"),
                               "staging": dropin_staging}}
+        if with_e2e and world > 1 and args.precision == "bf16":
+            # end to end at N ranks through the same calls: every step uploads the rank's X replica
+            # from pinned host memory, runs the shard's windows with the overlapped all-gather of the
+            # output rows, and reads the rank's rows back into pinned host memory
+            xh = x.cpu().pin_memory()
+            out_h = torch.empty((local_a.num_rows, dim), dtype=torch.float32, pin_memory=True)
+
+            def e2e_step():
+                x.copy_(xh, non_blocking=True)
+                step()
+                out_h.copy_(z[:local_a.num_rows, :dim], non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+
+            for _ in range(2):
+                e2e_step()
+            dist.barrier()
+            k = max(3, min(steps, 20))
+            t1 = time.perf_counter()
+            for _ in range(k):
+                e2e_step()
+            t_loc = (time.perf_counter() - t1) / k
+            tt = torch.tensor([t_loc], device=dev if not gloo else "cpu", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = float(tt[0])
+            e2e = {"value": 2.0 * nnz * dim / e2e_s / 1e9, "unit": "GFLOP/s",
+                   "h2d_bytes_per_step": int(xh.numel() * xh.element_size()),
+                   "d2h_bytes_per_step": int(out_h.numel() * out_h.element_size()),
+                   "ms_per_step": e2e_s * 1e3,
+                   "api": ("per rank: pinned bf16 X replica -> HBM, the shard's hybrid SpMM in "
+                           f"{len(parts)} parts with the overlapped all-gather of the output rows, the rank's "
+                           "fp32 rows -> pinned host memory; max over ranks (wall clock per step)")}
         return ms, tile_ms, sampler.summary(), e2e
 
     dim = args.dim
