@@ -141,9 +141,6 @@ int hcs_set_tile_npr3(int on);
  * 0 = one warp per contiguous range of (window, slice, chunk); 2 = 1 only when X exceeds 96 MB.
  * All deterministic. */
 int hcs_set_tile_pairing(int on);
-/* plain bf16 SpMM with 64-feature slices: 1 (default) = the 12-warp, 2-stage kernel, 0 = the 8-warp,
- * 3-stage kernel (experiment switch) */
-int hcs_set_tile_warp2(int on);
 int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
                   const int64_t* ent_ptr, const void* ent, int ent_dtype, int64_t n_rows, int32_t wh, const void* x,
                   int x_dtype, int64_t x_rows, int32_t dim, int64_t ldx, float* z, int64_t ldz, void* workspace,

@@ -646,249 +646,6 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
   cp_async_wait<0>();
 }
 
-// ---------------------------------------------------------------- 12-warp, 2-stage variant
-// Occupancy measured on k_tile_warp at C2 (profiles/r02_tile_occupancy.txt): 4 / 6 / 8 warps per SM
-// take 4.15 / 3.11 / 2.43 ms at N = 128 -- almost linear, the kernel is issue-latency bound with
-// 2 warps per scheduler.  Shared memory (3 x 8 KB stages + a 2 KB slab per warp) caps it at 8; with
-// a 2-stage ring (18 KB per warp) a CTA holds 12 warps, at <= 168 registers per thread.  Chunk k's
-// gathers are issued one step ahead (into the slot chunk k-2 used), its indices two steps ahead;
-// the rest (slab, MMAs, split units) is k_tile_warp's.  Plain SpMM, 64-feature slices.
-constexpr int kW2Warps = 12;
-constexpr int kW2Stages = 2;
-constexpr int kW2PerWarp = kW2Stages * WarpCfg<8>::kStageBytes + kWarpSlabBytes;
-constexpr int kW2Smem = kW2Warps * kW2PerWarp + 128;
-static_assert(kW2Smem <= 227 * 1024, "smem");
-
-__global__ void __launch_bounds__(kW2Warps * 32, 1)
-    k_tile_warp2(const int32_t* __restrict__ tile_list, int64_t T, const int64_t* __restrict__ chunk_ptr,
-                 const int32_t* __restrict__ gidx, const int64_t* __restrict__ ent_ptr,
-                 const uint32_t* __restrict__ ent, int64_t n_rows, int wh, const __nv_bfloat16* __restrict__ x,
-                 int64_t ldx, int dim, int FS, float* __restrict__ z, int64_t ldz, float* __restrict__ scratch,
-                 int paired, unsigned* __restrict__ cnt) {
-  constexpr int SWV = 8;
-  using C = WarpCfg<SWV>;
-  constexpr int NI = C::kIssue;  // 16 copies of 16 B per lane per chunk
-  constexpr int kStage = C::kStageBytes;
-  extern __shared__ uint8_t w2smem_raw[];
-  uint8_t* wsmem = (uint8_t*)(((uintptr_t)w2smem_raw + 127) & ~(uintptr_t)127);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t nwarps = (int64_t)gridDim.x * kW2Warps;
-  const int64_t gw = (int64_t)blockIdx.x * kW2Warps + warp;
-  const int64_t c0 = chunk_ptr[0];
-  const int FSr = paired ? 1 : FS;
-  const int fw = paired ? (int)(gw % FS) : 0;
-  const int64_t ngroups = paired ? nwarps / FS : nwarps;
-  const int64_t total = (int64_t)FSr * (chunk_ptr[T] - c0);
-  int64_t a = 0, b = 0;
-  if (!paired || gw < ngroups * FS) warp_range(total, ngroups, paired ? gw / FS : gw, a, b);
-  if (a >= b) return;
-  const uint32_t stage0 = smem_u32(wsmem + warp * kW2PerWarp);
-  const uint32_t slab = stage0 + kW2Stages * kStage;
-  const uint64_t keep = policy_evict_last();
-  const uint64_t once = (FS > 1 && !paired) ? policy_evict_normal() : policy_evict_first();
-  const int gv = lane % SWV, rg = lane / SWV;
-  // smem destination of copy it = rg * NI * 128 + it * 128 + ((gv ^ (it & 7)) << 4) (C::off, SWV = 8)
-  uint32_t y8[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) y8[k] = (uint32_t)rg * NI * 128u + ((uint32_t)(gv ^ k) << 4);
-  const int featv = gv * 8;
-  const char* xb = reinterpret_cast<const char*>(x);
-  const uint32_t ldxb = (uint32_t)(ldx * 2);
-  const int ar = lane & 15, akc = lane >> 4;
-  const int bk = (lane & 7) + ((lane >> 3) & 1) * 8, bfc = lane >> 4;
-
-  struct Pos {
-    int64_t base;
-    int32_t t, f, j, nj, rem;
-  };
-  auto mk = [&](const ChunkPos& c) {
-    Pos p;
-    p.base = c.base;
-    p.t = (int32_t)c.t;
-    p.f = c.f;
-    p.j = c.j;
-    p.nj = c.nj;
-    p.rem = (int32_t)(b - c.fi);
-    return p;
-  };
-  auto adv = [&](Pos& p) {
-    --p.rem;
-    if (++p.j < p.nj) return;
-    p.j = 0;
-    if (++p.f < FSr) return;
-    p.f = 0;
-    ++p.t;
-    p.base += p.nj;
-    p.nj = (p.t < T && p.rem > 0) ? (int32_t)(ldg64(chunk_ptr + p.t + 1) - p.base) : 1;
-  };
-  auto load_gidx = [&](const Pos& p, int (&g)[NI]) {
-    if (p.rem > 0) {
-      const int4* gp = reinterpret_cast<const int4*>(gidx + (p.base + p.j) * 64 + rg * NI);
-#pragma unroll
-      for (int q = 0; q < NI / 4; ++q) {
-        int4 v;
-        asm volatile("ld.global.nc.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
-                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                     : "l"(gp + q), "l"(once));
-        g[4 * q] = v.x;
-        g[4 * q + 1] = v.y;
-        g[4 * q + 2] = v.z;
-        g[4 * q + 3] = v.w;
-      }
-    }
-  };
-  auto issue = [&](const Pos& p, const int (&g)[NI], int slot) {
-    if (p.rem > 0) {
-      const int feat = (p.f + fw) * C::kFeat + featv;
-      const uint32_t vb = feat < ldx ? 16u : 0u;
-      const char* src = xb + (int64_t)feat * 2;
-      const uint32_t dst = stage0 + slot * kStage;
-      if (p.j + 1 < p.nj) {
-#pragma unroll
-        for (int it = 0; it < NI; ++it)
-          cp_async16(dst + y8[it & 7] + it * 128, src + (uint64_t)(uint32_t)g[it] * ldxb, vb, keep);
-      } else {
-#pragma unroll
-        for (int it = 0; it < NI; ++it) {
-          const int gi = g[it];
-          cp_async16(dst + y8[it & 7] + it * 128, src + (uint64_t)(uint32_t)max(gi, 0) * ldxb, gi >= 0 ? vb : 0u,
-                     keep);
-        }
-      }
-    }
-    cp_async_commit();
-  };
-  auto load_ep = [&](const Pos& p, int64_t (&e)[2]) {
-    if (p.rem > 0) {
-      const int64_t c = p.base + p.j;
-      e[0] = ld_plan_s64(ent_ptr + c, once);
-      e[1] = ld_plan_s64(ent_ptr + c + 1, once);
-    } else {
-      e[0] = e[1] = 0;
-    }
-  };
-  auto load_ent = [&](const int64_t (&ep)[2], uint32_t (&e)[kWarpEntRegs]) {
-#pragma unroll
-    for (int q = 0; q < kWarpEntRegs; ++q) {
-      const int64_t i = ep[0] + lane + 32 * q;
-      e[q] = i < ep[1] ? ld_plan_u32(ent + i, once) : 0u;
-    }
-    const int64_t ov = ep[0] + 32 * kWarpEntRegs + 32 * lane;
-    if (ov < ep[1]) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(ent + ov));
-  };
-
-  float acc[SWV][4];
-#pragma unroll
-  for (int i = 0; i < SWV; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
-  bool in_head;
-  int s0 = 0;
-
-  // step: compute P0 (slot s0, gathers issued last step), issue P1 into slot s0 ^ 1, load the
-  // indices of P2, the entries of P1 and the entry pointers of P2
-  auto step = [&](Pos& P0, const Pos& P1, const Pos& P2, int (&Gcur)[NI], int (&Gnext)[NI],
-                  uint32_t (&Ecur)[kWarpEntRegs], uint32_t (&Enext)[kWarpEntRegs], const int64_t (&EP0)[2],
-                  const int64_t (&EP1)[2], int64_t (&EP2)[2]) -> bool {
-    if (P0.rem <= 0) return true;
-    issue(P1, Gcur, s0 ^ 1);
-    load_gidx(P2, Gnext);
-    load_ent(EP1, Enext);
-    load_ep(P2, EP2);
-    const int ne = (int)(EP0[1] - EP0[0]);
-    {
-#pragma unroll
-      for (int q = 0; q < kWarpEntRegs; ++q)
-        if (lane + 32 * q < ne) sts16(slab + (Ecur[q] & 0x7FFu), Ecur[q] >> 16);
-      for (int i0 = 32 * kWarpEntRegs; i0 < ne; i0 += 32 * 8) {
-        uint32_t w[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int i = i0 + 32 * u + lane;
-          w[u] = i < ne ? ld_plan_u32(ent + EP0[0] + i, once) : 0u;
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (i0 + 32 * u + lane < ne) sts16(slab + (w[u] & 0x7FFu), w[u] >> 16);
-      }
-    }
-    cp_async_wait<1>();  // P0's gathers landed (P1's may be in flight)
-    __syncwarp();
-    {
-      const uint32_t st = stage0 + s0 * kStage;
-#pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
-        uint32_t af[4];
-        const int kc = 2 * ks + akc;
-        ldsm_x4(af, slab + ar * 128 + (((kc ^ ar) & 7) << 4));
-        const int k = ks * 16 + bk;
-#pragma unroll
-        for (int pr = 0; pr < SWV / 2; ++pr) {
-          uint32_t bb[4];
-          ldsm_x4_trans(bb, st + C::off(k, 2 * pr + bfc));
-          hmma_16816(acc[2 * pr], af, bb[0], bb[1]);
-          hmma_16816(acc[2 * pr + 1], af, bb[2], bb[3]);
-        }
-      }
-    }
-    __syncwarp();
-    if (ne <= 32 * kWarpEntRegs) {
-#pragma unroll
-      for (int q = 0; q < kWarpEntRegs; ++q)
-        if (lane + 32 * q < ne) sts16(slab + (Ecur[q] & 0x7FFu), 0u);
-    } else {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) sts128_zero(slab + (lane + 32 * q) * 16);
-    }
-    __syncwarp();  // the next chunk's scatter may hit a slot another lane clears here
-    const bool unit_done = P0.j + 1 == P0.nj;
-    if (unit_done || P0.rem == 1) {
-      const int64_t rs = (int64_t)__ldg(tile_list + P0.t) * wh;
-      const int rows = (int)(n_rows - rs < wh ? n_rows - rs : wh);
-      if (!in_head && unit_done) {
-        store_slice<SWV>(z, ldz, rs, rows, dim, P0.f + fw, acc, lane);
-      } else {
-        write_slot<SWV>(scratch + (gw * 2 + (in_head ? 0 : 1)) * C::kSlot, acc, lane);
-        finish_split_z<SWV, C::kSlot>(chunk_ptr, T, FS, paired, kW2Warps, cnt, scratch, z, ldz, P0.base, P0.f,
-                                      P0.nj, rs, rows, dim);
-      }
-      in_head = false;
-#pragma unroll
-      for (int i = 0; i < SWV; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
-    }
-    s0 ^= 1;
-    P0 = P2;  // P0's variable becomes position +3
-    adv(P0);
-    return false;
-  };
-
-#pragma unroll
-  for (int q = 0; q < 4; ++q) sts128_zero(slab + (lane + 32 * q) * 16);
-  __syncwarp();
-  const ChunkPos first = locate(chunk_ptr, T, FSr, a);
-  in_head = first.j != 0;
-  Pos Q0 = mk(first), Q1 = Q0;
-  adv(Q1);
-  Pos Q2 = Q1;
-  adv(Q2);
-  int G0[NI], G1[NI];
-  load_gidx(Q0, G1);
-  issue(Q0, G1, 0);
-  load_gidx(Q1, G0);
-  int64_t EPa[2], EPb[2], EPc[2];
-  load_ep(Q0, EPa);
-  load_ep(Q1, EPb);
-  uint32_t E0[kWarpEntRegs], E1[kWarpEntRegs];
-  load_ent(EPa, E0);
-  for (;;) {
-    if (step(Q0, Q1, Q2, G0, G1, E0, E1, EPa, EPb, EPc)) break;
-    if (step(Q1, Q2, Q0, G1, G0, E1, E0, EPb, EPc, EPa)) break;
-    if (step(Q2, Q0, Q1, G0, G1, E0, E1, EPc, EPa, EPb)) break;
-    if (step(Q0, Q1, Q2, G1, G0, E1, E0, EPa, EPb, EPc)) break;
-    if (step(Q1, Q2, Q0, G0, G1, E0, E1, EPb, EPc, EPa)) break;
-    if (step(Q2, Q0, Q1, G1, G0, E1, E0, EPc, EPa, EPb)) break;
-  }
-  cp_async_wait<0>();
-}
-
 // ---------------------------------------------------------------- tf32 variant
 // Same schedule and fix-up; fp32 X rows (32-feature slices of 128 B), 16 x 64 fp32 slab,
 // mma.sync m16n8k8 tf32 (X and values RNA-rounded to tf32 by the caller / plan).
@@ -1181,9 +938,6 @@ static int g_warp_swv = 0;     // 0 auto, 4 or 8 (16-B vectors per row slice)
 static int g_warp_paired = 1;
 // 33..48-feature single slice: 1 = skip the empty 16-feature group at compile time (NPR = 3)
 static int g_warp_npr3 = 1;
-// 1 (default): plain bf16 SpMM with 64-feature slices runs the 12-warp, 2-stage k_tile_warp2;
-// 0: the 8-warp, 3-stage k_tile_warp (experiment switch, hcs_set_tile_warp2)
-static int g_warp2 = 1;
 constexpr int64_t kPairMinXBytes = 96ll << 20;
 
 template <int SWV, bool FUSED = false>
@@ -1211,14 +965,6 @@ static int launch_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* 
   // one slice of 33..48 features: the fused (GCN) kernel skips the empty 16-feature group
   // (C3 5.92 -> 5.71 ms); the plain SpMM is faster with the full unrolled schedule now that
   // every lane copies whole padded rows (N = 40/41/48: 1.29 -> 1.21 ms; tools/exp_c3_npr3.sh)
-  if (SWV == 8 && !FUSED && g_warp2) {  // the 12-warp, 2-stage kernel (plain SpMM, 64-feature slices)
-    const int paired2 = (FS > 1 && want && kW2Warps % FS == 0) ? 1 : 0;
-    HCS_CUDA(cudaFuncSetAttribute(k_tile_warp2, cudaFuncAttributeMaxDynamicSharedMemorySize, kW2Smem));
-    k_tile_warp2<<<grid, kW2Warps * 32, kW2Smem, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh,
-                                                        x, ldx, dim, FS, z, ldz, slots, paired2, cnt);
-    HCS_LAUNCH_CHECK("k_tile_warp2");
-    return HCS_OK;
-  }
   auto kern = (FUSED && g_warp_npr3 && SWV == 8 && FS == 1 && dim <= 48 && dim > 32)
                   ? k_tile_warp<SWV, FUSED, (SWV == 8 ? 3 : SWV / 2)>
                   : k_tile_warp<SWV, FUSED>;
@@ -1357,13 +1103,5 @@ extern "C" int hcs_set_tile_pairing(int on) {
 extern "C" int hcs_tile_scratch_floats(int64_t* floats) {
   HCS_REQUIRE(floats != nullptr, HCS_EINVAL, "floats is NULL");
   *floats = hcs::tile_warp_scratch_floats();
-  return HCS_OK;
-}
-
-// Experiment switch: the 12-warp, 2-stage plain tile kernel (1, default) or the 8-warp, 3-stage
-// one (0).  Both deterministic; warp ranges differ (12 vs 8 warps per CTA), so the last bits can.
-extern "C" int hcs_set_tile_warp2(int on) {
-  HCS_REQUIRE(on == 0 || on == 1, HCS_EINVAL, "warp2 switch must be 0 or 1 (got %d)", on);
-  hcs::g_warp2 = on;
   return HCS_OK;
 }

@@ -480,37 +480,3 @@ def test_spmm_graph_replay(cuda_ok, precision):
 
 
 
-
-@pytest.mark.parametrize("dim", [64, 128, 100])
-def test_warp2_kernel_matches_8warp_kernel(cuda_ok, dim):
-    """The 12-warp, 2-stage tile kernel (default for the plain bf16 SpMM with 64-feature slices) ==
-    the 8-warp, 3-stage kernel to fp32 summation order (different warp ranges cut windows at
-    different chunks), == the exact product, run-to-run bitwise, and over row-range parts."""
-    from paper_2412_08902_b200 import _lib
-    from paper_2412_08902_b200.executors import _alloc_z, get_plan, stage_operand
-
-    a = plaw8k_csr()
-    ws = hc.partition(to_hc(a))
-    asg = Assignment.uniform(len(ws), Path.TILE)
-    x = torch.from_numpy(orc.random_dense(a.num_cols, dim, 3)).to(torch.bfloat16).cuda()
-    plan = get_plan(ws, asg, "bf16")
-    xop, _ = stage_operand(x, "bf16", x.device)
-    out = {}
-    try:
-        for on in (1, 0):
-            _lib.call("hcs_set_tile_warp2", on)
-            z, ldz = _alloc_z(ws.num_rows, dim, x.device)
-            plan.run(xop, z, ldz)
-            z2, _ = _alloc_z(ws.num_rows, dim, x.device)
-            plan.run(xop, z2, ldz)
-            zp, _ = _alloc_z(ws.num_rows, dim, x.device)
-            for part in plan.parts(5):
-                plan.run(xop, zp, ldz, part=part)
-            assert torch.equal(z, z2)
-            out[on] = (z[:, :dim].float().cpu().numpy(), zp[:, :dim].float().cpu().numpy())
-    finally:
-        _lib.call("hcs_set_tile_warp2", 1)
-    exact = orc.spmm_exact(a, x.float().cpu().numpy())
-    for v in out[1]:
-        assert orc.max_rel_err(v, exact) <= BF16_TOL
-        assert np.abs(v - out[0][0]).max() <= 1e-5 * np.abs(out[0][0]).max()
