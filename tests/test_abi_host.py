@@ -159,3 +159,44 @@ def test_host_convert_f64_matches_torch_casts():
         assert (o32[:, 77:] == 0).all()
     with pytest.raises(ValueError, match="leading dimensions"):
         _lib.call("hcs_host_convert_f64", a.ctypes.data, 777, 77, 70, out.ctypes.data, 96, _lib.DTYPE_BF16, 1)
+
+
+def test_scalar_piece_list_host_logic():
+    """executors.build_scalar_pieces (the small-plan K3's work list, host side, CPU tensors): every
+    row of the listed windows is covered by consecutive pieces of <= 32 entries in entry order,
+    empty rows get one empty piece, p_first/p_count name each row's piece range, window -> piece
+    pointers are prefix sums, and rows past n_rows (a short last window) are skipped."""
+    import torch
+
+    from paper_2412_08902_b200.executors import build_scalar_pieces
+
+    rng = np.random.default_rng(3)
+    n, wh = 53, 7
+    lens = rng.integers(0, 90, n)
+    lens[[4, 11]] = 0
+    lens[20] = 64  # exactly two pieces
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(lens, out=rp[1:])
+
+    class _Csr:  # the attributes build_scalar_pieces reads
+        row_ptr = torch.from_numpy(rp)
+        num_rows = n
+        device = torch.device("cpu")
+
+    W = -(-n // wh)
+    wl = torch.tensor([1, 3, W - 1, 0], dtype=torch.int32)  # any order; the last window is short
+    p_row, p_k, p_first, p_count, win_piece = build_scalar_pieces(_Csr, wl, wh)
+    p_row, p_k, p_first, p_count = p_row.numpy(), p_k.numpy(), p_first.numpy(), p_count.numpy()
+    assert (p_k[:, 1] - p_k[:, 0] <= 32).all() and (p_k[:, 1] >= p_k[:, 0]).all()
+    q = 0
+    for wi, w in enumerate(wl.tolist()):
+        assert win_piece[wi] == q
+        for r in range(w * wh, min(w * wh + wh, n)):
+            k0, k1 = rp[r], rp[r + 1]
+            cnt = max(1, -(-(k1 - k0) // 32))
+            assert (p_row[q:q + cnt] == r).all()
+            assert (p_first[q:q + cnt] == q).all() and (p_count[q:q + cnt] == cnt).all()
+            assert p_k[q, 0] == k0 and p_k[q + cnt - 1, 1] == k1
+            assert (p_k[q + 1:q + cnt, 0] == p_k[q:q + cnt - 1, 1]).all()  # consecutive
+            q += cnt
+    assert win_piece[len(wl)] == q == p_row.size
