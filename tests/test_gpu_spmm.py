@@ -480,3 +480,28 @@ def test_spmm_graph_replay(cuda_ok, precision):
 
 
 
+
+
+@pytest.mark.parametrize("precision,dim", [("bf16", 520), ("bf16", 1000), ("tf32", 300), ("tf32", 7)])
+def test_scalar_pieces_wide_rows_and_hubs(cuda_ok, precision, dim):
+    """The small-plan K3 piece kernel with feature rows wider than one warp covers (several
+    32-vector chunks per piece: bf16 N > 512, fp32 N > 256) and hub rows split into many pieces:
+    == the exact product within tolerance, bitwise run-to-run, and == spmm_scalar."""
+    rng = np.random.default_rng(11)
+    n, m = 100, 2000
+    rows, cols = [], []
+    for r in range(n):
+        k = 700 if r in (3, 50) else int(rng.integers(0, 40))
+        rows += [r] * k
+        cols += list(rng.choice(m, size=k, replace=False))
+    a = orc.from_coo(n, m, rows, cols, rng.uniform(-1, 1, len(rows)))
+    x = orc.random_dense(m, dim, seed=5)
+    ws = hc.partition(to_hc(a))
+    asg = Assignment.uniform(len(ws), Path.SCALAR)
+    r1 = hc.spmm_hybrid(ws, asg, hc.DenseMatrix(x), precision=precision).z.data
+    r2 = hc.spmm_hybrid(ws, asg, hc.DenseMatrix(x), precision=precision).z.data
+    assert np.array_equal(r1, r2)
+    tol = BF16_TOL if precision == "bf16" else 1e-3
+    assert orc.max_rel_err(r1, orc.spmm_exact(a, x)) <= tol
+    s = hc.spmm_scalar(to_hc(a), hc.DenseMatrix(x), precision=precision).z.data
+    assert np.array_equal(r1, s)
