@@ -131,12 +131,12 @@ int hcs_spmm_scalar_pieces(const int32_t* col_idx, const void* values, int value
  * partial sums.  It must be ZEROED before its first use (the kernels leave the counters zero
  * again), and one workspace must not be shared by launches that can run concurrently. */
 int hcs_tile_scratch_floats(int64_t* floats);
-/* engine 2 row-slice width in 16-B vectors: 0 auto (8 for dim > 32, else 4), 4 or 8 */
+/* tile kernel row-slice width in 16-B vectors: 0 auto (8 for dim > 32, else 4), 4 or 8 */
 int hcs_set_tile_slice(int vectors);
-/* engine 2 fused GCN epilogue, one 33..48-feature slice: 1 (default) = kernel that skips the
+/* tile kernel fused GCN epilogue, one 33..48-feature slice: 1 (default) = kernel that skips the
  * empty 16-feature group, 0 = the full 64-feature kernel (experiment switch) */
 int hcs_set_tile_npr3(int on);
-/* engine 2 with > 1 feature slice: 1 (default) = the FS warps of a group walk the same
+/* tile kernel with > 1 feature slice: 1 (default) = the FS warps of a group walk the same
  * (window, chunk) range, one slice each (plan read once, an X row's slices fetched together);
  * 0 = one warp per contiguous range of (window, slice, chunk); 2 = 1 only when X exceeds 96 MB.
  * All deterministic. */
