@@ -38,22 +38,51 @@ def init_process_group(backend: str = "nccl", device: torch.device | None = None
     dist.init_process_group(backend, **kw)
 
 
-def shard_window_ranges(row_ptr, n_rows: int, world: int, wh: int = 16) -> list[tuple[int, int]]:
-    """Split windows [0, W) into `world` contiguous ranges with ~equal nnz.
+def shard_window_ranges(row_ptr, n_rows: int, world: int, wh: int = 16,
+                        window_cost=None) -> list[tuple[int, int]]:
+    """Split windows [0, W) into `world` contiguous ranges with ~equal nnz -- or, given a per-window
+    cost (window_costs), ~equal cost.
 
-    Boundary r is the first window whose starting entry offset reaches r*nnz/world,
+    Boundary r is the first window whose prefix (entries, or cost) reaches r/world of the total,
     snapped to whole windows; deterministic and identical on every rank."""
-    rp = row_ptr.cpu().numpy() if isinstance(row_ptr, torch.Tensor) else np.asarray(row_ptr)
     W = -(-n_rows // wh)
-    starts = rp[np.minimum(np.arange(W + 1) * wh, n_rows)].astype(np.int64)  # entry offset at each window start
-    nnz = int(starts[-1])
+    if window_cost is not None:
+        c = np.asarray(window_cost, dtype=np.float64)
+        if c.shape != (W,):
+            raise ValueError(f"window_cost must have one entry per window ({W}), got {c.shape}")
+        starts = np.zeros(W + 1, dtype=np.float64)
+        np.cumsum(c, out=starts[1:])
+        total = float(starts[-1])
+        targets = [total * r / world for r in range(1, world)]
+    else:
+        rp = row_ptr.cpu().numpy() if isinstance(row_ptr, torch.Tensor) else np.asarray(row_ptr)
+        starts = rp[np.minimum(np.arange(W + 1) * wh, n_rows)].astype(np.int64)  # entry offset at each window
+        nnz = int(starts[-1])
+        targets = [(nnz * r) // world for r in range(1, world)]
     bounds = [0]
-    for r in range(1, world):
-        target = (nnz * r) // world
+    for target in targets:
         b = int(np.searchsorted(starts, target, side="left"))
         bounds.append(min(max(b, bounds[-1]), W))
     bounds.append(W)
     return [(bounds[i], bounds[i + 1]) for i in range(world)]
+
+
+# Measured B200 cost of the two paths (profiles/r02_shard_compute.txt, DESIGN.md section 5): the tile
+# kernel moves one X row slice per condensed column (C5: ~31 ps per column at N = 128), the scalar
+# kernel one per entry with less reuse (~75 ps per entry); a window also pays a fixed launch share.
+TILE_COL_COST = 1.0
+SCALAR_ENTRY_COST = 2.4
+WINDOW_COST = 4.0
+
+
+def window_costs(windows, codes) -> np.ndarray:
+    """Per-window cost for shard_window_ranges: TILE windows by condensed columns, SCALAR windows
+    by entries (the nnz balance alone left C5's slowest of 8 shards 22 % above the mean)."""
+    ncols = windows.ncols().to(torch.float64)
+    nnz = windows.nnz_per_window().to(torch.float64)
+    tile = torch.as_tensor(np.asarray(codes), device=ncols.device).to(torch.bool)
+    cost = torch.where(tile, TILE_COL_COST * ncols, SCALAR_ENTRY_COST * nnz) + WINDOW_COST * (nnz > 0)
+    return cost.cpu().numpy()
 
 
 def row_slice(a: DeviceCsr, r0: int, r1: int) -> DeviceCsr:
@@ -117,11 +146,12 @@ class Shard:
         self._spans: dict = {}
 
     @classmethod
-    def from_operator(cls, a: DeviceCsr, world: int, rank: int, wh: int = 16, group=None) -> "Shard":
+    def from_operator(cls, a: DeviceCsr, world: int, rank: int, wh: int = 16, group=None,
+                      window_cost=None) -> "Shard":
         rp = a.row_ptr.cpu().numpy() if isinstance(a.row_ptr, torch.Tensor) else np.asarray(a.row_ptr)
         W = -(-a.num_rows // wh)
         starts = rp[np.minimum(np.arange(W + 1) * wh, a.num_rows)]
-        return cls(shard_window_ranges(rp, a.num_rows, world, wh), rank, a.num_rows, wh, group, starts)
+        return cls(shard_window_ranges(rp, a.num_rows, world, wh, window_cost), rank, a.num_rows, wh, group, starts)
 
     def part_spans(self, parts: int) -> list[list[tuple[int, int]]]:
         """Every rank's `parts` exchange parts as LOCAL window bounds [(lw0, lw1)] (contiguous,

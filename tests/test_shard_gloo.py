@@ -160,3 +160,29 @@ def test_sharded_gcn_autograd_matches_single_process():
         assert abs(l - float(loss.detach())) < 1e-12
         np.testing.assert_allclose(g1, tw1.grad.numpy(), rtol=1e-4, atol=1e-9)
         np.testing.assert_allclose(g2, tw2.grad.numpy(), rtol=1e-4, atol=1e-9)
+
+
+def test_shard_ranges_by_window_cost():
+    """shard_window_ranges with a per-window cost: contiguous, covering, ~equal cost (each range's
+    cost within one window's cost of total/world); a cost array of the wrong length is rejected."""
+    import numpy as np
+
+    from paper_2412_08902_b200.shard import shard_window_ranges
+
+    rng = np.random.default_rng(0)
+    n, wh = 1000, 16
+    W = -(-n // wh)
+    lens = rng.integers(0, 50, n)
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(lens, out=rp[1:])
+    cost = rng.uniform(0.0, 10.0, W)
+    for world in (1, 2, 3, 8):
+        r = shard_window_ranges(rp, n, world, wh, window_cost=cost)
+        assert r[0][0] == 0 and r[-1][1] == W and all(r[i][1] == r[i + 1][0] for i in range(world - 1))
+        sums = [cost[a:b].sum() for a, b in r]
+        assert max(sums) - cost.sum() / world <= cost.max() + 1e-9
+    try:
+        shard_window_ranges(rp, n, 2, wh, window_cost=cost[:-1])
+        raise AssertionError("expected ValueError")
+    except ValueError as e:
+        assert "one entry per window" in str(e)

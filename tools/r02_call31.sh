@@ -1,3 +1,3 @@
 #!/bin/bash
 mkdir -p gpurun_out/c31
-timeout 2400 python tools/exp_shard_compute.py > gpurun_out/c31/shard_compute.txt 2>&1
+CFGS=c5,c2 timeout 2400 python tools/exp_shard_compute.py > gpurun_out/c31/shard_compute.txt 2>&1
