@@ -388,6 +388,10 @@ def run_ours(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms, tile_ms = float(t[0]), float(t[1])
             EXTRA["spmm_only_ms"] = float(t[2])
+            if not gloo:
+                from paper_2412_08902_b200.shard import NCCL_RESERVED_SMS
+
+                EXTRA["nccl_reserved_sms"] = int(os.environ.get("HCS_NCCL_RESERVED_SMS", str(NCCL_RESERVED_SMS)))
             EXTRA["exchange"] = f"NCCL all-gather of bf16 rows in {nparts} parts, overlapped" if not gloo else \
                 f"gloo all-gather of bf16 rows in {nparts} parts (shared-GPU test mode)"
         e2e = None

@@ -141,6 +141,9 @@ int hcs_set_tile_npr3(int on);
  * 0 = one warp per contiguous range of (window, slice, chunk); 2 = 1 only when X exceeds 96 MB.
  * All deterministic. */
 int hcs_set_tile_pairing(int on);
+/* CTAs per tile launch: 0 = one per SM (default), n > 0 = min(n, SMs) -- the multi-GPU runs leave
+ * SMs to the NCCL kernels of the overlapped exchange (a tile CTA fills its SM's shared memory) */
+int hcs_set_tile_grid(int ctas);
 int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
                   const int64_t* ent_ptr, const void* ent, int ent_dtype, int64_t n_rows, int32_t wh, const void* x,
                   int x_dtype, int64_t x_rows, int32_t dim, int64_t ldx, float* z, int64_t ldz, void* workspace,

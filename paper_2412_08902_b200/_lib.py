@@ -52,6 +52,7 @@ _SIGS = {
     "hcs_set_tile_npr3": (ctypes.c_int, [ctypes.c_int]),
     "hcs_set_scalar_variant": (ctypes.c_int, [ctypes.c_int]),
     "hcs_set_tile_pairing": (ctypes.c_int, [ctypes.c_int]),
+    "hcs_set_tile_grid": (ctypes.c_int, [ctypes.c_int]),
     "hcs_set_tile_plan_builder": (ctypes.c_int, [ctypes.c_int]),
     "hcs_gcn_tile": (ctypes.c_int, [P, I64, P, P, P, P, ctypes.c_int, I64, I32, P, ctypes.c_int, I64, I32, I64, P,
                                      I64, P, I32, P, I64, P, SZ, P]),

@@ -904,6 +904,12 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
 // paired 32-feature slices for the tf32 SpMM (1 default; hcs_set_tile_pairing(0) turns it off too)
 static int g_warp_paired_tf32 = 1;
 
+// CTAs of a tile launch: one per SM (default), or fewer when SMs are left to concurrent NCCL
+// kernels (the multi-GPU exchange of the previous part runs beside the next part's tiles only if
+// some SMs are free: a tile CTA holds 213 KB of shared memory and 57 K registers of its SM)
+static int g_tile_grid = 0;
+static int tile_grid() { return g_tile_grid > 0 ? std::min(g_tile_grid, num_sms()) : num_sms(); }
+
 // tf32 SpMM (m == nullptr) or fused GCN layer (m = tf32-rounded M [dim x d_out], d_out <= 64; z may
 // be nullptr when no z_cache is wanted).
 int spmm_tile_warp_tf32(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
@@ -911,7 +917,7 @@ int spmm_tile_warp_tf32(const int32_t* tile_list, int64_t n_tile, const int64_t*
                         int dim, float* z, int64_t ldz, float* scratch, int64_t scratch_floats, cudaStream_t st,
                         const float* m = nullptr, int d_out = 0, float* out = nullptr, int64_t ldo = 0) {
   const int FS = (dim + 31) / 32;
-  const int grid = num_sms();
+  const int grid = tile_grid();
   const int64_t nwarps = (int64_t)grid * kTfWarps;
   const bool fused = m != nullptr;
   const int64_t cw = 2 * tile_cnt_words();
@@ -948,7 +954,7 @@ static int launch_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* 
                        int64_t ldo = 0, int64_t x_rows = 0) {
   using C = WarpCfg<SWV>;
   const int FS = (dim + C::kFeat - 1) / C::kFeat;
-  const int grid = num_sms();
+  const int grid = tile_grid();
   const int64_t nwarps = (int64_t)grid * C::kWarps;
   const int64_t cw = 2 * tile_cnt_words();
   const int64_t need = cw + nwarps * 2 * C::kSlot + (FUSED ? nwarps * 2 * kOutSlot : 0);
@@ -1103,5 +1109,13 @@ extern "C" int hcs_set_tile_pairing(int on) {
 extern "C" int hcs_tile_scratch_floats(int64_t* floats) {
   HCS_REQUIRE(floats != nullptr, HCS_EINVAL, "floats is NULL");
   *floats = hcs::tile_warp_scratch_floats();
+  return HCS_OK;
+}
+
+// CTAs per tile launch: 0 = one per SM (default), n > 0 = min(n, SMs).  Results are deterministic
+// for a given grid; different grids cut windows at different chunks (fp32 summation order).
+extern "C" int hcs_set_tile_grid(int ctas) {
+  HCS_REQUIRE(ctas >= 0, HCS_EINVAL, "tile grid must be >= 0 (got %d)", ctas);
+  hcs::g_tile_grid = ctas;
   return HCS_OK;
 }

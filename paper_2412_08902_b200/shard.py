@@ -36,6 +36,25 @@ def init_process_group(backend: str = "nccl", device: torch.device | None = None
     if backend == "nccl" and device is not None:
         kw["device_id"] = device
     dist.init_process_group(backend, **kw)
+    if backend == "nccl":
+        reserve_sms_for_exchange()
+
+
+NCCL_RESERVED_SMS = 16
+
+
+def reserve_sms_for_exchange(reserved: int | None = None) -> int:
+    """Leave `reserved` SMs (HCS_NCCL_RESERVED_SMS, default 16) out of every tile launch, so the NCCL
+    kernels of the overlapped exchange (part k's all-gather under part k+1's SpMM) find free SMs: a
+    tile CTA fills its SM's shared memory and most of its registers.  Returns the tile CTAs per launch."""
+    from . import _lib
+
+    if reserved is None:
+        reserved = int(os.environ.get("HCS_NCCL_RESERVED_SMS", str(NCCL_RESERVED_SMS)))
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    ctas = max(1, sms - max(0, reserved)) if reserved > 0 else 0
+    _lib.call("hcs_set_tile_grid", ctas)
+    return ctas or sms
 
 
 def shard_window_ranges(row_ptr, n_rows: int, world: int, wh: int = 16,

@@ -505,3 +505,30 @@ def test_scalar_pieces_wide_rows_and_hubs(cuda_ok, precision, dim):
     assert orc.max_rel_err(r1, orc.spmm_exact(a, x)) <= tol
     s = hc.spmm_scalar(to_hc(a), hc.DenseMatrix(x), precision=precision).z.data
     assert np.array_equal(r1, s)
+
+
+def test_tile_grid_setter(cuda_ok):
+    """hcs_set_tile_grid (SMs left to the NCCL kernels of the multi-GPU exchange): any CTA count gives
+    the product to fp32 summation order (different warp ranges), deterministic per grid; the
+    fused GCN epilogue too; 0 restores one CTA per SM."""
+    from paper_2412_08902_b200 import _lib, gnn
+
+    a = plaw8k_csr()
+    ws = hc.partition(to_hc(a))
+    asg = hc.classify_windows(hc.default_model(), ws)
+    x = torch.from_numpy(orc.random_dense(a.num_cols, 128, 3)).to(torch.bfloat16).cuda()
+    z0 = hc.spmm_hybrid(ws, asg, x).z.data.clone()
+    layer = gnn.GnnLayer.random(128, 64, seed=1)
+    f0, _, _ = gnn.forward(layer, ws, x.float(), mode="fused", assignment=asg, windows=ws)
+    try:
+        for ctas in (1, 37, 132):
+            _lib.call("hcs_set_tile_grid", ctas)
+            z1 = hc.spmm_hybrid(ws, asg, x).z.data
+            z2 = hc.spmm_hybrid(ws, asg, x).z.data
+            assert torch.equal(z1, z2)
+            assert float((z1 - z0).abs().max() / z0.abs().max()) <= 1e-5
+            f1, _, _ = gnn.forward(layer, ws, x.float(), mode="fused", assignment=asg, windows=ws)
+            assert float((f1.data - f0.data).abs().max() / f0.data.abs().max()) <= 1e-2
+    finally:
+        _lib.call("hcs_set_tile_grid", 0)
+    assert torch.equal(hc.spmm_hybrid(ws, asg, x).z.data, z0)
