@@ -545,9 +545,11 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
       }
       in_head = false;
       if (FUSED) {
-        // oacc += Z_slice (16 x 8*SWV, bf16 RNE) . M[slice rows, :]
-        const uint32_t* wt = reinterpret_cast<const uint32_t*>(wsmem + C::kOffW);
-        const int g8 = lane >> 2, t4 = lane & 3;
+        // oacc += Z_slice (16 x 8*SWV, bf16 RNE) . M[slice rows, :]; the B fragments of two n8 tiles
+        // (W^T rows n, k-halves lo / hi) per ldmatrix.x4 -- lane l addresses row l & 7 of matrix l >> 3
+        // = (n8 pair half (l >> 4), k half ((l >> 3) & 1)); the 272-B row pitch is conflict-free
+        const uint32_t wt_s = smem_u32(wsmem + C::kOffW);
+        const int wrow_n = (lane & 7) + ((lane >> 4) << 3), wrow_k = ((lane >> 3) & 1) * 8;
 #pragma unroll
         for (int j = 0; j < NPR; ++j) {
           uint32_t af[4];
@@ -557,10 +559,12 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
           af[3] = pack_bf16(acc[2 * j + 1][2], acc[2 * j + 1][3]);
           const int kb = (P0.f + fw) * C::kFeat + 16 * j;
 #pragma unroll
-          for (int n8 = 0; n8 < kFusedOutMax / 8; ++n8) {
-            if (n8 * 8 < d_out) {
-              const uint32_t* wrow = wt + ((n8 * 8 + g8) * kFusedLdw + kb) / 2 + t4;
-              hmma_16816(oacc[n8], af, wrow[0], wrow[4]);
+          for (int n16 = 0; n16 < kFusedOutMax / 16; ++n16) {
+            if (n16 * 16 < d_out) {
+              uint32_t wb[4];
+              ldsm_x4(wb, wt_s + (uint32_t)(((n16 * 16 + wrow_n) * kFusedLdw + kb + wrow_k) * 2));
+              hmma_16816(oacc[2 * n16], af, wb[0], wb[1]);
+              if (n16 * 16 + 8 < d_out) hmma_16816(oacc[2 * n16 + 1], af, wb[2], wb[3]);
             }
           }
         }
@@ -576,15 +580,18 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
             if (fw == 1) {
 #pragma unroll
               for (int n8 = 0; n8 < kFusedOutMax / 8; ++n8)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) sts32f(xs + ((n8 * 4 + q) * 32 + lane) * 4, oacc[n8][q]);
+                sts128f(xs + (n8 * 32 + lane) * 16, oacc[n8][0], oacc[n8][1], oacc[n8][2], oacc[n8][3]);
             }
             named_bar_sync(bar, 64);
             if (fw == 0) {
 #pragma unroll
-              for (int n8 = 0; n8 < kFusedOutMax / 8; ++n8)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) oacc[n8][q] += lds32f(xs + ((n8 * 4 + q) * 32 + lane) * 4);
+              for (int n8 = 0; n8 < kFusedOutMax / 8; ++n8) {
+                const float4 v = lds128f(xs + (n8 * 32 + lane) * 16);
+                oacc[n8][0] += v.x;
+                oacc[n8][1] += v.y;
+                oacc[n8][2] += v.z;
+                oacc[n8][3] += v.w;
+              }
             }
             named_bar_sync(bar, 64);
           }
