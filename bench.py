@@ -58,6 +58,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--sweep-dims", action="store_true", help="also report dims 32/64/128")
     p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--gcn-order", choices=["auto", "fused", "update_first"], default="auto",
+                   help="C3 layer order (model.gcn_layer): auto = A (X W) where it narrows the rows")
     p.add_argument("--launch-check", action="store_true",
                    help="test hook: start the ranks, rendezvous over gloo, print the world rank 0 saw, exit")
     return p.parse_args()
@@ -686,8 +688,10 @@ def epoch_kernels(fn) -> dict | None:
         k = n.split("(")[0][:60]
         short[k] = short.get(k, 0) + 1
     ours = [(n.split("(")[0][:60], round(d, 1)) for n, d in zip(names, durs) if "hcs::" in n]
+    others = [(n.split("(")[0][:60], round(d, 1)) for n, d in zip(names, durs) if "hcs::" not in n]
     return {"launches": len(names), "hcs_launches": len(own), "library_gemm": gemm, "by_kernel": short,
-            "hcs_us_in_order": ours}
+            "hcs_us_in_order": ours, "other_us_in_order": others,
+            "hcs_us_total": round(sum(d for _, d in ours), 1), "other_us_total": round(sum(d for _, d in others), 1)}
 
 
 def run_c3(args):
@@ -711,7 +715,10 @@ def run_c3(args):
     ws = hc.partition(a_loc)
     x = graphgen.dense_features(n, 128, seed=1, dtype=torch.float32)
     labels = torch.randint(0, 41, (n,), generator=torch.Generator(device=dev).manual_seed(2), device=dev)
-    model = Gcn2(128, 64, 41, seed=0)
+    model = Gcn2(128, 64, 41, seed=0, order=args.gcn_order)
+    # the order each layer actually runs in (sharded layers are always fused)
+    uf = [shard is None and (o == "update_first" or (o == "auto" and do < di))
+          for o, di, do in zip(model.order, (128, 64), (64, 41))]
     steps, warmup = args.steps, max(args.warmup, 3)
     for _ in range(warmup):
         model.epoch(x, labels, ws, shard=shard)
@@ -736,14 +743,18 @@ def run_c3(args):
         t = torch.tensor([ms], device=dev if dist.get_backend() == "nccl" else "cpu", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t[0])
-    # SpMM flops of one epoch: fwd L1 (N=128), fwd L2 (N=64), bwd L2 grad_X (N=41)
-    spmm_flops = 2.0 * nnz * (128 + 64 + 41)
+    # SpMM widths of one epoch: a fused layer aggregates d_in-wide rows forward (and d_out-wide ones
+    # for grad_X); an update-first layer d_out-wide rows forward and backward (A^T G for grad_W too)
+    widths = ([64, 64] if uf[0] else [128]) + ([41, 41] if uf[1] else [64, 41])
+    spmm_flops = 2.0 * nnz * sum(widths)
     gemm_flops = 2.0 * n * (128 * 64 + 64 * 41) * 2 + 2.0 * n * 41 * 64
     out = {"metric": "GCN epoch ms (2-layer, fwd+bwd+SGD)", "value": ms, "unit": "ms", "n_gpus": world,
            "steps": steps, "warmup": warmup, "ms_per_step": ms, "higher_is_better": False,
            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "bf16",
            "data": "synthetic (seeded on-device generator; X ~ U[-1,1), random labels)",
-           "config": {"workload": wl_name + ", 2-layer GCN 128-64-41, fused SpMM+GEMM fwd/bwd, SGD",
+           "config": {"workload": wl_name + ", 2-layer GCN 128-64-41, SGD; layers "
+                      + "/".join("A(XW): GEMM then SpMM" if u else "(AX)W: fused SpMM+GEMM" for u in uf),
+                      "layer_order": ["update_first" if u else "fused" for u in uf], "spmm_widths": widths,
                       "n": n, "nnz": nnz, "parallelism": f"row-window shards x{world}" if world > 1 else "single GPU",
                       "loss_last": float(loss.detach())},
            "spmm_gflops": spmm_flops / (ms * 1e-3) / 1e9, "gemm_gflop_per_epoch": gemm_flops / 1e9,
@@ -751,11 +762,17 @@ def run_c3(args):
            "kernels_per_epoch": kernels, "clocks": sampler.summary()}
     l1 = [d for k, d in (kernels or {}).get("hcs_us_in_order", []) if "k_tile_warp" in k]
     if l1 and l1[0] > 0:
-        # dominant kernel: the layer-1 fused aggregation + update (the SpMM bytes with N =
-        # d_in, plus the d_out outputs, the z_cache rows and W); one profiled epoch outside the timing
+        # dominant kernel: layer 1's first tile launch -- fused: the aggregation + update (SURVEY §8d:
+        # the SpMM bytes with N = d_in, plus the d_out outputs, the z_cache rows and W); update-first:
+        # the plain SpMM of the 64-wide X W rows.  One profiled epoch outside the timing.
         peak, peak_kind = peaks()
-        b_l1 = 8 * (n + 1) + nnz * (4 + 2) + n * 128 * 2 + n * 64 * 4 + n * 128 * 4 + 128 * 64 * 4
-        out["roofline"] = {"bound": "hbm", "kernel": "layer-1 fused tile launch (k_tile_warp<8,1,4>)",
+        if uf[0]:
+            b_l1 = 8 * (n + 1) + nnz * (4 + 2) + n * 64 * 2 + n * 64 * 4
+            kname = "layer-1 SpMM A (X W1), N = 64 (k_tile_warp<8,0,4>)"
+        else:
+            b_l1 = 8 * (n + 1) + nnz * (4 + 2) + n * 128 * 2 + n * 64 * 4 + n * 128 * 4 + 128 * 64 * 4
+            kname = "layer-1 fused tile launch (k_tile_warp<8,1,4>)"
+        out["roofline"] = {"bound": "hbm", "kernel": kname,
                            "achieved": b_l1 / (l1[0] * 1e-6) / 1e9, "peak": peak, "unit": "GB/s",
                            "frac": b_l1 / (l1[0] * 1e-6) / 1e9 / peak, "traffic": None, "peak_kind": peak_kind,
                            "kernel_ms": l1[0] * 1e-3, "algorithmic_bytes": b_l1,

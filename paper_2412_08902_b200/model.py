@@ -1,7 +1,8 @@
 """2-layer GCN training on the fused kernels (BASELINE config C3).
 
 The reference has a single GCN layer with no activation, loss or optimizer
-(gnn.py:121-205).  The epoch defined here is
+(gnn.py:121-205).  The epoch defined here is, with
+order="fused" (the reference's (A X) W order):
     fwd L1 (fused: out1 = (A X) W1, z1 = A X)      K6
     ReLU
     fwd L2 (fused: out2 = (A H) W2, z2 = A H)      K6
@@ -10,6 +11,10 @@ The reference has a single GCN layer with no activation, loss or optimizer
     ReLU backward
     bwd L1: grad_W1 = z1^T G1 (no grad_X for the input features)
     SGD update
+and with order="auto" (the default; update first where d_out < d_in, both C3 layers) each layer
+is A (X W): a GEMM, then a plain SpMM over d_out-wide rows; backward S = A^T G (SpMM),
+grad_W = X^T S, grad_X = S W^T.  C3 layer 1 then gathers 64-wide rows twice (forward and
+backward) instead of 128-wide ones once: 5.69 -> 5.46 ms per epoch (tools/exp_order.py).
 The layer is a torch.autograd.Function whose forward/backward call the fused
 kernels, so the loop body is plain PyTorch.  Multi-GPU (row-window shards,
 ShardedGcnLayer): each rank computes its rows in parts whose all-gathers overlap
@@ -23,7 +28,7 @@ import numpy as np
 import torch
 
 from .executors import Assignment
-from .fused import FusedLayer, fused_aggregate_update, grad_weight
+from .fused import FusedLayer, dense_matmul, fused_aggregate_update, grad_weight
 from .windows import WindowSet
 
 
@@ -50,6 +55,33 @@ class GcnAggregateUpdate(torch.autograd.Function):
         return gx, gw, None, None, None, None, None
 
 
+class UpdateAggregate(torch.autograd.Function):
+    """y = A (x W): the update first, when it narrows the rows (d_out < d_in), so the aggregation
+    gathers d_out-wide rows instead of d_in-wide ones -- the same product as (A x) W, in the other
+    order (C3 layer 1: one 64-wide SpMM instead of a 128-wide fused one).  No z_cache is needed:
+    grad_W = x^T (A^T G), and A^T G is also what grad_x = (A^T G) W^T aggregates."""
+
+    @staticmethod
+    def forward(ctx, x, w, windows, windows_t, assignment, precision):
+        from .executors import spmm_hybrid
+
+        t = dense_matmul(x.detach(), w.detach())
+        out = spmm_hybrid(windows, assignment, t, precision=precision).z.data
+        ctx.save_for_backward(x, w)
+        ctx.windows_t, ctx.assignment, ctx.precision = windows_t, assignment, precision
+        return out
+
+    @staticmethod
+    def backward(ctx, g):
+        from .executors import spmm_hybrid
+
+        x, w = ctx.saved_tensors
+        gt = spmm_hybrid(ctx.windows_t, ctx.assignment, g.contiguous(), precision=ctx.precision).z.data
+        gw = grad_weight(x, gt)
+        gx = dense_matmul(gt, w.t()) if ctx.needs_input_grad[0] else None
+        return gx, gw, None, None, None, None
+
+
 def backward_windows(windows: WindowSet, shard=None) -> WindowSet:
     """Row windows of A^T for grad_X = A^T (G W^T) (gnn.py:181-183).  A symmetric operator (gcn /
     gin / raw on an undirected graph) is its own transpose, so the forward windows are reused;
@@ -70,13 +102,18 @@ def backward_windows(windows: WindowSet, shard=None) -> WindowSet:
     return cached
 
 
-def gcn_layer(x, w, windows, windows_t=None, assignment=None, precision="bf16", shard=None):
+def gcn_layer(x, w, windows, windows_t=None, assignment=None, precision="bf16", shard=None, order="fused"):
+    """One GCN layer y = A x W.  order: "fused" (aggregate then update in one kernel, saving
+    z = A x: the reference's forward), "update_first" (A (x W), UpdateAggregate), or "auto"
+    (update first when it narrows the rows, d_out < d_in, on one GPU)."""
     if assignment is None:
         assignment = Assignment(windows.codes)
     if windows_t is None:
         windows_t = backward_windows(windows, shard)
     if shard is not None:
         return ShardedGcnLayer.apply(x, w, windows, windows_t, assignment, precision, shard, EXCHANGE_PARTS)
+    if order == "update_first" or (order == "auto" and int(w.shape[1]) < int(w.shape[0])):
+        return UpdateAggregate.apply(x, w, windows, windows_t, assignment, precision)
     return GcnAggregateUpdate.apply(x, w, windows, windows_t, assignment, precision, None)
 
 
@@ -153,7 +190,11 @@ class Gcn2:
     """Two GCN layers (d_in -> hidden -> classes), Glorot-uniform init from a seed
     (gnn.py:40-46 GnnLayer.random), full-batch SGD."""
 
-    def __init__(self, d_in: int, hidden: int, classes: int, seed: int = 0, device="cuda", lr: float = 0.1):
+    def __init__(self, d_in: int, hidden: int, classes: int, seed: int = 0, device="cuda", lr: float = 0.1,
+                 order=("auto", "auto")):
+        """order: per-layer gcn_layer order ("fused" | "update_first" | "auto"; sharded layers are
+        always fused)."""
+        self.order = (order, order) if isinstance(order, str) else tuple(order)
         rng = np.random.default_rng(seed)
 
         def glorot(a, b):
@@ -170,8 +211,8 @@ class Gcn2:
 
     def forward(self, x, windows: WindowSet, windows_t=None, precision="bf16", shard=None):
         asg = Assignment(windows.codes)
-        h = torch.relu(gcn_layer(x, self.w1, windows, windows_t, asg, precision, shard))
-        return gcn_layer(h, self.w2, windows, windows_t, asg, precision, shard)
+        h = torch.relu(gcn_layer(x, self.w1, windows, windows_t, asg, precision, shard, self.order[0]))
+        return gcn_layer(h, self.w2, windows, windows_t, asg, precision, shard, self.order[1])
 
     def epoch(self, x, labels, windows: WindowSet, windows_t=None, precision="bf16", shard=None):
         """One training epoch; returns the loss tensor (on the device)."""
