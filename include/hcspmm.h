@@ -182,6 +182,24 @@ int hcs_grad_w(const float* a, int64_t lda, const float* b, int64_t ldb, int64_t
                int64_t ldc, void* workspace, size_t ws_bytes, void* stream);
 int hcs_gemm(const float* a, int64_t lda, const float* b, int64_t ldb, int64_t K, int32_t M, int32_t N, float* c,
              int64_t ldc, void* stream);
+/* hcs_gemm with a bf16 destination that is the next aggregation's operand (model.Gcn2's
+ * update-first layers, A (X W)): C[K x n_store] = bf16_rne((A B) * 1[mask > 0]) for columns < N
+ * (mask: optional fp32 [K x N], ld_mask -- the ReLU backward, grad * 1[H > 0]), zeros for columns
+ * [N, n_store) (rows padded to whole gather slices).  n_store, ldc even. */
+int hcs_gemm_bf16(const float* a, int64_t lda, const float* b, int64_t ldb, int64_t K, int32_t M, int32_t N, void* c,
+                  int64_t ldc, int32_t n_store, const float* mask, int64_t ld_mask, void* stream);
+
+/* ---------------------------------------------------------------- training-epoch loss (C3)
+ * Not in the reference (its GCN has no loss or optimizer): the C3 epoch's softmax
+ * cross-entropy.  *loss = -mean_i log_softmax(logits_i)[labels_i] (device float, reduced in a
+ * fixed order); grad [rows x n_store] (ld_grad; bf16 or f32) = grad_scale * (softmax(logits_i) -
+ * onehot(labels_i)) for columns < classes, zeros up to n_store.  labels: int64 [rows]; a label
+ * outside [0, classes) makes the loss NaN.  workspace: hcs_softmax_xent_workspace_bytes(rows),
+ * zero-filled before first use (left zeroed). */
+int hcs_softmax_xent_workspace_bytes(int64_t rows, size_t* bytes);
+int hcs_softmax_xent(const float* logits, int64_t ld, int64_t rows, int32_t classes, const int64_t* labels,
+                     float grad_scale, float* loss, void* grad, int grad_dtype, int64_t ld_grad, int32_t n_store,
+                     void* workspace, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------- K8 LOA
  * layout.py:186-263 build_windows_optimized (paper Alg. 6): greedy 16-vertex groups

@@ -61,6 +61,10 @@ _SIGS = {
     "hcs_grad_w_workspace_bytes": (ctypes.c_int, [I64, I32, I32, ctypes.POINTER(SZ)]),
     "hcs_grad_w": (ctypes.c_int, [P, I64, P, I64, I64, I32, I32, P, I64, P, SZ, P]),
     "hcs_gemm": (ctypes.c_int, [P, I64, P, I64, I64, I32, I32, P, I64, P]),
+    "hcs_gemm_bf16": (ctypes.c_int, [P, I64, P, I64, I64, I32, I32, P, I64, I32, P, I64, P]),
+    "hcs_softmax_xent_workspace_bytes": (ctypes.c_int, [I64, ctypes.POINTER(SZ)]),
+    "hcs_softmax_xent": (ctypes.c_int, [P, I64, I64, I32, P, ctypes.c_float, P, P, ctypes.c_int, I64, I32, P, SZ,
+                                        P]),
     "hcs_loa_workspace_bytes": (ctypes.c_int, [I64, ctypes.POINTER(SZ)]),
     "hcs_loa": (ctypes.c_int, [P, P, I64, I32, I32, P, P, P, P, P, SZ, P]),
     "hcs_convert": (ctypes.c_int, [P, P, I64, ctypes.c_int, P]),

@@ -132,11 +132,15 @@ __global__ void k_gradw_reduce(const float* __restrict__ part, int S, int mtiles
   c[(int64_t)m * ldc + n] = v;
 }
 
-// C = A B, A [K x M] (lda), B [M x N] (ldb), C [K x N] (ldc).  grid (ceil(K/64), ceil(N/64)).
-template <bool VA, bool VB>
+// C = A B, A [K x M] (lda), B [M x N] (ldb), C [K x N] (ldc).  grid (ceil(K/64), ceil(n_store/64)).
+// BF16OUT: C is bf16 (RNE), multiplied by 1[mask > 0] where mask != nullptr (the ReLU backward of
+// the next aggregation's operand), and columns [N, n_store) are written as zeros (slice padding).
+template <bool VA, bool VB, bool BF16OUT = false>
 __global__ void __launch_bounds__(kDenseThreads) k_gemm_tall(const float* __restrict__ a, int64_t lda,
                                                               const float* __restrict__ b, int64_t ldb, int64_t K,
-                                                              int M, int N, float* __restrict__ c, int64_t ldc) {
+                                                              int M, int N, void* __restrict__ cv, int64_t ldc,
+                                                              const float* __restrict__ mask, int64_t ldm,
+                                                              int n_store) {
   __shared__ __align__(16) float As[2][64][kLdA];
   __shared__ __align__(16) float Bs[2][kKT][kLdT];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -186,6 +190,28 @@ __global__ void __launch_bounds__(kDenseThreads) k_gemm_tall(const float* __rest
     __syncthreads();
     stage ^= 1;
   }
+  if (BF16OUT) {
+    __nv_bfloat16* c = static_cast<__nv_bfloat16*>(cv);
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      const int col = n0 + nt * 8 + 2 * t;  // even; ldc even, n_store even
+      if (col >= n_store) continue;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t r = r0 + warp * 16 + g + 8 * h;
+        if (r >= K) continue;
+        float v0 = col < N ? acc[nt][2 * h] : 0.f, v1 = col + 1 < N ? acc[nt][2 * h + 1] : 0.f;
+        if (mask != nullptr) {
+          const float* mp = mask + r * ldm + col;
+          if (col < N && !(__ldg(mp) > 0.f)) v0 = 0.f;
+          if (col + 1 < N && !(__ldg(mp + 1) > 0.f)) v1 = 0.f;
+        }
+        *reinterpret_cast<__nv_bfloat162*>(c + r * ldc + col) = __floats2bfloat162_rn(v0, v1);
+      }
+    }
+    return;
+  }
+  float* c = static_cast<float*>(cv);
 #pragma unroll
   for (int nt = 0; nt < 8; ++nt) {
     const int col = n0 + nt * 8 + 2 * t;
@@ -259,7 +285,33 @@ extern "C" int hcs_gemm(const float* a, int64_t lda, const float* b, int64_t ldb
   const bool va = vec_ok(a, lda), vb = vec_ok(b, ldb);
   auto kern = va ? (vb ? k_gemm_tall<true, true> : k_gemm_tall<true, false>)
                  : (vb ? k_gemm_tall<false, true> : k_gemm_tall<false, false>);
-  kern<<<dim3((unsigned)bx, (N + 63) / 64), kDenseThreads, 0, as_stream(stream)>>>(a, lda, b, ldb, K, M, N, c, ldc);
+  kern<<<dim3((unsigned)bx, (N + 63) / 64), kDenseThreads, 0, as_stream(stream)>>>(a, lda, b, ldb, K, M, N, c, ldc,
+                                                                                  nullptr, 0, N);
+  HCS_LAUNCH_CHECK("k_gemm_tall");
+  return HCS_OK;
+}
+
+// hcs_gemm with a bf16 destination: C[K x n_store] = bf16((A B) * 1[mask > 0]) for columns < N,
+// zeros for columns [N, n_store) -- the next aggregation's operand, staged (padded to whole gather
+// slices) by the GEMM itself instead of a conversion pass.
+extern "C" int hcs_gemm_bf16(const float* a, int64_t lda, const float* b, int64_t ldb, int64_t K, int32_t M,
+                             int32_t N, void* c, int64_t ldc, int32_t n_store, const float* mask, int64_t ld_mask,
+                             void* stream) {
+  HCS_REQUIRE(K >= 0 && M > 0 && N > 0 && n_store >= N && ldc >= n_store, HCS_EINVAL,
+              "bad GEMM shape (K %lld, M %d, N %d, n_store %d, ldc %lld)", (long long)K, M, N, n_store, (long long)ldc);
+  HCS_REQUIRE(n_store % 2 == 0 && ldc % 2 == 0 && ((uintptr_t)c & 3) == 0, HCS_EINVAL,
+              "bf16 GEMM output needs an even n_store and ldc and a 4-byte aligned base");
+  HCS_REQUIRE(lda >= M && ldb >= N, HCS_EINVAL, "GEMM operands need lda >= M, ldb >= N");
+  HCS_REQUIRE(mask == nullptr || ld_mask >= N, HCS_EINVAL, "mask needs ld_mask >= N");
+  HCS_REQUIRE(((uintptr_t)a & 3) == 0 && ((uintptr_t)b & 3) == 0, HCS_EINVAL, "GEMM operands must be fp32-aligned");
+  if (K == 0) return HCS_OK;
+  const int64_t bx = (K + 63) / 64;
+  HCS_REQUIRE(bx < (1ll << 31), HCS_EINVAL, "too many rows");
+  const bool va = vec_ok(a, lda), vb = vec_ok(b, ldb);
+  auto kern = va ? (vb ? k_gemm_tall<true, true, true> : k_gemm_tall<true, false, true>)
+                 : (vb ? k_gemm_tall<false, true, true> : k_gemm_tall<false, false, true>);
+  kern<<<dim3((unsigned)bx, (n_store + 63) / 64), kDenseThreads, 0, as_stream(stream)>>>(a, lda, b, ldb, K, M, N, c,
+                                                                                        ldc, mask, ld_mask, n_store);
   HCS_LAUNCH_CHECK("k_gemm_tall");
   return HCS_OK;
 }

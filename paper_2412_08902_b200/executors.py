@@ -573,6 +573,26 @@ def spmm_hybrid(windows, assignment: Assignment, x, precision: str = "bf16", thr
     return _wrap_result(z, xop.dim, _host_kind(x) if was_host else False, ExecStats(**plan.stats.as_dict()))
 
 
+def spmm_staged(windows, assignment: Assignment, xop: DeviceOperand, precision: str = "bf16") -> torch.Tensor:
+    """spmm_hybrid for an operand already staged on the device in the compute dtype (rows padded
+    to whole gather slices, e.g. written by hcs_gemm_bf16 or hcs_softmax_xent): returns the fp32
+    device product as a [rows, dim] view (model.Gcn2's explicit epoch)."""
+    from .windows import as_windowset
+
+    precision = _resolve_precision(precision)
+    want = _lib.DTYPE_BF16 if precision == "bf16" else _lib.DTYPE_F32
+    if xop.dtype_code != want:
+        raise ValueError(f"operand dtype code {xop.dtype_code} does not match precision {precision!r}")
+    if len(assignment) != len(windows):
+        raise ValueError(f"assignment covers {len(assignment)} windows, expected {len(windows)}")
+    ws = as_windowset(windows)
+    _check_window_bounds(ws, xop.rows)
+    plan = get_plan(ws, assignment, precision)
+    z, ldz = _alloc_z(ws.num_rows, xop.dim, ws.csr.device)
+    plan.run(xop, z, ldz)
+    return z[:, :xop.dim]
+
+
 HOST_PIPELINE_MIN_WINDOWS = 4096
 HOST_PIPELINE_PARTS = 8  # measured on C2 (tools/exp_e2e_parts.py): 4 -> 4.36 ms, 8 -> 4.18, 16 -> 4.18, 32 -> 4.48
 _COPY_STREAMS: dict = {}

@@ -73,6 +73,69 @@ def dense_matmul(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = No
     return out
 
 
+def slice_padded(dim: int) -> int:
+    """Row length of a bf16 operand padded to whole gather slices (executors.stage_operand)."""
+    from .executors import PAD_TO_SLICE, _round_up
+
+    s = 32 if dim <= 32 else 64
+    return _round_up(dim, s) if PAD_TO_SLICE else _round_up(dim, 8)
+
+
+def dense_matmul_bf16(a: torch.Tensor, b: torch.Tensor, mask: torch.Tensor | None = None):
+    """The next aggregation's operand straight from the GEMM (hcs_gemm_bf16): a DeviceOperand of
+    bf16(a @ b * 1[mask > 0]) with rows padded to whole gather slices."""
+    from .executors import DeviceOperand
+
+    dev = a.device
+    a, b = _f32_2d(a, dev), _f32_2d(b, dev)
+    K, M, N = int(a.shape[0]), int(a.shape[1]), int(b.shape[1])
+    if int(b.shape[0]) != M:
+        raise ValueError(f"inner dimensions differ: {M} vs {int(b.shape[0])}")
+    ld = slice_padded(N)
+    out = torch.empty((K, ld), dtype=torch.bfloat16, device=dev)
+    mp, ldm = 0, 0
+    if mask is not None:
+        if tuple(mask.shape) != (K, N) or mask.dtype != torch.float32 or mask.stride(1) != 1:
+            raise ValueError(f"mask must be float32 ({K}, {N}) with unit column stride")
+        mp, ldm = mask.data_ptr(), mask.stride(0)
+    if K:
+        _lib.call("hcs_gemm_bf16", a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), K, M, N, out.data_ptr(), ld,
+                  ld, mp, ldm, _lib.stream())
+    return DeviceOperand(out, N, ld, _lib.DTYPE_BF16)
+
+
+_XENT_WS: dict = {}
+
+
+def softmax_xent(logits: torch.Tensor, labels: torch.Tensor, grad_scale: float | None = None):
+    """(loss, grad operand): loss = -mean log_softmax(logits)[labels] (device scalar), grad =
+    grad_scale * (softmax - onehot) (default scale 1/rows: d loss / d logits) as a bf16
+    DeviceOperand padded to whole gather slices, ready for the backward aggregation (hcs_softmax_xent)."""
+    from .executors import DeviceOperand
+
+    dev = logits.device
+    if logits.dtype != torch.float32 or logits.dim() != 2 or logits.stride(1) != 1:
+        raise ValueError("logits must be a float32 matrix with unit column stride")
+    rows, classes = int(logits.shape[0]), int(logits.shape[1])
+    labels = labels.to(device=dev, dtype=torch.int64).contiguous()
+    if labels.numel() != rows:
+        raise ValueError(f"{labels.numel()} labels for {rows} rows")
+    ld = slice_padded(classes)
+    grad = torch.empty((rows, ld), dtype=torch.bfloat16, device=dev)
+    loss = torch.empty((), dtype=torch.float32, device=dev)
+    wsb = _lib.ctypes.c_size_t(0)
+    _lib.check(_lib.lib().hcs_softmax_xent_workspace_bytes(rows, _lib.ctypes.byref(wsb)))
+    key = (dev, _lib.stream())  # one workspace (counter + partials) per stream
+    ws = _XENT_WS.get(key)
+    if ws is None or ws.numel() * 4 < wsb.value:
+        ws = _XENT_WS[key] = torch.zeros(max(int(wsb.value) // 4, 64), dtype=torch.float32, device=dev)
+    scale = (1.0 / rows) if grad_scale is None else float(grad_scale)
+    _lib.call("hcs_softmax_xent", logits.data_ptr(), logits.stride(0), rows, classes, labels.data_ptr(), scale,
+              loss.data_ptr(), grad.data_ptr(), _lib.DTYPE_BF16, ld, ld, ws.data_ptr(), ws.numel() * 4,
+              _lib.stream())
+    return loss, DeviceOperand(grad, classes, ld, _lib.DTYPE_BF16)
+
+
 class FusedLayer:
     """One GCN aggregation + update over a WindowSet: out = (A X) M (and z = A X), staged once and
     launched for all windows or for row-window parts (plan.parts / window bounds), so a sharded

@@ -113,10 +113,10 @@ def test_two_ranks_match_one(cuda_ok):
     z1 = hc.spmm_hybrid(ws, asg, x).z.data.cpu().numpy()
     xf = torch.from_numpy(np.random.default_rng(2).uniform(-1, 1, (n, 128))).float().cuda()
     labels = torch.from_numpy(np.random.default_rng(3).integers(0, 41, n)).cuda()
-    m = Gcn2(128, 64, 41, seed=0)
+    m = Gcn2(128, 64, 41, seed=0, order="fused")  # sharded layers run fused: the same order
     w1, w2 = m.w1.detach().clone(), m.w2.detach().clone()
     with torch.no_grad():
-        mask1 = (gcn_layer(xf, w1, ws) > 0).cpu().numpy()
+        mask1 = (gcn_layer(xf, w1, ws, order=m.order[0]) > 0).cpu().numpy()  # the order m.epoch runs
     loss1 = float(m.epoch(xf, labels, ws).detach())
     g1, g2 = m.w1.grad.cpu().numpy(), m.w2.grad.cpu().numpy()
     ctx = mp.get_context("spawn")
