@@ -81,6 +81,11 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
 // byte offset of fp32 element (row r, column c) in a 16 x 64 fp32 slab (256-B rows,
 // 16-B chunks XOR-swizzled by the row's low 3 bits: conflict-free ldmatrix.x4 of tf32 A tiles)
 __host__ __device__ __forceinline__ uint32_t tf32_slab_off(uint32_t r, uint32_t c) {

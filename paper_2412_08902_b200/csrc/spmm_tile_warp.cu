@@ -236,6 +236,29 @@ __device__ __forceinline__ void store_slice(float* __restrict__ z, int64_t ldz, 
   }
 }
 
+// tf32 kernel's slice (permuted n8 tiles): lane (g, t) holds features 8t..8t+7 of rows g, g+8 as
+// acc[0..3][0], acc[0..3][1] (row g) and acc[0..3][2], acc[0..3][3] (row g+8)
+__device__ __forceinline__ void store_slice_tf32p(float* __restrict__ z, int64_t ldz, int64_t rs, int rows, int dim,
+                                                  int f, const float (&acc)[4][4], int lane) {
+  const int r0 = lane >> 2, c0 = f * 32 + (lane & 3) * 8;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int r = r0 + 8 * h;
+    if (r >= rows) continue;
+    float* zp = z + (rs + r) * ldz + c0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {  // features c0 + 2q, c0 + 2q + 1
+      const int j0 = 2 * q, j1 = 2 * q + 1;
+      const float v0 = acc[j0 & 3][2 * h + (j0 >> 2)], v1 = acc[j1 & 3][2 * h + (j1 >> 2)];
+      if (c0 + j1 < dim) {
+        *reinterpret_cast<float2*>(zp + j0) = make_float2(v0, v1);
+      } else if (c0 + j0 < dim) {
+        zp[j0] = v0;
+      }
+    }
+  }
+}
+
 constexpr int kFusedOutMax = 64;        // d_out of the warp kernel's fused epilogue
 constexpr int kFusedLdw = 128 + 8;      // bf16 per M^T row (d_in <= 128)
 constexpr int kOutSlot = 16 * kFusedOutMax;
@@ -259,7 +282,7 @@ __device__ __forceinline__ void store_out(float* __restrict__ out, int64_t ldo, 
 // parameters (rare path), so none of it stays live across the gather/MMA loop (the 32-feature
 // kernel runs at its 128-register cap).  unit = (window chunk base, slice f) of a sequence of
 // FSr = (paired ? 1 : FS) slices per window; warp of group k = k * FSm + fw (FSm = paired ? FS : 1).
-template <int SWV, int SLOT>
+template <int SWV, int SLOT, bool PERM = false>
 __device__ __forceinline__ void finish_split_z(const int64_t* __restrict__ chunk_ptr, int64_t T, int FS, int paired,
                                                int warps_per_cta, unsigned* __restrict__ cnt,
                                                const float* __restrict__ slots, float* __restrict__ z, int64_t ldz,
@@ -279,7 +302,11 @@ __device__ __forceinline__ void finish_split_z(const int64_t* __restrict__ chunk
   if (!split_arrive(cnt + g_o * FSm + fw, us, us + nj, a, b, lane)) return;
   float acc[SWV][4];
   split_reduce<SWV, SLOT>(slots, total, ng, g_o, FSm, fw, us + nj, acc, lane);
-  store_slice<SWV>(z, ldz, rs, rows, dim, f + fw, acc, lane);
+  if constexpr (PERM) {
+    store_slice_tf32p(z, ldz, rs, rows, dim, f + fw, acc, lane);
+  } else {
+    store_slice<SWV>(z, ldz, rs, rows, dim, f + fw, acc, lane);
+  }
 }
 
 // the same for a window's fused out rows (window = positions [FSr (base - c0), + FSr nj) of the
@@ -656,7 +683,8 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
 // ---------------------------------------------------------------- tf32 variant
 // Same schedule and fix-up; fp32 X rows (32-feature slices of 128 B), 16 x 64 fp32 slab,
 // mma.sync m16n8k8 tf32 (X and values RNA-rounded to tf32 by the caller / plan).
-// B fragments are read with conflict-free 32-bit loads (16-B chunk XOR 2*(row&3)).
+// B fragments: n8 tile nt's column g is feature 4g + nt, so a lane's words for all four tiles
+// are one conflict-free 128-bit load per k row (16-B chunk XOR 2*(row&3)); Z is stored unpermuted.
 constexpr int kTfWarps = 8;
 constexpr int kTfRow = 128;
 constexpr int kTfStage = 64 * kTfRow;
@@ -817,14 +845,15 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
         uint32_t af[4];
         const int ch = 2 * ks + ach;
         ldsm_x4(af, slab + arow * 256 + ((((ch & 8) | ((ch ^ arow) & 7))) << 4));
+        // n8 tile nt, column g <-> feature 4g + nt: a lane's B words of all four tiles are one
+        // 16-B vector per k row (2 x LDS.128 per k step instead of 8 x LDS.32)
         const int k0 = ks * 8 + t4, k1 = k0 + 4;
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt) {
-          const int n = nt * 8 + g8;
-          const uint32_t b0 = lds32(st + k0 * kTfRow + (swz_tf(k0, n >> 2) << 4) + (n & 3) * 4);
-          const uint32_t b1 = lds32(st + k1 * kTfRow + (swz_tf(k1, n >> 2) << 4) + (n & 3) * 4);
-          mma_tf32_1688(acc[nt], af, b0, b1);
-        }
+        const uint4 v0 = lds128(st + k0 * kTfRow + (swz_tf(k0, g8) << 4));
+        const uint4 v1 = lds128(st + k1 * kTfRow + (swz_tf(k1, g8) << 4));
+        mma_tf32_1688(acc[0], af, v0.x, v1.x);
+        mma_tf32_1688(acc[1], af, v0.y, v1.y);
+        mma_tf32_1688(acc[2], af, v0.z, v1.z);
+        mma_tf32_1688(acc[3], af, v0.w, v1.w);
       }
     }
     __syncwarp();
@@ -845,7 +874,7 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
       bool zsplit = false;
       if (z != nullptr) {
         if (!in_head && unit_done) {
-          store_slice<4>(z, ldz, rs, rows, dim, p0.f + fw, acc, lane);
+          store_slice_tf32p(z, ldz, rs, rows, dim, p0.f + fw, acc, lane);
         } else {
           write_slot<4>(scratch + (gw * 2 + (in_head ? 0 : 1)) * WarpCfg<4>::kSlot, acc, lane);
           zsplit = true;
@@ -853,8 +882,9 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
       }
       in_head = false;
       if (FUSED) {
-        // oacc += Z_slice (16 x 32) . M[32 f .. 32 f + 31, :]; within each 8-feature block the MMA's
-        // k index t <-> feature 2t and t + 4 <-> 2t + 1 (the accumulator layout), on both operands
+        // oacc += Z_slice (16 x 32) . M[32 f .. 32 f + 31, :]; MMA step nt takes the accumulators of
+        // n8 tile nt as its A fragment: k index t <-> feature 8t + nt, t + 4 <-> 8t + 4 + nt (the
+        // permuted accumulator layout), on both operands
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) {
           uint32_t af[4];
@@ -862,14 +892,14 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
           asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(af[1]) : "f"(acc[nt][2]));
           asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(af[2]) : "f"(acc[nt][1]));
           asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(af[3]) : "f"(acc[nt][3]));
-          const int k0 = p0.f * 32 + nt * 8 + 2 * t4;
+          const int k0 = p0.f * 32 + 8 * t4 + nt, k1 = k0 + 4;
 #pragma unroll
           for (int n8 = 0; n8 < NO; ++n8) {
             if (n8 * 8 < d_out) {
               const int col = n8 * 8 + g8;
               const uint32_t b0 = (k0 < dim && col < d_out) ? __float_as_uint(__ldg(mw + (int64_t)k0 * d_out + col)) : 0u;
               const uint32_t b1 =
-                  (k0 + 1 < dim && col < d_out) ? __float_as_uint(__ldg(mw + (int64_t)(k0 + 1) * d_out + col)) : 0u;
+                  (k1 < dim && col < d_out) ? __float_as_uint(__ldg(mw + (int64_t)k1 * d_out + col)) : 0u;
               mma_tf32_1688(oacc[n8], af, b0, b1);
             }
           }
@@ -888,7 +918,7 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
         }
       }
       if (zsplit)
-        finish_split_z<4, WarpCfg<4>::kSlot>(chunk_ptr, T, FS, paired, kTfWarps, cnt, scratch, z, ldz, p0.base,
+        finish_split_z<4, WarpCfg<4>::kSlot, true>(chunk_ptr, T, FS, paired, kTfWarps, cnt, scratch, z, ldz, p0.base,
                                              p0.f, p0.nj, rs, rows, dim);
 #pragma unroll
       for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
