@@ -42,7 +42,8 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=5)
-    p.add_argument("--dim", type=int, default=128)
+    p.add_argument("--dim", type=int, default=None,
+                   help="dense feature dim (default: 32 for c1, BASELINE configs[0]; 128 otherwise)")
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--config", choices=["c2", "c1", "c3", "c4", "c5"], default="c2")
     p.add_argument("--graph", choices=["powerlaw", "community"], default="powerlaw",
@@ -62,7 +63,10 @@ def parse():
                    help="C3 layer order (model.gcn_layer): auto = A (X W) where it narrows the rows")
     p.add_argument("--launch-check", action="store_true",
                    help="test hook: start the ranks, rendezvous over gloo, print the world rank 0 saw, exit")
-    return p.parse_args()
+    args = p.parse_args()
+    if args.dim is None:
+        args.dim = 32 if args.config == "c1" else 128
+    return args
 
 
 # ----------------------------------------------------------------------------- helpers

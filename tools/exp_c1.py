@@ -39,12 +39,13 @@ def main():
     adj = graphgen.gcn_normalize_device(graphgen.cora_shaped(seed=0))
     ws = hc.partition(adj)
     dim = int(os.environ.get("DIM", "128"))
+    prec = os.environ.get("PREC", "bf16")
     x = graphgen.dense_features(adj.num_rows, dim, seed=1)
     for name, asg in (("classified", hc.classify_windows(hc.default_model(), ws)),
                       ("all-scalar", Assignment.uniform(len(ws), Path.SCALAR)),
                       ("all-tile", Assignment.uniform(len(ws), Path.TILE))):
-        plan = get_plan(ws, asg, "bf16")
-        xop, _ = stage_operand(x, "bf16", x.device)
+        plan = get_plan(ws, asg, prec)
+        xop, _ = stage_operand(x, prec, x.device, tf32_round=prec == "tf32")
         z, ldz = _alloc_z(ws.num_rows, dim, x.device)
         scr = plan.new_scratch() if plan.n_tile else None
         nt, ns = plan.n_tile, int(plan.scalar_list.numel())
@@ -61,7 +62,7 @@ def main():
                 res[f"both ({var})"] = graph_us(lambda: plan.run(xop, z, ldz, scratch=scr))
             set_scalar_variant("auto")
         res["empty graph node (torch add)"] = graph_us(lambda: z.add_(0))
-        print(f"{name}: tile windows {nt}, scalar windows {ns}, chunks {plan.nchunks}: " +
+        print(f"{prec} dim {dim} {name}: tile windows {nt}, scalar windows {ns}, chunks {plan.nchunks}: " +
               ", ".join(f"{k} {v:.2f} us" for k, v in res.items()), flush=True)
 
 
