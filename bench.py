@@ -742,7 +742,8 @@ def run_c3(args):
         torch.cuda.synchronize()
         profile_range(False)
     ms = s_ev.elapsed_time(e_ev) / steps
-    kernels = epoch_kernels(lambda: model.epoch(x, labels, ws, shard=shard)) if rank == 0 else None
+    # every rank runs the profiled epoch (its layers exchange rows); rank 0 reports its census
+    kernels = epoch_kernels(lambda: model.epoch(x, labels, ws, shard=shard))
     if world > 1:
         t = torch.tensor([ms], device=dev if dist.get_backend() == "nccl" else "cpu", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
