@@ -10,6 +10,9 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32
   asm volatile("cp.async.cg.shared.global.L2::cache_hint.L2::256B [%0], [%1], 16, %2, %3;" ::"r"(dst), "l"(src),
                "r"(src_bytes), "l"(pol)
                : "memory");
+#elif defined(HCS_EXP_XPOL_NONE)  // experiment: no L2 hint on the X gathers (address-range policies apply)
+  (void)pol;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 #else
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(dst), "l"(src),
                "r"(src_bytes), "l"(pol)

@@ -38,6 +38,13 @@ namespace hcs {
 #ifndef HCS_TILE_WARPS8
 #define HCS_TILE_WARPS8 8
 #endif
+// 128-B lines of packed entries past the chunk being loaded that are pulled into L2 one step
+// early, 64-feature slices only (C2 N = 128 2.441 -> 2.404 ms, N = 64 1.200 -> 1.195; N = 32
+// 0.815 -> 0.834, so not there; prefetching the gather indices ahead instead cost +30 %:
+// profiles/r02_exp_c5_tile.txt)
+#ifndef HCS_PLAN_PF_ENTL
+#define HCS_PLAN_PF_ENTL 4
+#endif
 constexpr int kWarpTileStages = 3;   // cp.async ring depth per warp
 constexpr int kWarpSlabBytes = 16 * 64 * 2;
 constexpr int kWarpEntRegs = 4;      // packed entries per lane held in registers (128 per chunk)
@@ -380,6 +387,9 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
   const uint32_t stage0 = smem_u32(wsmem + warp * kWarpSmemPerWarp);
   const uint32_t slab = stage0 + kWarpTileStages * kWarpStageBytes;
   const uint64_t keep = policy_evict_last();
+#if HCS_PLAN_PF_ENTL > 0
+  const int64_t ent_end = __ldg(ent_ptr + chunk_ptr[T]);  // entries of this launch end here
+#endif
   // plan data (indices, entries) is read once per feature slice: keep it for the window's
   // other slice-warps (FS > 1), stream it otherwise
   // (paired slice-warps read each chunk's plan together: stream it)
@@ -478,6 +488,14 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
     // a dense chunk's remaining entries: pull them into L2 one chunk ahead (lane = 128-B line)
     const int64_t ov = e0 + 32 * kWarpEntRegs + 32 * lane;
     if (ov < e1) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(ent + ov));
+#if HCS_PLAN_PF_ENTL > 0
+    // the entries of the following chunks are contiguous after e1: pull their lines into L2
+    // a step before their loads
+    {
+      const int64_t pv = (e1 & ~(int64_t)31) + 32 * lane;
+      if (SWV == 8 && lane < HCS_PLAN_PF_ENTL && pv < ent_end) asm volatile("prefetch.global.L2 [%0];" ::"l"(ent + pv));
+    }
+#endif
   };
 
   float acc[SWV][4];
