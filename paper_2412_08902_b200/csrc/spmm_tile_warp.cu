@@ -45,6 +45,9 @@ namespace hcs {
 #ifndef HCS_PLAN_PF_ENTL
 #define HCS_PLAN_PF_ENTL 4
 #endif
+#ifndef HCS_PLAN_PF_TFL
+#define HCS_PLAN_PF_TFL 0  // the same for the tf32 kernel's 8-B entries (lines)
+#endif
 constexpr int kWarpTileStages = 3;   // cp.async ring depth per warp
 constexpr int kWarpSlabBytes = 16 * 64 * 2;
 constexpr int kWarpEntRegs = 4;      // packed entries per lane held in registers (128 per chunk)
@@ -388,7 +391,7 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
   const uint32_t slab = stage0 + kWarpTileStages * kWarpStageBytes;
   const uint64_t keep = policy_evict_last();
 #if HCS_PLAN_PF_ENTL > 0
-  const int64_t ent_end = __ldg(ent_ptr + chunk_ptr[T]);  // entries of this launch end here
+  const int64_t ent_end = SWV == 8 ? __ldg(ent_ptr + chunk_ptr[T]) : 0;  // entries of this launch end here
 #endif
   // plan data (indices, entries) is read once per feature slice: keep it for the window's
   // other slice-warps (FS > 1), stream it otherwise
@@ -745,6 +748,9 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
   const uint32_t slab = stage0 + kWarpTileStages * kTfStage;
   uint8_t* slab_p = tsmem + warp * kTfPerWarp + kWarpTileStages * kTfStage;
   const uint64_t keep = policy_evict_last();
+#if HCS_PLAN_PF_TFL > 0
+  const int64_t ent_end = __ldg(ent_ptr + chunk_ptr[T]);
+#endif
   const uint64_t once = policy_evict_first();
   const char* xb = reinterpret_cast<const char*>(x);
   const int64_t ldxb = ldx * 4;
@@ -810,6 +816,12 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
       const int64_t i = e0 + lane + 32 * q;
       e[q] = i < e1 ? __ldg(ent + i) : make_uint2(0u, 0u);
     }
+#if HCS_PLAN_PF_TFL > 0
+    {  // entry lines of the next chunks into L2 a step early (16 entries per 128-B line)
+      const int64_t pv = (e1 & ~(int64_t)15) + 16 * lane;
+      if (lane < HCS_PLAN_PF_TFL && pv < ent_end) asm volatile("prefetch.global.L2 [%0];" ::"l"(ent + pv));
+    }
+#endif
   };
 
   int g_a[NI], g_b[NI], g2[NI];

@@ -12,7 +12,8 @@ torch.cuda.set_device(0)
 adj = graphgen.reddit_shaped(seed=0); adj.symmetric = True
 a = normalize_adj(adj, "gcn")
 ws = hc.partition(a)
-plan = get_plan(ws, hc.classify_windows(hc.default_model(), ws), "bf16")
+prec = os.environ.get("PREC", "bf16")
+plan = get_plan(ws, hc.classify_windows(hc.default_model(), ws), prec)
 res = {}
 pads = [int(p) for p in os.environ.get("PADS", "1").split(",")]
 if os.environ.get("NPR3") is not None:
@@ -22,7 +23,7 @@ for dim in [int(d) for d in os.environ.get("DIMS", "16,32").split(",")]:
   for pad in pads:
     ex.PAD_TO_SLICE = bool(pad)
     x = torch.rand(a.num_rows, dim, device="cuda")
-    xop, _ = stage_operand(x, "bf16", torch.device("cuda"))
+    xop, _ = stage_operand(x, prec, torch.device("cuda"), tf32_round=prec == "tf32")
     z, ldz = _alloc_z(a.num_rows, dim, torch.device("cuda"))
     for _ in range(3):
         plan.run(xop, z, ldz)
