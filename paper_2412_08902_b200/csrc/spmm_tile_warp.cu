@@ -137,7 +137,13 @@ __device__ __forceinline__ void advance(ChunkPos& p, const int64_t* __restrict__
   p.nj = p.t < T ? (int32_t)(ldg64(chunk_ptr + p.t + 1) - p.base) : 1;  // past the end: never used
 }
 
-__device__ __forceinline__ void warp_range(int64_t total, int64_t nwarps, int64_t gw, int64_t& a, int64_t& b) {
+__device__ __forceinline__ void warp_range(int64_t total, int64_t nwarps, int64_t gw, int64_t& a, int64_t& b,
+                                           const int64_t* __restrict__ wb = nullptr) {
+  if (wb != nullptr) {  // cost-weighted bounds (k_tile_bounds): range g = [wb[g], wb[g + 1])
+    a = __ldg(wb + gw);
+    b = __ldg(wb + gw + 1);
+    return;
+  }
   a = (total * gw) / nwarps;
   b = (total * (gw + 1)) / nwarps;
 }
@@ -157,7 +163,16 @@ inline int64_t tile_cnt_words() { return ((int64_t)num_sms() * kMaxWarpsPerCta +
 
 // group of a balanced split of `total` positions over `ng` ranges that owns position v
 // (largest g with floor(total * g / ng) <= v; see warp_range)
-__device__ __forceinline__ int64_t range_owner(int64_t total, int64_t ng, int64_t v) {
+__device__ __forceinline__ int64_t range_owner(int64_t total, int64_t ng, int64_t v,
+                                               const int64_t* __restrict__ wb = nullptr) {
+  if (wb != nullptr) {  // largest g < ng with wb[g] <= v (empty ranges have wb[g] == wb[g + 1])
+    int64_t lo = 0, hi = ng - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (__ldg(wb + mid) <= v) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+  }
   return ((v + 1) * ng - 1) / total;
 }
 
@@ -184,7 +199,8 @@ __device__ __forceinline__ bool split_arrive(unsigned* cnt, int64_t us, int64_t 
 // SLOT floats (s = 1: the unit it opened, s = 0: the unit it continued); warp of group k = k * FSm + fw.
 template <int NT, int SLOT>
 __device__ __forceinline__ void split_reduce(const float* __restrict__ slots, int64_t total, int64_t ng, int64_t g_o,
-                                             int FSm, int fw, int64_t ue, float (&acc)[NT][4], int lane) {
+                                             int FSm, int fw, int64_t ue, float (&acc)[NT][4], int lane,
+                                             const int64_t* __restrict__ wb = nullptr) {
   const float* s = slots + ((g_o * FSm + fw) * 2 + 1) * (int64_t)SLOT;
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt)
@@ -193,13 +209,18 @@ __device__ __forceinline__ void split_reduce(const float* __restrict__ slots, in
   // range bounds floor(total * k / ng) stepped incrementally (no 64-bit division in the loop)
   const int64_t tq = total / ng, tr = total - tq * ng;
   int64_t bk = (total * (g_o + 1)) / ng, br = total * (g_o + 1) - bk * ng;
+  if (wb != nullptr) bk = __ldg(wb + g_o + 1);
   for (int64_t k = g_o + 1; k < ng; ++k) {
     const int64_t ak = bk;
-    bk += tq;
-    br += tr;
-    if (br >= ng) {
-      ++bk;
-      br -= ng;
+    if (wb != nullptr) {
+      bk = __ldg(wb + k + 1);
+    } else {
+      bk += tq;
+      br += tr;
+      if (br >= ng) {
+        ++bk;
+        br -= ng;
+      }
     }
     if (ak >= bk) continue;
     const float* sk = slots + ((k * FSm + fw) * 2 + 0) * (int64_t)SLOT;
@@ -296,7 +317,8 @@ template <int SWV, int SLOT, bool PERM = false>
 __device__ __forceinline__ void finish_split_z(const int64_t* __restrict__ chunk_ptr, int64_t T, int FS, int paired,
                                                int warps_per_cta, unsigned* __restrict__ cnt,
                                                const float* __restrict__ slots, float* __restrict__ z, int64_t ldz,
-                                               int64_t base, int f, int nj, int64_t rs, int rows, int dim) {
+                                               int64_t base, int f, int nj, int64_t rs, int rows, int dim,
+                                               const int64_t* __restrict__ wb = nullptr) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (int64_t)blockIdx.x * warps_per_cta + (threadIdx.x >> 5);
   const int64_t nwarps = (int64_t)gridDim.x * warps_per_cta;
@@ -306,12 +328,12 @@ __device__ __forceinline__ void finish_split_z(const int64_t* __restrict__ chunk
   const int64_t c0 = __ldg(chunk_ptr);
   const int64_t total = (int64_t)FSr * (__ldg(chunk_ptr + T) - c0);
   int64_t a, b;
-  warp_range(total, ng, gi, a, b);
+  warp_range(total, ng, gi, a, b, wb);
   const int64_t us = (int64_t)FSr * (base - c0) + (int64_t)f * nj;
-  const int64_t g_o = range_owner(total, ng, us);
+  const int64_t g_o = range_owner(total, ng, us, wb);
   if (!split_arrive(cnt + g_o * FSm + fw, us, us + nj, a, b, lane)) return;
   float acc[SWV][4];
-  split_reduce<SWV, SLOT>(slots, total, ng, g_o, FSm, fw, us + nj, acc, lane);
+  split_reduce<SWV, SLOT>(slots, total, ng, g_o, FSm, fw, us + nj, acc, lane, wb);
   if constexpr (PERM) {
     store_slice_tf32p(z, ldz, rs, rows, dim, f + fw, acc, lane);
   } else {
@@ -324,7 +346,8 @@ __device__ __forceinline__ void finish_split_z(const int64_t* __restrict__ chunk
 __device__ __forceinline__ void finish_split_out(const int64_t* __restrict__ chunk_ptr, int64_t T, int FS,
                                                  int paired, int warps_per_cta, unsigned* __restrict__ cnt,
                                                  const float* __restrict__ oslots, float* __restrict__ out,
-                                                 int64_t ldo, int64_t base, int nj, int64_t rs, int rows, int d_out) {
+                                                 int64_t ldo, int64_t base, int nj, int64_t rs, int rows, int d_out,
+                                                 const int64_t* __restrict__ wb = nullptr) {
   const int lane = threadIdx.x & 31;
   const int FSr = paired ? 1 : FS, FSm = paired ? FS : 1;
   const int64_t gw = (int64_t)blockIdx.x * warps_per_cta + (threadIdx.x >> 5);
@@ -332,12 +355,12 @@ __device__ __forceinline__ void finish_split_out(const int64_t* __restrict__ chu
   const int64_t c0 = __ldg(chunk_ptr);
   const int64_t total = (int64_t)FSr * (__ldg(chunk_ptr + T) - c0);
   int64_t a, b;
-  warp_range(total, ng, gw / FSm, a, b);
+  warp_range(total, ng, gw / FSm, a, b, wb);
   const int64_t ws = (int64_t)FSr * (base - c0), we = ws + (int64_t)FSr * nj;
-  const int64_t g_o = range_owner(total, ng, ws);
+  const int64_t g_o = range_owner(total, ng, ws, wb);
   if (!split_arrive(cnt + tile_cnt_words_dev() + g_o, ws, we, a, b, lane)) return;
   float oacc[kFusedOutMax / 8][4];
-  split_reduce<kFusedOutMax / 8, kOutSlot>(oslots, total, ng, g_o, 1, 0, we, oacc, lane);
+  split_reduce<kFusedOutMax / 8, kOutSlot>(oslots, total, ng, g_o, 1, 0, we, oacc, lane, wb);
   store_out(out, ldo, rs, rows, d_out, oacc, lane);
 }
 
@@ -350,15 +373,19 @@ __device__ __forceinline__ void finish_split_out(const int64_t* __restrict__ chu
 // NPR = 16-feature groups of a slice that hold features (compile time, so the unrolled
 // ldmatrix/mma schedule is kept): SWV/2, or 3 for a single 33..48-feature slice (the 41-wide
 // GCN gradient), whose last group is neither gathered nor multiplied.
-template <int SWV, bool FUSED, int NPR = SWV / 2>
+template <int SWV, bool FUSED, int NPR = SWV / 2, bool WB = false>
 __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
     k_tile_warp(const int32_t* __restrict__ tile_list, int64_t T, const int64_t* __restrict__ chunk_ptr,
                 const int32_t* __restrict__ gidx, const int64_t* __restrict__ ent_ptr,
                 const uint32_t* __restrict__ ent, int64_t n_rows, int wh, const __nv_bfloat16* __restrict__ x,
                 int64_t ldx, int dim, int FS, float* __restrict__ z, int64_t ldz, float* __restrict__ scratch,
                 const float* __restrict__ mw, int d_out, float* __restrict__ out, int64_t ldo,
-                float* __restrict__ oscratch, int paired, unsigned* __restrict__ cnt) {
+                float* __restrict__ oscratch, int paired, unsigned* __restrict__ cnt,
+                const int64_t* __restrict__ wb_arg) {
   using C = WarpCfg<SWV>;
+  // WB: cost-weighted warp ranges from k_tile_bounds (a separate instantiation, so the uniform
+  // kernel's code is unchanged by the weighted path: +6 % on C2 when both shared one body)
+  const int64_t* wb = WB ? wb_arg : nullptr;
   constexpr int kWarpTileWarps = C::kWarps, kWarpStageBytes = C::kStageBytes, kWarpSmemPerWarp = C::kPerWarp;
   constexpr int NI = C::kIssue;
   extern __shared__ uint8_t wsmem_raw[];
@@ -376,7 +403,7 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
   const int64_t ngroups = paired ? nwarps / FS : nwarps;
   const int64_t total = (int64_t)FSr * (chunk_ptr[T] - c0);
   int64_t a = 0, b = 0;
-  if (!paired || gw < ngroups * FS) warp_range(total, ngroups, paired ? gw / FS : gw, a, b);
+  if (!paired || gw < ngroups * FS) warp_range(total, ngroups, paired ? gw / FS : gw, a, b, wb);
   if (FUSED) {
     __nv_bfloat16* wt = reinterpret_cast<__nv_bfloat16*>(wsmem + C::kOffW);
     for (int i = threadIdx.x; i < kFusedOutMax * kFusedLdw; i += blockDim.x) {
@@ -650,7 +677,7 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
               const int64_t gi = paired ? gw / FS : gw;
               write_slot(oscratch + (gi * 2 + (win_head ? 0 : 1)) * kOutSlot, oacc, lane);
               finish_split_out(chunk_ptr, T, FS, paired, kWarpTileWarps, cnt, oscratch, out, ldo, P0.base, P0.nj,
-                               rs, rows, d_out);
+                               rs, rows, d_out, wb);
             }
           }
 #pragma unroll
@@ -659,7 +686,7 @@ __global__ void __launch_bounds__(WarpCfg<SWV>::kWarps * 32, 1)
       }
       if (zsplit)
         finish_split_z<SWV, C::kSlot>(chunk_ptr, T, FS, paired, kWarpTileWarps, cnt, scratch, z, ldz, P0.base, P0.f,
-                                      P0.nj, rs, rows, dim);
+                                      P0.nj, rs, rows, dim, wb);
 #pragma unroll
       for (int i = 0; i < SWV; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
     }
@@ -1002,6 +1029,63 @@ int spmm_tile_warp_tf32(const int32_t* tile_list, int64_t n_tile, const int64_t*
   return HCS_OK;
 }
 
+// Cost-weighted warp ranges.  The uniform split gives every warp (group) the same number of
+// 64-column chunks, but a chunk costs a 64-row gather plus its entries' scatter, and the hub
+// windows of a skewed graph (R-MAT C5: the first windows) hold chunks of up to ~900 entries, so
+// the first ranges carry 1.8x the mean entries (tools/exp_tile_balance.py) and the launch waits
+// for them.  k_tile_bounds splits the positions on the prefix cost alpha * chunks + entries
+// (ent_ptr is already the entries' prefix sum) with one 32-way warp search per boundary; the tile
+// kernel reads its range from the bounds and locates split-unit owners by binary search.
+// alpha comes with the launch (hcs_spmm_tile_balanced; 0 = uniform).  Used when one position is one chunk (paired slices or a
+// single slice) and the launch has >= kBalanceMinTilesPerGroup windows per group (host-known, so
+// small plans keep one launch and no sync is needed).
+constexpr int64_t kBalanceMinTilesPerGroup = 8;
+
+__global__ void k_tile_bounds(const int64_t* __restrict__ chunk_ptr, int64_t T, const int64_t* __restrict__ ent_ptr,
+                              int64_t ng, int64_t alpha, int64_t* __restrict__ wb) {
+  // one warp per boundary g: wb[g] = smallest p with (alpha p + entries before p) * ng >= g * F,
+  // found by a 32-way search (one round of 32 parallel ent_ptr loads per step, ~5 steps)
+  const int lane = threadIdx.x & 31;
+  const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (g > ng) return;
+  const int64_t c0 = __ldg(chunk_ptr), total = __ldg(chunk_ptr + T) - c0;
+  if (g == 0 || g == ng) {
+    if (lane == 0) wb[g] = g == 0 ? 0 : total;
+    return;
+  }
+  const int64_t e0 = __ldg(ent_ptr + c0);
+  const int64_t F = alpha * total + (__ldg(ent_ptr + c0 + total) - e0);
+  const int64_t target = g * F;
+  auto pred = [&](int64_t p) { return (alpha * p + (__ldg(ent_ptr + c0 + p) - e0)) * ng >= target; };
+  int64_t lo = 0, hi = total;  // answer in [lo, hi]; pred(total) holds
+  while (hi - lo >= 32) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t p = min(lo + lane * step, hi);
+    const unsigned m = __ballot_sync(0xffffffffu, pred(p));
+    if (m & 1u) {
+      hi = lo;
+      break;
+    }
+    const int j = m ? __ffs(m) - 1 : 32;  // answer in (p_{j-1}, p_j]
+    const int64_t nlo = min(lo + (int64_t)(j - 1) * step, hi) + 1;
+    hi = j < 32 ? min(lo + (int64_t)j * step, hi) : hi;
+    lo = nlo;
+  }
+  const int64_t p = lo + lane;
+  const unsigned m = __ballot_sync(0xffffffffu, p <= hi && pred(p));
+  if (lane == 0) wb[g] = m ? lo + __ffs(m) - 1 : hi;
+}
+
+// int64 bounds of the weighted split, after the largest slot region of the workspace
+inline int64_t tile_bounds_offset_floats() {
+  static_assert(WarpCfg<4>::kWarps <= kMaxWarpsPerCta && WarpCfg<8>::kWarps <= kMaxWarpsPerCta &&
+                    kTfWarps <= kMaxWarpsPerCta, "split counters");
+  return 2 * tile_cnt_words() + std::max<int64_t>(
+      std::max<int64_t>((int64_t)num_sms() * WarpCfg<4>::kWarps * 2 * WarpCfg<4>::kSlot,
+                        (int64_t)num_sms() * WarpCfg<8>::kWarps * 2 * (WarpCfg<8>::kSlot + kOutSlot)),
+      (int64_t)num_sms() * WarpCfg<16>::kWarps * 2 * WarpCfg<16>::kSlot);
+}
+
 static int g_warp_swv = 0;     // 0 auto, 4 or 8 (16-B vectors per row slice)
 // Feature slices of a window walked side by side by sibling warps: 1 on (default), 0 off,
 // 2 auto = on when X does not fit in L2.  Paired warps read each chunk's plan together (the
@@ -1018,7 +1102,7 @@ static int launch_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* 
                        const int64_t* ent_ptr, const uint32_t* ent, int64_t n_rows, int wh, const __nv_bfloat16* x,
                        int64_t ldx, int dim, float* z, int64_t ldz, float* scratch, int64_t scratch_floats,
                        cudaStream_t st, const float* mw = nullptr, int d_out = 0, float* out = nullptr,
-                       int64_t ldo = 0, int64_t x_rows = 0) {
+                       int64_t ldo = 0, int64_t x_rows = 0, int alpha = 0) {
   using C = WarpCfg<SWV>;
   const int FS = (dim + C::kFeat - 1) / C::kFeat;
   const int grid = tile_grid();
@@ -1038,12 +1122,21 @@ static int launch_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* 
   // one slice of 33..48 features: the fused (GCN) kernel skips the empty 16-feature group
   // (C3 5.92 -> 5.71 ms); the plain SpMM is faster with the full unrolled schedule now that
   // every lane copies whole padded rows (N = 40/41/48: 1.29 -> 1.21 ms; tools/exp_c3_npr3.sh)
-  auto kern = (FUSED && g_warp_npr3 && SWV == 8 && FS == 1 && dim <= 48 && dim > 32)
-                  ? k_tile_warp<SWV, FUSED, (SWV == 8 ? 3 : SWV / 2)>
-                  : k_tile_warp<SWV, FUSED>;
+  const bool npr3 = FUSED && g_warp_npr3 && SWV == 8 && FS == 1 && dim <= 48 && dim > 32;
+  // cost-weighted ranges (positions are chunks when paired or FS == 1)
+  int64_t* wb = nullptr;
+  const int64_t ng = paired ? nwarps / FS : nwarps;
+  if (alpha > 0 && !npr3 && (paired || FS == 1) && n_tile >= kBalanceMinTilesPerGroup * ng &&
+      scratch_floats >= tile_bounds_offset_floats() + 2 * (ng + 1)) {
+    wb = reinterpret_cast<int64_t*>(scratch + tile_bounds_offset_floats());
+    k_tile_bounds<<<(unsigned)((ng + 8) / 8), 256, 0, st>>>(chunk_ptr, n_tile, ent_ptr, ng, alpha, wb);
+    HCS_LAUNCH_CHECK("k_tile_bounds");
+  }
+  auto kern = npr3 ? k_tile_warp<SWV, FUSED, (SWV == 8 ? 3 : SWV / 2)>
+                   : (wb ? k_tile_warp<SWV, FUSED, SWV / 2, true> : k_tile_warp<SWV, FUSED>);
   HCS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   kern<<<grid, C::kWarps * 32, smem, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim,
-                                            FS, z, ldz, slots, mw, d_out, out, ldo, oscratch, paired, cnt);
+                                            FS, z, ldz, slots, mw, d_out, out, ldo, oscratch, paired, cnt, wb);
   HCS_LAUNCH_CHECK("k_tile_warp");
   return HCS_OK;
 }
@@ -1060,7 +1153,7 @@ int gcn_tile_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk
 int spmm_tile_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
                    const int64_t* ent_ptr, const uint32_t* ent, int64_t n_rows, int wh, const __nv_bfloat16* x,
                    int64_t x_rows, int64_t ldx, int dim, float* z, int64_t ldz, float* scratch, int64_t scratch_floats,
-                   cudaStream_t st) {
+                   cudaStream_t st, int alpha = 0) {
   // 64-feature slices halve the per-feature slab work once a window has >= 2 slices of 32
   const int swv = g_warp_swv ? g_warp_swv : (dim > 32 ? 8 : 4);
   if (swv == 16)
@@ -1068,18 +1161,14 @@ int spmm_tile_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chun
                           scratch_floats, st, nullptr, 0, nullptr, 0, x_rows);
   if (swv == 8)
     return launch_warp<8>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim, z, ldz, scratch,
-                          scratch_floats, st, nullptr, 0, nullptr, 0, x_rows);
+                          scratch_floats, st, nullptr, 0, nullptr, 0, x_rows, alpha);
   return launch_warp<4>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim, z, ldz, scratch,
-                          scratch_floats, st, nullptr, 0, nullptr, 0, x_rows);
+                          scratch_floats, st, nullptr, 0, nullptr, 0, x_rows, alpha);
 }
 
 int64_t tile_warp_scratch_floats() {
-  static_assert(WarpCfg<4>::kWarps <= kMaxWarpsPerCta && WarpCfg<8>::kWarps <= kMaxWarpsPerCta &&
-                    kTfWarps <= kMaxWarpsPerCta, "split counters");
-  return 2 * tile_cnt_words() + std::max<int64_t>(
-      std::max<int64_t>((int64_t)num_sms() * WarpCfg<4>::kWarps * 2 * WarpCfg<4>::kSlot,
-                        (int64_t)num_sms() * WarpCfg<8>::kWarps * 2 * (WarpCfg<8>::kSlot + kOutSlot)),
-      (int64_t)num_sms() * WarpCfg<16>::kWarps * 2 * WarpCfg<16>::kSlot);
+  // slots, then (ng + 1) int64 range bounds for up to one group per warp
+  return tile_bounds_offset_floats() + 2 * ((int64_t)num_sms() * kMaxWarpsPerCta + 2);
 }
 
 }  // namespace hcs
@@ -1089,10 +1178,12 @@ using namespace hcs;
 // K4: tile windows on the tensor cores (executors.py:111-141 tile_window for every window of
 // tile_list).  bf16 plan + bf16 X: k_tile_warp (mma.sync m16n8k16); fp32 plan + tf32-rounded fp32
 // X: k_tile_warp_tf32 (m16n8k8).  workspace: >= hcs_tile_scratch_floats() floats.
-extern "C" int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
-                             const int64_t* ent_ptr, const void* ent, int ent_dtype, int64_t n_rows, int32_t wh,
-                             const void* x, int x_dtype, int64_t x_rows, int32_t dim, int64_t ldx, float* z,
-                             int64_t ldz, void* workspace, size_t ws_bytes, void* stream) {
+extern "C" int hcs_spmm_tile_balanced(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr,
+                                      const int32_t* gidx, const int64_t* ent_ptr, const void* ent, int ent_dtype,
+                                      int64_t n_rows, int32_t wh, const void* x, int x_dtype, int64_t x_rows,
+                                      int32_t dim, int64_t ldx, float* z, int64_t ldz, void* workspace,
+                                      size_t ws_bytes, int alpha, void* stream) {
+  HCS_REQUIRE(alpha >= 0 && alpha <= 1 << 16, HCS_EINVAL, "tile balance alpha must be in [0, 65536] (got %d)", alpha);
   HCS_REQUIRE(wh > 0 && wh <= 16, HCS_EINVAL, "tile path supports window heights 1..16 (got %d)", wh);
   HCS_REQUIRE(dim > 0, HCS_EINVAL, "dim must be positive");
   HCS_REQUIRE(((uintptr_t)x & 15) == 0, HCS_EINVAL, "x must be 16-byte aligned");
@@ -1110,7 +1201,15 @@ extern "C" int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int
   if (n_tile == 0) return HCS_OK;
   return spmm_tile_warp(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, (const uint32_t*)ent, n_rows, wh,
                         (const __nv_bfloat16*)x, x_rows, ldx, dim, z, ldz, (float*)workspace,
-                        (int64_t)(ws_bytes / sizeof(float)), as_stream(stream));
+                        (int64_t)(ws_bytes / sizeof(float)), as_stream(stream), alpha);
+}
+
+extern "C" int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
+                             const int64_t* ent_ptr, const void* ent, int ent_dtype, int64_t n_rows, int32_t wh,
+                             const void* x, int x_dtype, int64_t x_rows, int32_t dim, int64_t ldx, float* z,
+                             int64_t ldz, void* workspace, size_t ws_bytes, void* stream) {
+  return hcs_spmm_tile_balanced(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, ent_dtype, n_rows, wh, x, x_dtype,
+                                x_rows, dim, ldx, z, ldz, workspace, ws_bytes, 0, stream);
 }
 
 // K6/K7: tile windows with the fused GCN epilogue: out = (A_w X) M per TILE window, plus

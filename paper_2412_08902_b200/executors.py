@@ -307,6 +307,14 @@ class HybridPlan:
                       self.chunk_ptr.data_ptr(), self.nchunks, self.gidx.data_ptr(), self.ent_ptr.data_ptr(),
                       self.ent.data_ptr(), ent_dtype, self.nnz_tile, ws.data_ptr(), ws.numel(), _lib.stream())
             del ws
+        # skewed plans (a chunk with more entries than the kernel holds in registers: hub windows,
+        # e.g. R-MAT) run with cost-weighted warp ranges (hcs_spmm_tile_balanced; C5 tile launch
+        # 28.7 -> 27.9 ms at alpha 256, tools/exp_tile_alpha.py); balanced plans keep equal chunk
+        # counts (C2: the weighted split only adds its bounds launch)
+        self.tile_alpha = 0
+        if self.n_tile and precision == "bf16" and self.nchunks:
+            if int((self.ent_ptr[1:] - self.ent_ptr[:-1]).max().item()) > TILE_DENSE_CHUNK:
+                self.tile_alpha = TILE_BALANCE_ALPHA
         if precision == "bf16":
             self.scalar_vals, self.scalar_vals_code = csr.values_bf16(), _lib.DTYPE_BF16
         else:
@@ -407,10 +415,11 @@ class HybridPlan:
         if t1 > t0:
             if scratch is None:
                 scratch = self.scratch(s)
-            _lib.call("hcs_spmm_tile", self.tile_list.data_ptr() + 4 * t0, t1 - t0, self.chunk_ptr.data_ptr() + 8 * t0,
-                      self.gidx.data_ptr(), self.ent_ptr.data_ptr(), self.ent.data_ptr(), self.ent_dtype,
-                      csr.num_rows, self.windows.window_height, xop.t.data_ptr(), xop.dtype_code, xop.rows, xop.dim,
-                      xop.ld, z.data_ptr(), ldz, scratch.data_ptr(), scratch.numel() * 4, s)
+            _lib.call("hcs_spmm_tile_balanced", self.tile_list.data_ptr() + 4 * t0, t1 - t0,
+                      self.chunk_ptr.data_ptr() + 8 * t0, self.gidx.data_ptr(), self.ent_ptr.data_ptr(),
+                      self.ent.data_ptr(), self.ent_dtype, csr.num_rows, self.windows.window_height, xop.t.data_ptr(),
+                      xop.dtype_code, xop.rows, xop.dim, xop.ld, z.data_ptr(), ldz, scratch.data_ptr(),
+                      scratch.numel() * 4, self.tile_alpha, s)
         if tile_events is not None:
             tile_events[1].record()
         if s1 > s0:
@@ -426,6 +435,8 @@ class HybridPlan:
 
 
 CONCURRENT_MAX_WINDOWS = 8192
+TILE_DENSE_CHUNK = 128   # entries the tile kernel holds in registers per chunk (kWarpEntRegs x 32)
+TILE_BALANCE_ALPHA = 256  # cost of one chunk in entries for the weighted split (tools/exp_tile_alpha.py)
 SCALAR_PIECES_MAX_WINDOWS = 1024  # scalar lists up to this length run hcs_spmm_scalar_pieces
 _SIDE_STREAMS: dict = {}
 

@@ -507,6 +507,45 @@ def test_scalar_pieces_wide_rows_and_hubs(cuda_ok, precision, dim):
     assert np.array_equal(r1, s)
 
 
+def test_tile_balanced_ranges_on_skewed_plan(cuda_ok):
+    """A skewed plan (hub windows whose 64-column chunks hold up to 1,024 entries, plus enough
+    ordinary windows for the weighted split to apply): HybridPlan picks cost-weighted warp
+    ranges (hcs_spmm_tile_balanced, k_tile_bounds); the product == the exact one within the bf16
+    tolerance, bitwise run to run, and == the uniform-range product to fp32 summation order."""
+    rng = np.random.default_rng(21)
+    n, m, dim = 16 * 6000, 30000, 128
+    hub_cols = rng.choice(m, size=300, replace=False)
+    rows, cols = [], []
+    for w in range(n // 16):
+        for r in range(16 * w, 16 * w + 16):
+            if w % 40 == 0:  # hub window: every row on the same 300 columns
+                c = hub_cols
+            else:
+                c = rng.choice(m, size=int(rng.integers(8, 24)), replace=False)
+            rows += [r] * len(c)
+            cols += list(c)
+    a = orc.from_coo(n, m, rows, cols, rng.uniform(-1, 1, len(rows)))
+    ws = hc.partition(to_hc(a))
+    asg = Assignment.uniform(len(ws), Path.TILE)
+    from paper_2412_08902_b200.executors import get_plan
+
+    plan = get_plan(ws, asg, "bf16")
+    assert plan.tile_alpha > 0  # chunks above 128 entries were detected
+    x = orc.random_dense(m, dim, seed=8)
+    xt = torch.from_numpy(x).to(torch.bfloat16).cuda()
+    r1 = hc.spmm_hybrid(ws, asg, xt).z.data.clone()
+    r2 = hc.spmm_hybrid(ws, asg, xt).z.data.clone()
+    assert torch.equal(r1, r2)
+    exact = orc.spmm_exact(a, xt.float().cpu().numpy().astype(np.float64))
+    assert orc.max_rel_err(r1.cpu().numpy(), exact) <= BF16_TOL
+    alpha, plan.tile_alpha = plan.tile_alpha, 0
+    try:
+        r0 = hc.spmm_hybrid(ws, asg, xt).z.data.clone()
+    finally:
+        plan.tile_alpha = alpha
+    assert orc.max_rel_err(r1.cpu().numpy(), r0.cpu().numpy().astype(np.float64)) <= 1e-5
+
+
 def test_tile_grid_setter(cuda_ok):
     """hcs_set_tile_grid (SMs left to the NCCL kernels of the multi-GPU exchange): any CTA count gives
     the product to fp32 summation order (different warp ranges), deterministic per grid; the
