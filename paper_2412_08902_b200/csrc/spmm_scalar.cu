@@ -780,6 +780,11 @@ extern "C" int hcs_gcn_scalar(const int64_t* row_ptr, const int32_t* col_idx, co
 // p_count[i] = its number of pieces; p_k = [k0, k1) entry ranges (2 int64 per piece).
 // slots: npieces x ld_slot floats (ld_slot >= dim, multiple of 4, 16-B aligned); cnt: npieces
 // uint32 completion counters, zero before the first launch (left zero).
+#ifndef HCS_PIECES_BF16_V16_MAXDIM
+// bf16 rows up to this width use 16-B lane vectors (4 lanes per 64-B row, a 3-step shuffle tree
+// instead of 4 over twice the floats): C1 dim 32 piece launch 10.26 -> 8.23 us, bench 10.5 -> 10.3 us
+#define HCS_PIECES_BF16_V16_MAXDIM 64
+#endif
 extern "C" int hcs_spmm_scalar_pieces(const int32_t* col_idx, const void* values, int values_dtype,
                                       const int32_t* p_row, const int64_t* p_k, const int32_t* p_first,
                                       const int32_t* p_count, int64_t npieces, const void* x, int x_dtype,
@@ -795,7 +800,8 @@ extern "C" int hcs_spmm_scalar_pieces(const int32_t* col_idx, const void* values
   const unsigned grid = (unsigned)((npieces + 7) / 8);
   const bool v32 = ((uintptr_t)x & 31) == 0 && (ldx * (x_dtype == HCS_DTYPE_BF16 ? 2 : 4)) % 32 == 0 &&
                    ldx >= ((dim + (x_dtype == HCS_DTYPE_BF16 ? 15 : 7)) / (x_dtype == HCS_DTYPE_BF16 ? 16 : 8)) *
-                              (x_dtype == HCS_DTYPE_BF16 ? 16 : 8);
+                              (x_dtype == HCS_DTYPE_BF16 ? 16 : 8) &&
+                   !(x_dtype == HCS_DTYPE_BF16 && dim <= HCS_PIECES_BF16_V16_MAXDIM);
 #define HCS_PIECES(XT, VT)                                                                                        \
   do {                                                                                                          \
     if (v32)                                                                                                    \
