@@ -544,6 +544,22 @@ def test_tile_balanced_ranges_on_skewed_plan(cuda_ok):
     finally:
         plan.tile_alpha = alpha
     assert orc.max_rel_err(r1.cpu().numpy(), r0.cpu().numpy().astype(np.float64)) <= 1e-5
+    # small grids: few warp groups, many windows cut by weighted bounds (split owners found by
+    # binary search over the bounds), every paired / single-slice width
+    from paper_2412_08902_b200 import _lib
+
+    for ctas in (1, 4, 37):
+        _lib.call("hcs_set_tile_grid", ctas)
+        try:
+            for d in (128, 64, 41):
+                xd = torch.from_numpy(x[:, :d].copy()).to(torch.bfloat16).cuda()
+                ex = orc.spmm_exact(a, xd.float().cpu().numpy().astype(np.float64))
+                za = hc.spmm_hybrid(ws, asg, xd).z.data.clone()
+                zb = hc.spmm_hybrid(ws, asg, xd).z.data
+                assert torch.equal(za, zb), (ctas, d)
+                assert orc.max_rel_err(za.cpu().numpy(), ex) <= BF16_TOL, (ctas, d)
+        finally:
+            _lib.call("hcs_set_tile_grid", 0)
 
 
 def test_tile_grid_setter(cuda_ok):

@@ -1,7 +1,8 @@
 """compute-sanitizer workload (memcheck / racecheck / synccheck / initcheck): every product kernel
 once on small inputs -- C1 (Cora-shaped) and the 8,192-node power-law graph (mixed TILE/SCALAR
 windows): K1 partition + selector, K2 tile plan, K4 tile (bf16 + tf32), K3 scalar, the fused GCN
-epilogues (bf16 + tf32, tile + scalar), grad_W, the dense update, normalisation, LOA + permute.
+epilogues (bf16 + tf32, tile + scalar), grad_W, the dense update, normalisation, LOA + permute, and
+the cost-weighted tile ranges (k_tile_bounds + the WB kernel) on a hub-window plan with a 4-CTA grid.
 Run: compute-sanitizer --tool memcheck python tools/sanitize.py"""
 import os
 import sys
@@ -40,8 +41,38 @@ def run(a, name):
     print(name, "ok", flush=True)
 
 
+def skewed():
+    """Hub windows (chunks of up to 1,024 entries) -> HybridPlan.tile_alpha > 0; a 4-CTA tile grid
+    makes the weighted split apply to a small plan (>= 8 tile windows per warp group)."""
+    from oracle import rowwin_oracle as orc
+    from paper_2412_08902_b200 import _lib
+    from paper_2412_08902_b200.executors import get_plan
+
+    rng = np.random.default_rng(5)
+    n, m = 16 * 400, 4000
+    hub = rng.choice(m, size=200, replace=False)
+    rows, cols = [], []
+    for r in range(n):
+        c = hub if (r // 16) % 25 == 0 else rng.choice(m, size=int(rng.integers(4, 30)), replace=False)
+        rows += [r] * len(c)
+        cols += list(c)
+    a = orc.from_coo(n, m, rows, cols, rng.uniform(-1, 1, len(rows)))
+    ws = hc.partition(hc.SparseCsr(n, m, a.row_ptr, a.col_idx, a.values))
+    asg = Assignment.uniform(len(ws), Path.TILE)
+    assert get_plan(ws, asg, "bf16").tile_alpha > 0
+    _lib.call("hcs_set_tile_grid", 4)
+    try:
+        for dim in (128, 64):
+            hc.spmm_hybrid(ws, asg, torch.rand(m, dim, device="cuda") * 2 - 1)
+    finally:
+        _lib.call("hcs_set_tile_grid", 0)
+    torch.cuda.synchronize()
+    print("skewed ok", flush=True)
+
+
 def main():
     torch.cuda.set_device(0)
+    skewed()
     adj = graphgen.cora_shaped(seed=0)
     adj.symmetric = True
     run(gnn.normalize_adj(adj, "gcn"), "c1")
