@@ -167,6 +167,9 @@ constexpr int kScalarZsLd = kFusedMaxDim + 4;  // fused: per-warp window rows in
 #ifndef HCS_SCALAR_U32
 #define HCS_SCALAR_U32 3  // entries in flight per lane group (32-byte vectors)
 #endif
+#ifndef HCS_SCALAR_U16
+#define HCS_SCALAR_U16 6  // entries in flight per lane group (16-byte vectors; C5 sweep: 4/5/6/7/8 -> 7.47/6.51/6.17/6.41/6.96 ms)
+#endif
 #ifndef HCS_SCALAR_MINB
 #define HCS_SCALAR_MINB 3  // resident blocks per SM the register budget is sized for
 #endif
@@ -629,7 +632,7 @@ static int launch_scalar_w(const int64_t* row_ptr, const int32_t* col, const VT*
   const int64_t want = (n_list + kScalarWarps - 1) / kScalarWarps;
   const unsigned grid = (unsigned)std::min<int64_t>(want, (int64_t)num_sms() * (FUSED ? 1 : HCS_SCALAR_MINB));
   const int smem = kScalarWarps * (kScalarCap * 8 + (FUSED ? kFusedMaxRows * kScalarZsLd * 4 : 0));
-  auto k = v32 ? k_spmm_scalar_w<XT, VT, 32, HCS_SCALAR_U32, FUSED> : k_spmm_scalar_w<XT, VT, 16, 4, FUSED>;
+  auto k = v32 ? k_spmm_scalar_w<XT, VT, 32, HCS_SCALAR_U32, FUSED> : k_spmm_scalar_w<XT, VT, 16, HCS_SCALAR_U16, FUSED>;
   HCS_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   k<<<grid, kScalarWarps * 32, smem, st>>>(row_ptr, col, val, n_rows, wh, win_list, n_list, x, dim, ldx, z, ldz, mw,
                                             d_out, out, ldo);
@@ -687,7 +690,10 @@ extern "C" int hcs_spmm_scalar(const int64_t* row_ptr, const int32_t* col_idx, c
     return HCS_OK;
   }
   if (g_scalar_variant != 1 && wh <= 31) {
-    const bool v32 = scalar_v32(x, x_dtype, ldx, dim);
+    // bf16 X in auto mode: 16-B vectors (16 lanes per 256-B row, 2 rows at a time, 6 entries in
+    // flight per lane group) beat 32-B vectors with 3 in flight on C5's 910 K scalar windows:
+    // 6.87-6.99 -> 6.17-6.18 ms (tools/exp_c5.py; the 32-B variant stays as "warp", variant 4)
+    const bool v32 = scalar_v32(x, x_dtype, ldx, dim) && !(g_scalar_variant == 0 && x_dtype == HCS_DTYPE_BF16);
     if (x_dtype == HCS_DTYPE_BF16 && values_dtype == HCS_DTYPE_BF16)
       HCS_TRY(launch_scalar_w<false>(row_ptr, col_idx, (const __nv_bfloat16*)values, n_rows, wh, win_list, n_list,
                                      (const __nv_bfloat16*)x, dim, ldx, z, ldz, v32, st));

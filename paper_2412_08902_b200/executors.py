@@ -816,8 +816,9 @@ def _scalar_variant_auto() -> bool:
 def set_scalar_variant(variant: str = "auto") -> None:
     """Select the CUDA-core (K3) kernel: "auto" (inside a hybrid plan: the piece kernel, one warp
     per <= 32-entry piece of a row, for lists of <= 1,024 windows; through hcs_spmm_scalar
-    directly: "rows" for lists of <= 1,024 windows, else "warp"), "warp" (warp per window, col/val staged in shared memory, 32-byte X vectors when the
-    operand allows), "rows" (warp per row, pairs broadcast by shuffles; small graphs), "block"
+    directly: "rows" for lists of <= 1,024 windows, else the warp-per-window kernel with 16-byte X
+    vectors for bf16 X and 32-byte ones for fp32 X), "warp" (warp per window, col/val staged in
+    shared memory, 32-byte X vectors when the operand allows), "rows" (warp per row, pairs broadcast by shuffles; small graphs), "block"
     (block per window, one warp per row with a fixed shuffle tree), "warp16" (warp per window,
     16-byte vectors)."""
     if variant not in _SCALAR_VARIANTS:
