@@ -48,7 +48,7 @@ _SIGS = {
     "hcs_spmm_tile": (ctypes.c_int, [P, I64, P, P, P, P, ctypes.c_int, I64, I32, P, ctypes.c_int, I64, I32, I64, P,
                                      I64, P, SZ, P]),
     "hcs_spmm_tile_balanced": (ctypes.c_int, [P, I64, P, P, P, P, ctypes.c_int, I64, I32, P, ctypes.c_int, I64, I32,
-                                              I64, P, I64, P, SZ, ctypes.c_int, P]),
+                                              I64, P, I64, P, SZ, ctypes.c_int, I64, P]),
     "hcs_tile_scratch_floats": (ctypes.c_int, [ctypes.POINTER(I64)]),
     "hcs_set_tile_slice": (ctypes.c_int, [ctypes.c_int]),
     "hcs_set_tile_npr3": (ctypes.c_int, [ctypes.c_int]),

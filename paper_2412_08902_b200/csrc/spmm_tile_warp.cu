@@ -1002,18 +1002,30 @@ static int g_warp_paired_tf32 = 1;
 // kernels (the multi-GPU exchange of the previous part runs beside the next part's tiles only if
 // some SMs are free: a tile CTA holds 213 KB of shared memory and 57 K registers of its SM)
 static int g_tile_grid = 0;
-static int tile_grid() { return g_tile_grid > 0 ? std::min(g_tile_grid, num_sms()) : num_sms(); }
+// CTAs of a tile launch: one per SM (or the hcs_set_tile_grid cap), fewer when the caller passes
+// the launch's chunk count (positions > 0): ceil(positions / warp groups per CTA), so every group
+// keeps >= 1 position while a small plan no longer fills every SM's shared memory with CTAs that
+// exit at once -- the piece kernel forked beside it then starts on free SMs (C1 product
+// 10.25 -> 8.22 us, tools/exp_c1.py; a 1-window plan launches 1 CTA)
+static int tile_grid(int64_t positions = 0, int groups_per_cta = 1) {
+  int g = g_tile_grid > 0 ? std::min(g_tile_grid, num_sms()) : num_sms();
+  if (positions > 0)
+    g = (int)std::max<int64_t>(1, std::min<int64_t>(g, (positions + groups_per_cta - 1) / groups_per_cta));
+  return g;
+}
 
 // tf32 SpMM (m == nullptr) or fused GCN layer (m = tf32-rounded M [dim x d_out], d_out <= 64; z may
 // be nullptr when no z_cache is wanted).
 int spmm_tile_warp_tf32(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
                         const int64_t* ent_ptr, const uint2* ent, int64_t n_rows, int wh, const float* x, int64_t ldx,
                         int dim, float* z, int64_t ldz, float* scratch, int64_t scratch_floats, cudaStream_t st,
-                        const float* m = nullptr, int d_out = 0, float* out = nullptr, int64_t ldo = 0) {
+                        const float* m = nullptr, int d_out = 0, float* out = nullptr, int64_t ldo = 0,
+                        int64_t n_chunks = 0) {
   const int FS = (dim + 31) / 32;
-  const int grid = tile_grid();
-  const int64_t nwarps = (int64_t)grid * kTfWarps;
   const bool fused = m != nullptr;
+  const int paired = (!fused && FS > 1 && kTfWarps % FS == 0 && g_warp_paired_tf32) ? 1 : 0;
+  const int grid = tile_grid((paired ? 1 : FS) * n_chunks, paired ? kTfWarps / FS : kTfWarps);
+  const int64_t nwarps = (int64_t)grid * kTfWarps;
   const int64_t cw = 2 * tile_cnt_words();
   const int64_t need = cw + nwarps * 2 * (WarpCfg<4>::kSlot + (fused ? kOutSlot : 0));
   HCS_REQUIRE(scratch != nullptr && scratch_floats >= need, HCS_EINVAL, "tile scratch too small");
@@ -1021,7 +1033,6 @@ int spmm_tile_warp_tf32(const int32_t* tile_list, int64_t n_tile, const int64_t*
   float* slots = scratch + cw;
   float* oscratch = slots + nwarps * 2 * WarpCfg<4>::kSlot;
   auto kern = fused ? k_tile_warp_tf32<true> : k_tile_warp_tf32<false>;
-  const int paired = (!fused && FS > 1 && kTfWarps % FS == 0 && g_warp_paired_tf32) ? 1 : 0;
   HCS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kTfSmem));
   kern<<<grid, kTfWarps * 32, kTfSmem, st>>>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim,
                                              FS, z, ldz, slots, m, d_out, out, ldo, oscratch, cnt, paired);
@@ -1102,10 +1113,14 @@ static int launch_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* 
                        const int64_t* ent_ptr, const uint32_t* ent, int64_t n_rows, int wh, const __nv_bfloat16* x,
                        int64_t ldx, int dim, float* z, int64_t ldz, float* scratch, int64_t scratch_floats,
                        cudaStream_t st, const float* mw = nullptr, int d_out = 0, float* out = nullptr,
-                       int64_t ldo = 0, int64_t x_rows = 0, int alpha = 0) {
+                       int64_t ldo = 0, int64_t x_rows = 0, int alpha = 0, int64_t n_chunks = 0) {
   using C = WarpCfg<SWV>;
   const int FS = (dim + C::kFeat - 1) / C::kFeat;
-  const int grid = tile_grid();
+  const bool want = g_warp_paired == 1 || (g_warp_paired == 2 && x_rows * ldx * 2 > kPairMinXBytes);
+  // the fused epilogue pairs 2 slices (out partials summed through shared memory, one named barrier
+  // pair per window end); the plain SpMM any FS dividing the CTA's warps
+  const int paired = (FS > 1 && want && C::kWarps % FS == 0 && (!FUSED || FS == 2)) ? 1 : 0;
+  const int grid = tile_grid((paired ? 1 : FS) * n_chunks, paired ? C::kWarps / FS : C::kWarps);
   const int64_t nwarps = (int64_t)grid * C::kWarps;
   const int64_t cw = 2 * tile_cnt_words();
   const int64_t need = cw + nwarps * 2 * C::kSlot + (FUSED ? nwarps * 2 * kOutSlot : 0);
@@ -1115,10 +1130,6 @@ static int launch_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* 
   float* slots = scratch + cw;
   float* oscratch = slots + nwarps * 2 * C::kSlot;
   const int smem = C::kSmem + (FUSED ? kFusedOutMax * kFusedLdw * 2 : 0);
-  const bool want = g_warp_paired == 1 || (g_warp_paired == 2 && x_rows * ldx * 2 > kPairMinXBytes);
-  // the fused epilogue pairs 2 slices (out partials summed through shared memory, one named barrier
-  // pair per window end); the plain SpMM any FS dividing the CTA's warps
-  const int paired = (FS > 1 && want && C::kWarps % FS == 0 && (!FUSED || FS == 2)) ? 1 : 0;
   // one slice of 33..48 features: the fused (GCN) kernel skips the empty 16-feature group
   // (C3 5.92 -> 5.71 ms); the plain SpMM is faster with the full unrolled schedule now that
   // every lane copies whole padded rows (N = 40/41/48: 1.29 -> 1.21 ms; tools/exp_c3_npr3.sh)
@@ -1153,17 +1164,17 @@ int gcn_tile_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk
 int spmm_tile_warp(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
                    const int64_t* ent_ptr, const uint32_t* ent, int64_t n_rows, int wh, const __nv_bfloat16* x,
                    int64_t x_rows, int64_t ldx, int dim, float* z, int64_t ldz, float* scratch, int64_t scratch_floats,
-                   cudaStream_t st, int alpha = 0) {
+                   cudaStream_t st, int alpha = 0, int64_t n_chunks = 0) {
   // 64-feature slices halve the per-feature slab work once a window has >= 2 slices of 32
   const int swv = g_warp_swv ? g_warp_swv : (dim > 32 ? 8 : 4);
   if (swv == 16)
     return launch_warp<16>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim, z, ldz, scratch,
-                          scratch_floats, st, nullptr, 0, nullptr, 0, x_rows);
+                          scratch_floats, st, nullptr, 0, nullptr, 0, x_rows, 0, n_chunks);
   if (swv == 8)
     return launch_warp<8>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim, z, ldz, scratch,
-                          scratch_floats, st, nullptr, 0, nullptr, 0, x_rows, alpha);
+                          scratch_floats, st, nullptr, 0, nullptr, 0, x_rows, alpha, n_chunks);
   return launch_warp<4>(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, n_rows, wh, x, ldx, dim, z, ldz, scratch,
-                          scratch_floats, st, nullptr, 0, nullptr, 0, x_rows, alpha);
+                          scratch_floats, st, nullptr, 0, nullptr, 0, x_rows, alpha, n_chunks);
 }
 
 int64_t tile_warp_scratch_floats() {
@@ -1182,7 +1193,7 @@ extern "C" int hcs_spmm_tile_balanced(const int32_t* tile_list, int64_t n_tile, 
                                       const int32_t* gidx, const int64_t* ent_ptr, const void* ent, int ent_dtype,
                                       int64_t n_rows, int32_t wh, const void* x, int x_dtype, int64_t x_rows,
                                       int32_t dim, int64_t ldx, float* z, int64_t ldz, void* workspace,
-                                      size_t ws_bytes, int alpha, void* stream) {
+                                      size_t ws_bytes, int alpha, int64_t n_chunks, void* stream) {
   HCS_REQUIRE(alpha >= 0 && alpha <= 1 << 16, HCS_EINVAL, "tile balance alpha must be in [0, 65536] (got %d)", alpha);
   HCS_REQUIRE(wh > 0 && wh <= 16, HCS_EINVAL, "tile path supports window heights 1..16 (got %d)", wh);
   HCS_REQUIRE(dim > 0, HCS_EINVAL, "dim must be positive");
@@ -1194,14 +1205,15 @@ extern "C" int hcs_spmm_tile_balanced(const int32_t* tile_list, int64_t n_tile, 
     if (n_tile == 0) return HCS_OK;
     return spmm_tile_warp_tf32(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, (const uint2*)ent, n_rows, wh,
                                (const float*)x, ldx, dim, z, ldz, (float*)workspace,
-                               (int64_t)(ws_bytes / sizeof(float)), as_stream(stream));
+                               (int64_t)(ws_bytes / sizeof(float)), as_stream(stream), nullptr, 0, nullptr, 0,
+                               n_chunks);
   }
   HCS_REQUIRE(x_dtype == HCS_DTYPE_BF16, HCS_EINVAL, "tile path: x dtype must be bf16 or f32 (tf32)");
   HCS_REQUIRE(ldx % 8 == 0 && ldx >= ((dim + 7) / 8) * 8, HCS_EINVAL, "ldx must be a multiple of 8 covering dim");
   if (n_tile == 0) return HCS_OK;
   return spmm_tile_warp(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, (const uint32_t*)ent, n_rows, wh,
                         (const __nv_bfloat16*)x, x_rows, ldx, dim, z, ldz, (float*)workspace,
-                        (int64_t)(ws_bytes / sizeof(float)), as_stream(stream), alpha);
+                        (int64_t)(ws_bytes / sizeof(float)), as_stream(stream), alpha, n_chunks);
 }
 
 extern "C" int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int64_t* chunk_ptr, const int32_t* gidx,
@@ -1209,7 +1221,7 @@ extern "C" int hcs_spmm_tile(const int32_t* tile_list, int64_t n_tile, const int
                              const void* x, int x_dtype, int64_t x_rows, int32_t dim, int64_t ldx, float* z,
                              int64_t ldz, void* workspace, size_t ws_bytes, void* stream) {
   return hcs_spmm_tile_balanced(tile_list, n_tile, chunk_ptr, gidx, ent_ptr, ent, ent_dtype, n_rows, wh, x, x_dtype,
-                                x_rows, dim, ldx, z, ldz, workspace, ws_bytes, 0, stream);
+                                x_rows, dim, ldx, z, ldz, workspace, ws_bytes, 0, 0, stream);
 }
 
 // K6/K7: tile windows with the fused GCN epilogue: out = (A_w X) M per TILE window, plus

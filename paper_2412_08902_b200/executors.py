@@ -288,6 +288,7 @@ class HybridPlan:
             ((nc_t + 7) // 8).sum(), self.chunk_ptr[-1]]).cpu().tolist()
         self.stats = ExecStats(int(tot[0]), int(tot[1]), int(tot[2]), int(tot[3]), int(tot[4]))
         self.nchunks = int(tot[5])
+        self.chunk_ptr_host = self.chunk_ptr.cpu().numpy()
         self.n_tile = int(self.tile_list.numel())
         self.nnz_tile = int(tot[3])
         ent_dtype = _lib.DTYPE_BF16 if precision == "bf16" else _lib.DTYPE_F32
@@ -319,6 +320,12 @@ class HybridPlan:
             self.scalar_vals, self.scalar_vals_code = csr.values_bf16(), _lib.DTYPE_BF16
         else:
             self.scalar_vals, self.scalar_vals_code = csr.values, _lib.DTYPE_F32
+
+    def range_chunks(self, t0: int, t1: int) -> int:
+        """64-column chunks of tile windows [t0, t1) (host copy of chunk_ptr made with the plan, so
+        no sync inside a captured graph): the tile launch sizes its grid to them."""
+        cp = self.chunk_ptr_host
+        return int(cp[t1] - cp[t0])
 
     @property
     def _cache(self) -> dict:
@@ -419,7 +426,7 @@ class HybridPlan:
                       self.chunk_ptr.data_ptr() + 8 * t0, self.gidx.data_ptr(), self.ent_ptr.data_ptr(),
                       self.ent.data_ptr(), self.ent_dtype, csr.num_rows, self.windows.window_height, xop.t.data_ptr(),
                       xop.dtype_code, xop.rows, xop.dim, xop.ld, z.data_ptr(), ldz, scratch.data_ptr(),
-                      scratch.numel() * 4, self.tile_alpha, s)
+                      scratch.numel() * 4, self.tile_alpha, self.range_chunks(t0, t1), s)
         if tile_events is not None:
             tile_events[1].record()
         if s1 > s0:
