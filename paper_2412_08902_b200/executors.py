@@ -517,7 +517,10 @@ def get_plan(windows, assignment: Assignment, precision: str) -> HybridPlan:
     import hashlib
 
     dev = windows.csr.device
-    key = (precision, hashlib.sha1(assignment.codes.tobytes()).hexdigest())
+    h = getattr(assignment, "_sha1", None)
+    if h is None:  # one host copy + hash per Assignment object
+        h = assignment._sha1 = hashlib.sha1(assignment.codes.tobytes()).hexdigest()
+    key = (precision, h)
     plan = windows._plans.get(key)
     if plan is None:
         plan = HybridPlan(windows, assignment.device_codes(dev), precision)

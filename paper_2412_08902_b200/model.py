@@ -27,7 +27,6 @@ from __future__ import annotations
 import numpy as np
 import torch
 
-from .executors import Assignment
 from .fused import (FusedLayer, dense_matmul, dense_matmul_bf16, fused_aggregate_update, grad_weight,
                     softmax_xent)
 from .windows import WindowSet
@@ -108,7 +107,7 @@ def gcn_layer(x, w, windows, windows_t=None, assignment=None, precision="bf16", 
     z = A x: the reference's forward), "update_first" (A (x W), UpdateAggregate), or "auto"
     (update first when it narrows the rows, d_out < d_in, on one GPU)."""
     if assignment is None:
-        assignment = Assignment(windows.codes)
+        assignment = windows.assignment()
     if windows_t is None:
         windows_t = backward_windows(windows, shard)
     if shard is not None:
@@ -211,7 +210,7 @@ class Gcn2:
         return [self.w1, self.w2]
 
     def forward(self, x, windows: WindowSet, windows_t=None, precision="bf16", shard=None):
-        asg = Assignment(windows.codes)
+        asg = windows.assignment()
         h = torch.relu(gcn_layer(x, self.w1, windows, windows_t, asg, precision, shard, self.order[0]))
         return gcn_layer(h, self.w2, windows, windows_t, asg, precision, shard, self.order[1])
 
@@ -258,9 +257,9 @@ class Gcn2:
         (tests/test_gpu_gnn.py)."""
         from .executors import spmm_staged
 
-        asg = Assignment(windows.codes)
+        asg = windows.assignment()
         wt = backward_windows(windows) if windows_t is None else windows_t
-        asg_t = asg if wt is windows else Assignment(wt.codes)
+        asg_t = asg if wt is windows else wt.assignment()
         w1, w2 = self.w1.detach(), self.w2.detach()
         h = spmm_staged(windows, asg, dense_matmul_bf16(x, w1))
         h.relu_()

@@ -104,6 +104,19 @@ class WindowSet(Sequence):
         self._host = None
         self._plans = {}
 
+    def assignment(self):
+        """The selector's decisions (codes) as an executors.Assignment, made once per WindowSet with
+        its host copy and plan key, so per-call users (model.Gcn2's explicit epoch) neither copy the
+        codes to the host nor synchronise -- the epoch can be captured in a CUDA graph."""
+        a = getattr(self, "_assignment", None)
+        if a is None:
+            from .executors import Assignment
+
+            a = Assignment(self.codes)
+            _ = a.codes  # host copy now, not inside a later call
+            self._assignment = a
+        return a
+
     # ---------------------------------------------------------------- sizes
     @property
     def num_windows(self) -> int:
