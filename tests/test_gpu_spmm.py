@@ -562,6 +562,34 @@ def test_tile_balanced_ranges_on_skewed_plan(cuda_ok):
             _lib.call("hcs_set_tile_grid", 0)
 
 
+def test_plain_tile_entry_point_matches_plan(cuda_ok):
+    """hcs_spmm_tile (the C-ABI entry INTEGRATION.md binds; HybridPlan launches its
+    hcs_spmm_tile_balanced superset) on a plan's arrays == the plan's own tile launch, bitwise,
+    when neither weighting nor grid sizing changes the warp ranges."""
+    from paper_2412_08902_b200 import _lib
+    from paper_2412_08902_b200.executors import get_plan, stage_operand, _alloc_z
+
+    a = plaw8k_csr()
+    ws = hc.partition(to_hc(a))
+    asg = Assignment.uniform(len(ws), Path.TILE)
+    plan = get_plan(ws, asg, "bf16")
+    assert plan.tile_alpha == 0
+    groups = torch.cuda.get_device_properties(0).multi_processor_count * 4  # 8 warps, paired slices
+    assert plan.nchunks >= groups  # the plan's launch keeps the full grid
+    x = orc.random_dense(a.num_cols, 128, seed=6)
+    xop, _ = stage_operand(x, "bf16", torch.device("cuda"))
+    z1, ldz = _alloc_z(a.num_rows, 128, torch.device("cuda"))
+    z2, _ = _alloc_z(a.num_rows, 128, torch.device("cuda"))
+    plan.run(xop, z1, ldz)
+    scr = plan.new_scratch()
+    _lib.call("hcs_spmm_tile", plan.tile_list.data_ptr(), plan.n_tile, plan.chunk_ptr.data_ptr(), plan.gidx.data_ptr(),
+              plan.ent_ptr.data_ptr(), plan.ent.data_ptr(), plan.ent_dtype, a.num_rows, ws.window_height,
+              xop.t.data_ptr(), xop.dtype_code, xop.rows, xop.dim, xop.ld, z2.data_ptr(), ldz, scr.data_ptr(),
+              scr.numel() * 4, _lib.stream())
+    torch.cuda.synchronize()
+    assert torch.equal(z1[:, :128], z2[:, :128])
+
+
 def test_tile_grid_setter(cuda_ok):
     """hcs_set_tile_grid (SMs left to the NCCL kernels of the multi-GPU exchange): any CTA count gives
     the product to fp32 summation order (different warp ranges), deterministic per grid; the
