@@ -40,13 +40,10 @@ namespace hcs {
 #endif
 // 128-B lines of packed entries past the chunk being loaded that are pulled into L2 one step
 // early, 64-feature slices only (C2 N = 128 2.441 -> 2.404 ms, N = 64 1.200 -> 1.195; N = 32
-// 0.815 -> 0.834, so not there; prefetching the gather indices ahead instead cost +30 %:
-// profiles/r02_exp_c5_tile.txt)
+// 0.815 -> 0.834, so not there; the tf32 kernel +1 %; prefetching the gather indices ahead instead
+// cost +30 %: profiles/r02_exp_c5_tile.txt)
 #ifndef HCS_PLAN_PF_ENTL
 #define HCS_PLAN_PF_ENTL 4
-#endif
-#ifndef HCS_PLAN_PF_TFL
-#define HCS_PLAN_PF_TFL 0  // the same for the tf32 kernel's 8-B entries (lines)
 #endif
 constexpr int kWarpTileStages = 3;   // cp.async ring depth per warp
 constexpr int kWarpSlabBytes = 16 * 64 * 2;
@@ -775,9 +772,6 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
   const uint32_t slab = stage0 + kWarpTileStages * kTfStage;
   uint8_t* slab_p = tsmem + warp * kTfPerWarp + kWarpTileStages * kTfStage;
   const uint64_t keep = policy_evict_last();
-#if HCS_PLAN_PF_TFL > 0
-  const int64_t ent_end = __ldg(ent_ptr + chunk_ptr[T]);
-#endif
   const uint64_t once = policy_evict_first();
   const char* xb = reinterpret_cast<const char*>(x);
   const int64_t ldxb = ldx * 4;
@@ -843,12 +837,6 @@ __global__ void __launch_bounds__(kTfWarps * 32, 1)
       const int64_t i = e0 + lane + 32 * q;
       e[q] = i < e1 ? __ldg(ent + i) : make_uint2(0u, 0u);
     }
-#if HCS_PLAN_PF_TFL > 0
-    {  // entry lines of the next chunks into L2 a step early (16 entries per 128-B line)
-      const int64_t pv = (e1 & ~(int64_t)15) + 16 * lane;
-      if (lane < HCS_PLAN_PF_TFL && pv < ent_end) asm volatile("prefetch.global.L2 [%0];" ::"l"(ent + pv));
-    }
-#endif
   };
 
   int g_a[NI], g_b[NI], g2[NI];
