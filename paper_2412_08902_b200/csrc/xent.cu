@@ -22,9 +22,11 @@ constexpr int kXentThreads = 256;
 constexpr int kXentRows = 4;  // rows per warp and pass
 constexpr float kLog2e = 1.4426950408889634f;
 
+// resident CTAs only (8 per SM): the loss partials the last CTA sums stay few (C3: 7,280 partials
+// read ~28 deep per thread by the last CTA were most of the kernel's 40 us)
 static int xent_grid(int64_t rows) {
   const int64_t per = (kXentThreads / 32) * kXentRows;
-  return (int)std::max<int64_t>(1, std::min<int64_t>((rows + per - 1) / per, 65535));
+  return (int)std::max<int64_t>(1, std::min<int64_t>((rows + per - 1) / per, (int64_t)num_sms() * 8));
 }
 
 __device__ __forceinline__ float warp_max(float v) {
@@ -72,25 +74,42 @@ __global__ void __launch_bounds__(kXentThreads) k_softmax_xent(const float* __re
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t step = (int64_t)gridDim.x * (kXentThreads / 32) * kXentRows;
   float lsum = 0.f;
+  auto group_load = [&](int64_t r, int c0, float (&v)[8], int64_t& lab) {
+    const bool live = r < rows;
+    const float* x = logits + (live ? r : 0) * ld + c0;
+    if (VEC) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (live && c0 + 4 * h < C) q = __ldg(reinterpret_cast<const float4*>(x) + h);
+        v[4 * h] = q.x, v[4 * h + 1] = q.y, v[4 * h + 2] = q.z, v[4 * h + 3] = q.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = (live && c0 + j < C) ? __ldg(x + j) : 0.f;
+    }
+    lab = live ? __ldg(labels + r) : 0;
+  };
+  float nv[8];
+  int64_t nlab = 0;
+  bool have_next = false;
   for (int64_t r0 = ((int64_t)blockIdx.x * (kXentThreads / 32) + warp) * kXentRows; r0 < rows; r0 += step) {
     if (GROUP) {
       const int64_t r = r0 + (lane >> 3);
       const int c0 = (lane & 7) * 8;
       const bool live = r < rows;
-      const float* x = logits + (live ? r : 0) * ld + c0;
       float v[8];
-      if (VEC) {
+      int64_t lab;
+      if (have_next) {  // loaded during the previous row group
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (live && c0 + 4 * h < C) q = __ldg(reinterpret_cast<const float4*>(x) + h);
-          v[4 * h] = q.x, v[4 * h + 1] = q.y, v[4 * h + 2] = q.z, v[4 * h + 3] = q.w;
-        }
+        for (int j = 0; j < 8; ++j) v[j] = nv[j];
+        lab = nlab;
       } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = (live && c0 + j < C) ? __ldg(x + j) : 0.f;
+        group_load(r, c0, v, lab);
       }
-      const int64_t lab = live ? __ldg(labels + r) : 0;
+      // the next row group's loads go out before this group's math
+      have_next = r0 + step < rows;
+      if (have_next) group_load(r + step, c0, nv, nlab);
       float m = -INFINITY;
 #pragma unroll
       for (int j = 0; j < 8; ++j) m = c0 + j < C ? fmaxf(m, v[j]) : m;
@@ -184,15 +203,29 @@ __global__ void __launch_bounds__(kXentThreads) k_softmax_xent(const float* __re
   __syncthreads();
   if (!last) return;
   __threadfence();
+  // thread t: partials t, t + 256, ... (loads batched 8 deep, summed in order); then a fixed tree
   float t = 0.f;
-  for (unsigned i = threadIdx.x; i < gridDim.x; i += kXentThreads) t += __ldcg(partial + i);
+  for (unsigned i0 = threadIdx.x; i0 < gridDim.x; i0 += 8 * kXentThreads) {
+    float pv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const unsigned i = i0 + u * kXentThreads;
+      pv[u] = i < gridDim.x ? __ldcg(partial + i) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t += pv[u];
+  }
   red[threadIdx.x] = t;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    float tot = 0.f;
-    for (int i = 0; i < kXentThreads; ++i) tot += red[i];
-    *loss = tot / (float)rows;
-    *cnt = 0u;  // the workspace is left as it was found (zeroed counter)
+  if (warp == 0) {
+    float w8 = 0.f;
+#pragma unroll
+    for (int i = 0; i < kXentThreads / 32; ++i) w8 += red[lane * (kXentThreads / 32) + i];
+    const float tot = warp_sum(w8);
+    if (lane == 0) {
+      *loss = tot / (float)rows;
+      *cnt = 0u;  // the workspace is left as it was found (zeroed counter)
+    }
   }
 }
 
