@@ -13,6 +13,8 @@
 // Both stage 32-row K slabs with cp.async (2 stages) into padded shared tiles (conflict-free
 // fragment loads) and multiply on mma.sync m16n8k8 tf32 (operands RNA-rounded to tf32, fp32
 // accumulate).  They are HBM-bound at the C3 shapes: grad_W reads K * (M + N) * 4 bytes once.
+#include <type_traits>
+
 #include "common.cuh"
 #include "mma_helpers.cuh"
 
@@ -153,28 +155,38 @@ __global__ void k_gradw_reduce(const float* __restrict__ part, int S, int mtiles
 // C = A B, A [K x M] (lda), B [M x N] (ldb), C [K x N] (ldc).  grid (ceil(K/64), ceil(n_store/64)).
 // BF16OUT: C is bf16 (RNE), multiplied by 1[mask > 0] where mask != nullptr (the ReLU backward of
 // the next aggregation's operand), and columns [N, n_store) are written as zeros (slice padding).
-template <bool VA, bool VB, bool BF16OUT = false>
+// MT = m16 tiles per warp (64 * MT rows per CTA): with MT = 2 each W (B) fragment loaded and
+// rounded from shared memory feeds two MMAs -- the kernel is bound by those shared loads.
+template <bool VA, bool VB, bool BF16OUT = false, int MT = 1>
 __global__ void __launch_bounds__(kDenseThreads) k_gemm_tall(const float* __restrict__ a, int64_t lda,
                                                               const float* __restrict__ b, int64_t ldb, int64_t K,
                                                               int M, int N, void* __restrict__ cv, int64_t ldc,
                                                               const float* __restrict__ mask, int64_t ldm,
                                                               int n_store) {
-  __shared__ __align__(16) float As[2][64][kLdA];
-  __shared__ __align__(16) float Bs[2][kKT][kLdT];
+  constexpr int ROWS = 64 * MT;
+  extern __shared__ __align__(16) float gsm[];
+  float (*As)[ROWS][kLdA] = reinterpret_cast<float (*)[ROWS][kLdA]>(gsm);
+  float (*Bs)[kKT][kLdT] = reinterpret_cast<float (*)[kKT][kLdT]>(gsm + 2 * ROWS * kLdA);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int64_t r0 = (int64_t)blockIdx.x * 64;
+  const int64_t r0 = (int64_t)blockIdx.x * ROWS;
   const int n0 = blockIdx.y * 64;
   const uint64_t pol = policy_evict_first(), keep = policy_evict_last();
-  float acc[8][4];
+  float acc[MT][8][4];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+  for (int m = 0; m < MT; ++m)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[m][i][0] = acc[m][i][1] = acc[m][i][2] = acc[m][i][3] = 0.f;
   auto load = [&](int stage, int k0) {
+#pragma unroll
+    for (int q = 0; q < 4 * MT; ++q) {
+      const int i = tid + q * kDenseThreads;
+      const int ar = i >> 3, ac = (i & 7) * 4;  // A: ROWS rows x 8 chunks
+      ld4<VA>(smem_u32(&As[stage][ar][ac]), a, lda, r0 + ar, K, k0 + ac, M, pol);
+    }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int i = tid + q * kDenseThreads;
-      const int ar = i >> 3, ac = (i & 7) * 4;  // A: 64 rows x 8 chunks
-      ld4<VA>(smem_u32(&As[stage][ar][ac]), a, lda, r0 + ar, K, k0 + ac, M, pol);
       const int br = i >> 4, bc = (i & 15) * 4;  // B: 32 rows x 16 chunks (rows past M zero-filled)
       ld4<VB>(smem_u32(&Bs[stage][br][bc]), b, ldb, k0 + br, M, n0 + bc, N, keep);
     }
@@ -192,17 +204,22 @@ __global__ void __launch_bounds__(kDenseThreads) k_gemm_tall(const float* __rest
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < kKT / 8; ++kk) {
-      const int mr = warp * 16 + g, kc = kk * 8 + t;
-      uint32_t af[4];
-      af[0] = tf32_rna(As[stage][mr][kc]);
-      af[1] = tf32_rna(As[stage][mr + 8][kc]);
-      af[2] = tf32_rna(As[stage][mr][kc + 4]);
-      af[3] = tf32_rna(As[stage][mr + 8][kc + 4]);
+      const int kc = kk * 8 + t;
+      uint32_t af[MT][4];
+#pragma unroll
+      for (int m = 0; m < MT; ++m) {
+        const int mr = warp * 16 * MT + m * 16 + g;
+        af[m][0] = tf32_rna(As[stage][mr][kc]);
+        af[m][1] = tf32_rna(As[stage][mr + 8][kc]);
+        af[m][2] = tf32_rna(As[stage][mr][kc + 4]);
+        af[m][3] = tf32_rna(As[stage][mr + 8][kc + 4]);
+      }
 #pragma unroll
       for (int nt = 0; nt < 8; ++nt) {
         const uint32_t b0 = tf32_rna(Bs[stage][kc][nt * 8 + g]);
         const uint32_t b1 = tf32_rna(Bs[stage][kc + 4][nt * 8 + g]);
-        mma_tf32_1688(acc[nt], af, b0, b1);
+#pragma unroll
+        for (int m = 0; m < MT; ++m) mma_tf32_1688(acc[m][nt], af[m], b0, b1);
       }
     }
     __syncthreads();
@@ -211,18 +228,26 @@ __global__ void __launch_bounds__(kDenseThreads) k_gemm_tall(const float* __rest
   if (BF16OUT) {
     __nv_bfloat16* c = static_cast<__nv_bfloat16*>(cv);
 #pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
     for (int nt = 0; nt < 8; ++nt) {
       const int col = n0 + nt * 8 + 2 * t;  // even; ldc even, n_store even
       if (col >= n_store) continue;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int64_t r = r0 + warp * 16 + g + 8 * h;
+        const int64_t r = r0 + warp * 16 * MT + m * 16 + g + 8 * h;
         if (r >= K) continue;
-        float v0 = col < N ? acc[nt][2 * h] : 0.f, v1 = col + 1 < N ? acc[nt][2 * h + 1] : 0.f;
+        float v0 = col < N ? acc[m][nt][2 * h] : 0.f, v1 = col + 1 < N ? acc[m][nt][2 * h + 1] : 0.f;
         if (mask != nullptr) {
           const float* mp = mask + r * ldm + col;
-          if (col < N && !(__ldg(mp) > 0.f)) v0 = 0.f;
-          if (col + 1 < N && !(__ldg(mp + 1) > 0.f)) v1 = 0.f;
+          if (col + 1 < N && ((ldm & 1) == 0) && (((uintptr_t)mask & 7) == 0)) {  // one 8-B load for the pair
+            const float2 mk = __ldg(reinterpret_cast<const float2*>(mp));
+            if (!(mk.x > 0.f)) v0 = 0.f;
+            if (!(mk.y > 0.f)) v1 = 0.f;
+          } else {
+            if (col < N && !(__ldg(mp) > 0.f)) v0 = 0.f;
+            if (col + 1 < N && !(__ldg(mp + 1) > 0.f)) v1 = 0.f;
+          }
         }
         *reinterpret_cast<__nv_bfloat162*>(c + r * ldc + col) = __floats2bfloat162_rn(v0, v1);
       }
@@ -231,22 +256,30 @@ __global__ void __launch_bounds__(kDenseThreads) k_gemm_tall(const float* __rest
   }
   float* c = static_cast<float*>(cv);
 #pragma unroll
+  for (int m = 0; m < MT; ++m)
+#pragma unroll
   for (int nt = 0; nt < 8; ++nt) {
     const int col = n0 + nt * 8 + 2 * t;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int64_t r = r0 + warp * 16 + g + 8 * h;
+      const int64_t r = r0 + warp * 16 * MT + m * 16 + g + 8 * h;
       if (r >= K) continue;
       float* cp = c + r * ldc + col;
       if (col + 1 < N && ((ldc & 1) == 0)) {
-        *reinterpret_cast<float2*>(cp) = make_float2(acc[nt][2 * h], acc[nt][2 * h + 1]);
+        *reinterpret_cast<float2*>(cp) = make_float2(acc[m][nt][2 * h], acc[m][nt][2 * h + 1]);
       } else {
-        if (col < N) cp[0] = acc[nt][2 * h];
-        if (col + 1 < N) cp[1] = acc[nt][2 * h + 1];
+        if (col < N) cp[0] = acc[m][nt][2 * h];
+        if (col + 1 < N) cp[1] = acc[m][nt][2 * h + 1];
       }
     }
   }
 }
+
+#ifndef HCS_GEMM_MT
+#define HCS_GEMM_MT 2  // m16 tiles per warp of the tall GEMMs (64 * MT rows per CTA)
+#endif
+// dynamic shared memory of k_gemm_tall<..., MT>: the A and B double buffers
+inline int gemm_smem(int mt) { return (2 * 64 * mt * kLdA + 2 * kKT * kLdT) * (int)sizeof(float); }
 
 // rows staged with 16-byte copies need a 16-byte aligned base and a row stride of 4 floats
 static bool vec_ok(const float* p, int64_t ld) { return ((uintptr_t)p & 15) == 0 && ld % 4 == 0; }
@@ -304,12 +337,14 @@ extern "C" int hcs_gemm(const float* a, int64_t lda, const float* b, int64_t ldb
   HCS_REQUIRE(lda >= M && ldb >= N, HCS_EINVAL, "GEMM operands need lda >= M, ldb >= N");
   HCS_REQUIRE(((uintptr_t)a & 3) == 0 && ((uintptr_t)b & 3) == 0, HCS_EINVAL, "GEMM operands must be fp32-aligned");
   if (K == 0) return HCS_OK;
-  const int64_t bx = (K + 63) / 64;
+  constexpr int MT = HCS_GEMM_MT;
+  const int64_t bx = (K + 64 * MT - 1) / (64 * MT);
   HCS_REQUIRE(bx < (1ll << 31), HCS_EINVAL, "too many rows");
   const bool va = vec_ok(a, lda), vb = vec_ok(b, ldb);
-  auto kern = va ? (vb ? k_gemm_tall<true, true> : k_gemm_tall<true, false>)
-                 : (vb ? k_gemm_tall<false, true> : k_gemm_tall<false, false>);
-  kern<<<dim3((unsigned)bx, (N + 63) / 64), kDenseThreads, 0, as_stream(stream)>>>(a, lda, b, ldb, K, M, N, c, ldc,
+  auto kern = va ? (vb ? k_gemm_tall<true, true, false, MT> : k_gemm_tall<true, false, false, MT>)
+                 : (vb ? k_gemm_tall<false, true, false, MT> : k_gemm_tall<false, false, false, MT>);
+  HCS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem(MT)));
+  kern<<<dim3((unsigned)bx, (N + 63) / 64), kDenseThreads, gemm_smem(MT), as_stream(stream)>>>(a, lda, b, ldb, K, M, N, c, ldc,
                                                                                   nullptr, 0, N);
   HCS_LAUNCH_CHECK("k_gemm_tall");
   return HCS_OK;
@@ -329,13 +364,23 @@ extern "C" int hcs_gemm_bf16(const float* a, int64_t lda, const float* b, int64_
   HCS_REQUIRE(mask == nullptr || ld_mask >= N, HCS_EINVAL, "mask needs ld_mask >= N");
   HCS_REQUIRE(((uintptr_t)a & 3) == 0 && ((uintptr_t)b & 3) == 0, HCS_EINVAL, "GEMM operands must be fp32-aligned");
   if (K == 0) return HCS_OK;
-  const int64_t bx = (K + 63) / 64;
-  HCS_REQUIRE(bx < (1ll << 31), HCS_EINVAL, "too many rows");
+  // MT = 2 (two m16 tiles per warp) for the plain GEMMs; the masked one keeps MT = 1 (its epilogue's
+  // mask loads, twice as many per thread at MT = 2, made it slower: 49.6 -> 60.7 us, tools/exp_gemm.py)
   const bool va = vec_ok(a, lda), vb = vec_ok(b, ldb);
-  auto kern = va ? (vb ? k_gemm_tall<true, true, true> : k_gemm_tall<true, false, true>)
-                 : (vb ? k_gemm_tall<false, true, true> : k_gemm_tall<false, false, true>);
-  kern<<<dim3((unsigned)bx, (n_store + 63) / 64), kDenseThreads, 0, as_stream(stream)>>>(a, lda, b, ldb, K, M, N, c,
-                                                                                        ldc, mask, ld_mask, n_store);
+  auto launch = [&](auto mt_tag) -> int {
+    constexpr int MT = decltype(mt_tag)::value;
+    const int64_t bx = (K + 64 * MT - 1) / (64 * MT);
+    HCS_REQUIRE(bx < (1ll << 31), HCS_EINVAL, "too many rows");
+    auto kern = va ? (vb ? k_gemm_tall<true, true, true, MT> : k_gemm_tall<true, false, true, MT>)
+                   : (vb ? k_gemm_tall<false, true, true, MT> : k_gemm_tall<false, false, true, MT>);
+    HCS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm_smem(MT)));
+    kern<<<dim3((unsigned)bx, (n_store + 63) / 64), kDenseThreads, gemm_smem(MT), as_stream(stream)>>>(
+        a, lda, b, ldb, K, M, N, c, ldc, mask, ld_mask, n_store);
+    return HCS_OK;
+  };
+  const int rc = mask != nullptr ? launch(std::integral_constant<int, 1>{})
+                                 : launch(std::integral_constant<int, HCS_GEMM_MT>{});
+  if (rc != HCS_OK) return rc;
   HCS_LAUNCH_CHECK("k_gemm_tall");
   return HCS_OK;
 }
