@@ -59,6 +59,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--sweep-dims", action="store_true", help="also report dims 32/64/128")
     p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--shard-balance", choices=["cost", "nnz"], default="cost",
+                   help="--gpus N > 1: window ranges per rank balanced by the path cost model or by nnz")
     p.add_argument("--gcn-order", choices=["auto", "fused", "update_first"], default="auto",
                    help="C3 layer order (model.gcn_layer): auto = A (X W) where it narrows the rows")
     p.add_argument("--launch-check", action="store_true",
@@ -228,11 +230,21 @@ def make_graph(cfg: str, seed: int, graph: str = "powerlaw"):
     return adj, normalize_adj(adj, "gcn"), name
 
 
-def shard_rows(a, world, rank, wh=16):
-    """Contiguous window range of this rank, balanced by nnz (window boundaries)."""
-    from paper_2412_08902_b200.shard import shard_window_ranges, row_slice
+def shard_rows(a, world, rank, wh=16, balance="cost"):
+    """Contiguous window range of this rank, balanced by the path cost model (shard.window_costs:
+    TILE windows by condensed columns, SCALAR windows by entries; needs the global partition, done
+    once outside the timed region) or by nnz.  Cost balance measured better at every P on C2 and C5
+    (profiles/r02s3_shard_compute.txt: C5 at P = 8, slowest rank 5.25 -> 4.63 ms)."""
+    import paper_2412_08902_b200 as hc
+    from paper_2412_08902_b200.shard import shard_window_ranges, row_slice, window_costs
 
-    ranges = shard_window_ranges(a.row_ptr, a.num_rows, world, wh)
+    cost = None
+    if balance == "cost":
+        wsf = hc.partition(a)
+        cost = window_costs(wsf, hc.classify_windows(hc.default_model(), wsf).codes)
+        del wsf
+        torch.cuda.empty_cache()
+    ranges = shard_window_ranges(a.row_ptr, a.num_rows, world, wh, cost)
     w0, w1 = ranges[rank]
     return row_slice(a, w0 * wh, min(w1 * wh, a.num_rows)), ranges
 
@@ -251,7 +263,7 @@ def run_ours(args):
     t_gen = time.perf_counter() - t0
     n, nnz = a.num_rows, a.nnz
     if world > 1:
-        local_a, ranges = shard_rows(a, world, rank)
+        local_a, ranges = shard_rows(a, world, rank, balance=args.shard_balance)
     else:
         local_a, ranges = a, [(0, -(-n // 16))]
     # ---- preprocessing (K1 partition + selector, K2 plan), timed separately
@@ -560,6 +572,7 @@ def run_ours(args):
             "tile_windows": plan.stats.windows_tile, "scalar_windows": plan.stats.windows_scalar,
             "sum_ncols": sum_ncols, "aggregate_ci": local_a.nnz / max(sum_ncols, 1),
             "parallelism": f"row-window shards x{world}" if world > 1 else "single GPU",
+            "shard_balance": args.shard_balance if world > 1 else None,
             "selector": "reference default (selector_default.json)" if args.selector is None else args.selector,
             "launch": "one CUDA graph per step" if (use_graph and world == 1) else "stream launches",
             "l2_policy": ((f"inputs larger than L2 (tile plan + CSR stream {plan_bytes / 1e9:.2f} GB read once per "
