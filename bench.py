@@ -725,7 +725,14 @@ def run_c3(args):
     n, nnz = a.num_rows, a.nnz
     shard = None
     if world > 1:
-        shard = Shard.from_operator(a, world, rank)
+        cost = None
+        if args.shard_balance == "cost":  # as run_ours: path-cost-balanced window ranges
+            from paper_2412_08902_b200.shard import window_costs
+
+            wsf = hc.partition(a)
+            cost = window_costs(wsf, hc.classify_windows(hc.default_model(), wsf).codes)
+            del wsf
+        shard = Shard.from_operator(a, world, rank, window_cost=cost)
         a_loc = shard.local_operator(a)
     else:
         a_loc = a
