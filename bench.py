@@ -11,12 +11,14 @@ One step = one hybrid SpMM of the whole graph with inputs resident in HBM.  The
 CSR stream (0.69 GB) is larger than L2, so no explicit flush is needed.  Timing:
 CUDA events on the launching stream, barrier + synchronize around the timed
 region, max over ranks.  For N > 1 the row windows are sharded across ranks
-(contiguous ranges balanced by nnz) and each step ends with an NCCL all-gather of
-the output rows (the exchange between GCN layers), i.e. strong scaling.
+(contiguous window ranges balanced by the path cost model, --shard-balance cost|nnz)
+and each step ends with an NCCL all-gather of the output rows (the exchange between
+GCN layers, overlapped in 8 parts), i.e. strong scaling.
 
---impl reference times the reference's CPU algorithm (oracle/ restatement of
-rowwin partition + classify + spmm_hybrid, float32) on the host cores over a
-bounded window sample of the same graph.
+--impl reference times the reference's own CPU implementation (the unmodified rowwin
+from baseline/_ref: partition + classify_windows + spmm_hybrid, float32; the oracle/
+restatement when baseline/_ref is absent) on the host cores over a bounded window
+sample of the same graph.
 """
 
 from __future__ import annotations
