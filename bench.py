@@ -764,7 +764,9 @@ def run_c3(args):
                 model.epoch(x, labels, ws)
             torch.cuda.current_stream().wait_stream(side)
             graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph):
+            # captured on the warm-up stream: its per-stream workspaces already exist, so no
+            # allocation (and no zero-fill node) lands inside the graph
+            with torch.cuda.graph(graph, stream=side):
                 g_loss = model.epoch(x, labels, ws)
             graph.replay()
             torch.cuda.synchronize()
